@@ -1,0 +1,99 @@
+"""ctypes binding of include/exflow_c.h (libexflow_b200.so, built in-tree).
+
+There is deliberately no fallback: if the shared library is missing or was
+built without sm_100a kernels every call raises, so a GPU run can never
+silently go through a CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libexflow_b200.so")
+
+EXF_OK, EXF_RUNTIME, EXF_INVALID, EXF_CUDA, EXF_COMM = 0, 1, 2, 3, 4
+
+
+class ExflowError(RuntimeError):
+    """EXF_RUNTIME: mirrors std::runtime_error / ParseError (CLI exit 1)."""
+
+
+class ExflowInvalidArgument(ValueError):
+    """EXF_INVALID: mirrors std::invalid_argument (CLI exit 2)."""
+
+
+class ExflowCudaError(RuntimeError):
+    """EXF_CUDA: CUDA runtime, launch or kernel fault."""
+
+
+class ExflowCommError(RuntimeError):
+    """EXF_COMM: peer exchange failure or barrier timeout."""
+
+
+_ERRORS = {EXF_RUNTIME: ExflowError, EXF_INVALID: ExflowInvalidArgument,
+           EXF_CUDA: ExflowCudaError, EXF_COMM: ExflowCommError}
+
+
+class SimCounters(C.Structure):
+    _fields_ = [("gpu_local_events", C.c_int64), ("node_local_events", C.c_int64),
+                ("away_from_home_events", C.c_int64), ("coherent_moves", C.c_int64),
+                ("hops_intra_node", C.c_int64), ("hops_inter_node", C.c_int64)]
+
+
+class SimReportC(C.Structure):
+    _fields_ = [("hops_intra_node", C.c_int64), ("hops_inter_node", C.c_int64),
+                ("locality_gpu", C.c_double), ("locality_node", C.c_double),
+                ("p", C.c_double), ("p_star", C.c_double),
+                ("alltoall_count", C.c_int64), ("allgather_count", C.c_int64),
+                ("setup_allgather_count", C.c_int64), ("volume_units", C.c_double),
+                ("estimated_latency", C.c_double)]
+
+
+_VP = C.c_void_p
+_I32, _I64, _D = C.c_int32, C.c_int64, C.c_double
+
+# name -> (restype, argtypes); every symbol declared in include/exflow_c.h
+SIGNATURES = {
+    "exf_last_error": (C.c_char_p, []),
+    "exf_version": (_I32, []),
+    "exf_device_ok": (_I32, []),
+    "exf_count_transitions_workspace_bytes": (_I64, [_I64, _I32, _I32, _I32]),
+    "exf_count_transitions": (C.c_int, [_VP, _I64, _I32, _I32, _I32, _VP, _VP, _VP, _VP]),
+    "exf_count_transitions_host": (C.c_int, [_VP, _I64, _I32, _I32, _I32, _VP, _VP]),
+    "exf_route_replay": (C.c_int, [_VP, _VP, _VP, _I64, _I32, _I32, _I32, _I32, _I32, _VP,
+                                   _VP]),
+    "exf_sim_report_from_counters": (C.c_int, [_VP, _I64, _I32, _I32, _I32, _D, _D, _I32, _I32,
+                                               _VP]),
+    "exf_simulate_host": (C.c_int, [_VP, _I64, _I32, _I32, _VP, _I32, _I32, _D, _D, _I32, _I32,
+                                    _VP, _VP]),
+}
+
+_lib = None
+
+
+def load():
+    """Load libexflow_b200.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} missing: run __graft_entry__.build() (make -C "
+                "paper_2401_08383_b200/csrc); there is no CPU fallback")
+        lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != EXF_OK:
+        msg = load().exf_last_error().decode()
+        raise _ERRORS.get(rc, ExflowError)(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args))

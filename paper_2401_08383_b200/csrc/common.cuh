@@ -1,0 +1,70 @@
+// common.cuh -- shared host/device plumbing for the exflow sm_100a library:
+// status/error propagation for the C-ABI and small device helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "exflow_c.h"
+
+namespace exf {
+
+// Thread-local last-error message behind exf_last_error().
+void set_error(const std::string& msg);
+const std::string& last_error();
+
+struct Status {
+    exf_status code;
+    explicit Status(exf_status c) : code(c) {}
+};
+
+// Returns EXF_INVALID with a message (reference std::invalid_argument).
+inline exf_status invalid(const std::string& msg) {
+    set_error(msg);
+    return EXF_INVALID;
+}
+inline exf_status runtime_err(const std::string& msg) {
+    set_error(msg);
+    return EXF_RUNTIME;
+}
+exf_status cuda_status(cudaError_t err, const char* what);
+
+}  // namespace exf
+
+#define EXF_CUDA_TRY(expr)                                                   \
+    do {                                                                     \
+        cudaError_t _e = (expr);                                             \
+        if (_e != cudaSuccess) return ::exf::cuda_status(_e, #expr);         \
+    } while (0)
+
+#define EXF_TRY(expr)                                                        \
+    do {                                                                     \
+        exf_status _s = (expr);                                              \
+        if (_s != EXF_OK) return _s;                                         \
+    } while (0)
+
+// Launch check: catches configuration errors right after a <<<>>> launch.
+#define EXF_LAUNCH_CHECK(what) EXF_CUDA_TRY(cudaPeekAtLastError())
+
+namespace exf {
+
+__device__ __forceinline__ int4 ld_nc_v4(const void* p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+}  // namespace exf

@@ -1,0 +1,214 @@
+// replay.cu -- routing replay: the per-token, per-layer hot loop of
+// exflow::simulate (proj/src/sim.cpp:110-145), as exact integer counters.
+//
+// One thread follows one token through the L layers (the coherent location is
+// a sequential dependency), token rows are staged through shared memory with
+// coalesced loads (row stride padded to L|1 so per-thread column reads are
+// bank-conflict free), the placement table [L][E] lives in shared memory, and
+// counters are reduced warp -> CTA -> one 64-bit atomic per counter per CTA
+// (integer sums: order-independent, bit-exact).
+// Algorithmic bytes per launch: 4*T*L (+4*T homes when given).
+#include "common.cuh"
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+namespace exf {
+namespace {
+
+constexpr int kReplayThreads = 256;
+
+__global__ void __launch_bounds__(kReplayThreads)
+route_replay_kernel(const int32_t* __restrict__ paths, const int32_t* __restrict__ homes,
+                    const int32_t* __restrict__ assign, int64_t T, int32_t L, int32_t E,
+                    int32_t gpus_per_node, int32_t gpus, int32_t mode,
+                    unsigned long long* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int32_t stride = L | 1;
+    int32_t* s_assign = reinterpret_cast<int32_t*>(smem);
+    int32_t* tile = s_assign + ((L * E + 3) & ~3);
+    __shared__ unsigned long long s_cnt[6];
+
+    for (int32_t i = threadIdx.x; i < L * E; i += blockDim.x) s_assign[i] = assign[i];
+    if (threadIdx.x < 6) s_cnt[threadIdx.x] = 0ull;
+
+    int64_t gl = 0, nl = 0, away = 0, moves = 0, hi = 0, he = 0;
+    const int64_t tiles = (T + kReplayThreads - 1) / kReplayThreads;
+    for (int64_t tile_id = blockIdx.x; tile_id < tiles; tile_id += gridDim.x) {
+        const int64_t t0 = tile_id * kReplayThreads;
+        const int32_t nt = (int32_t)imin64(kReplayThreads, T - t0);
+        const int32_t nints = nt * L;
+        const int32_t* src = paths + t0 * L;
+        __syncthreads();
+        for (int32_t i = threadIdx.x; i < nints; i += blockDim.x) {
+            const int32_t r = i / L;
+            tile[r * stride + (i - r * L)] = __ldg(src + i);
+        }
+        __syncthreads();
+        if ((int32_t)threadIdx.x < nt) {
+            const int64_t t = t0 + threadIdx.x;
+            const int32_t home = homes ? __ldg(homes + t) : (int32_t)(t % gpus);
+            int32_t location = home;
+            const int32_t* p = tile + threadIdx.x * stride;
+            for (int32_t j = 0; j < L; ++j) {
+                const int32_t e = p[j];
+                const int32_t eg = ((unsigned)e < (unsigned)E) ? s_assign[j * E + e] : location;
+                gl += (eg == location);
+                nl += (eg / gpus_per_node == location / gpus_per_node);
+                away += (eg != home);
+                if (eg != location) {
+                    ++moves;
+                    if (mode == 1) {
+                        if (eg / gpus_per_node != location / gpus_per_node) ++he; else ++hi;
+                    }
+                }
+                if (mode == 0 && eg != home) {
+                    if (eg / gpus_per_node != home / gpus_per_node) he += 2; else hi += 2;
+                }
+                location = eg;
+            }
+        }
+    }
+    int64_t v[6] = {gl, nl, away, moves, hi, he};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const int64_t s = warp_sum(v[k]);
+        if ((threadIdx.x & 31) == 0 && s) atomicAdd(&s_cnt[k], (unsigned long long)s);
+    }
+    __syncthreads();
+    if (threadIdx.x < 6 && s_cnt[threadIdx.x])
+        atomicAdd(&out[threadIdx.x], s_cnt[threadIdx.x]);
+}
+
+}  // namespace
+}  // namespace exf
+
+using namespace exf;
+
+extern "C" exf_status exf_route_replay(const int32_t* d_paths, const int32_t* d_homes,
+                                       const int32_t* d_assign, int64_t T, int32_t L, int32_t E,
+                                       int32_t num_nodes, int32_t gpus_per_node, int32_t mode,
+                                       exf_sim_counters* d_out, exf_stream_t stream) {
+    if (num_nodes < 1 || gpus_per_node < 1)
+        return invalid("topology must have at least one node and one GPU per node");
+    if (E < 1 || L < 1 || T < 1) return invalid("replay needs T, L, E >= 1");
+    if (mode != 0 && mode != 1) return invalid("mode must be 0 (vanilla) or 1 (coherent)");
+    if ((int64_t)L * E * 4 + (int64_t)kReplayThreads * (L | 1) * 4 > 200 * 1024)
+        return invalid("placement table too large for the replay kernel");
+    if (!d_paths || !d_assign || !d_out) return invalid("null device pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t smem = (size_t)((L * E + 3) & ~3) * 4 + (size_t)kReplayThreads * (L | 1) * 4;
+    EXF_CUDA_TRY(cudaFuncSetAttribute(route_replay_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    EXF_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(exf_sim_counters), s));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles = (T + kReplayThreads - 1) / kReplayThreads;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 4LL * sms));
+    route_replay_kernel<<<blocks, kReplayThreads, smem, s>>>(
+        d_paths, d_homes, d_assign, T, L, E, gpus_per_node, num_nodes * gpus_per_node, mode,
+        reinterpret_cast<unsigned long long*>(d_out));
+    EXF_LAUNCH_CHECK("route_replay_kernel");
+    return EXF_OK;
+}
+
+extern "C" exf_status exf_sim_report_from_counters(const exf_sim_counters* c, int64_t T,
+                                                   int32_t L, int32_t num_nodes,
+                                                   int32_t gpus_per_node, double intra_cost,
+                                                   double inter_cost, int32_t tokens_per_gpu,
+                                                   int32_t mode, exf_sim_report* out) {
+    if (!c || !out) return invalid("null pointer");
+    if (tokens_per_gpu < 1) return invalid("tokens_per_gpu must be >= 1");
+    const int32_t gpus = num_nodes * gpus_per_node;
+    *out = exf_sim_report{};
+    out->hops_intra_node = c->hops_intra_node;
+    out->hops_inter_node = c->hops_inter_node;
+    const double events = (double)T * L;  // sim.cpp:147-151
+    out->locality_gpu = c->gpu_local_events / events;
+    out->locality_node = c->node_local_events / events;
+    out->p = c->away_from_home_events / events;
+    out->p_star = c->coherent_moves / events;
+    const double g = gpus, n = tokens_per_gpu, l = L;
+    if (mode == 0) {  // sim.cpp:153-157, volume_table1 deepspeed top-1 (:171-191)
+        out->alltoall_count = 2LL * L;
+        out->volume_units = 2.0 * g * n * l * out->p;
+    } else {  // sim.cpp:158-165, exflow top-1
+        out->alltoall_count = L;
+        out->allgather_count = 1;
+        out->setup_allgather_count = 1;
+        out->volume_units = g * n * (l * out->p_star + g);
+    }
+    out->estimated_latency = c->hops_intra_node * intra_cost + c->hops_inter_node * inter_cost;
+    return EXF_OK;
+}
+
+extern "C" exf_status exf_simulate_host(const int32_t* h_paths, int64_t T, int32_t L,
+                                        int32_t E, const int32_t* h_assign, int32_t num_nodes,
+                                        int32_t gpus_per_node, double intra_cost,
+                                        double inter_cost, int32_t tokens_per_gpu, int32_t mode,
+                                        const int32_t* h_homes, exf_sim_report* out) {
+    // validation order follows simulate (proj/src/sim.cpp:78-105)
+    if (E < 1) return invalid("num_experts must be >= 1, got " + std::to_string(E));
+    if (L < 2) return invalid("num_layers must be >= 2, got " + std::to_string(L));
+    if (T < 1) return invalid("trace contains no token paths");
+    for (int64_t i = 0; i < T * (int64_t)L; ++i)
+        if (h_paths[i] < 0 || h_paths[i] >= E)
+            return invalid("expert id out of range [0," + std::to_string(E) + ")");
+    if (num_nodes < 1 || gpus_per_node < 1)
+        return invalid("topology must have at least one node and one GPU per node");
+    if (intra_cost < 0.0 || inter_cost < intra_cost)
+        return invalid("hop costs must satisfy inter >= intra >= 0");
+    if (tokens_per_gpu < 1) return invalid("tokens_per_gpu must be >= 1");
+    const int32_t gpus = num_nodes * gpus_per_node;
+    if (E % gpus != 0)
+        return invalid("num_experts " + std::to_string(E) + " not divisible by total GPUs " +
+                       std::to_string(gpus));
+    const int32_t cap = E / gpus;
+    std::vector<int32_t> load(gpus);
+    for (int32_t j = 0; j < L; ++j) {  // Placement::validate, placement.cpp:434-470
+        std::fill(load.begin(), load.end(), 0);
+        for (int32_t e = 0; e < E; ++e) {
+            const int32_t g = h_assign[j * E + e];
+            if (g < 0 || g >= gpus)
+                return invalid("gpu id " + std::to_string(g) + " out of range [0," +
+                               std::to_string(gpus) + ") at layer " + std::to_string(j));
+            load[g]++;
+        }
+        for (int32_t g = 0; g < gpus; ++g)
+            if (load[g] != cap)
+                return invalid("layer " + std::to_string(j) + " places " + std::to_string(load[g]) +
+                               " experts on gpu " + std::to_string(g) + ", expected " +
+                               std::to_string(cap));
+    }
+    if (h_homes)
+        for (int64_t t = 0; t < T; ++t)
+            if (h_homes[t] < 0 || h_homes[t] >= gpus) return invalid("home gpu out of range");
+    const size_t paths_b = (size_t)T * L * 4, assign_b = (size_t)L * E * 4;
+    const size_t homes_b = h_homes ? (size_t)T * 4 : 0;
+    uint8_t* buf = nullptr;
+    EXF_CUDA_TRY(cudaMalloc(&buf, paths_b + assign_b + homes_b + sizeof(exf_sim_counters) + 64));
+    int32_t* d_paths = reinterpret_cast<int32_t*>(buf);
+    int32_t* d_assign = reinterpret_cast<int32_t*>(buf + paths_b);
+    int32_t* d_homes = h_homes ? reinterpret_cast<int32_t*>(buf + paths_b + assign_b) : nullptr;
+    exf_sim_counters* d_out = reinterpret_cast<exf_sim_counters*>(
+        buf + ((paths_b + assign_b + homes_b + 15) & ~size_t(15)));
+    exf_status st = EXF_OK;
+    exf_sim_counters c{};
+    cudaError_t e = cudaMemcpy(d_paths, h_paths, paths_b, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_assign, h_assign, assign_b, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && h_homes) e = cudaMemcpy(d_homes, h_homes, homes_b, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) st = cuda_status(e, "cudaMemcpy H2D");
+    if (st == EXF_OK)
+        st = exf_route_replay(d_paths, d_homes, d_assign, T, L, E, num_nodes, gpus_per_node, mode,
+                              d_out, nullptr);
+    if (st == EXF_OK) {
+        e = cudaMemcpy(&c, d_out, sizeof(c), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) st = cuda_status(e, "cudaMemcpy D2H counters");
+    }
+    cudaFree(buf);
+    if (st != EXF_OK) return st;
+    return exf_sim_report_from_counters(&c, T, L, num_nodes, gpus_per_node, intra_cost,
+                                        inter_cost, tokens_per_gpu, mode, out);
+}
