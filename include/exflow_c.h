@@ -5,7 +5,7 @@
  * namespace exflow. Each entry point below replaces one
  * reference function (file:line under /root/reference/proj) or adds the model
  * surface the reference leaves out (gate/FFN/collectives: SPEC.md:8, :108,
- * :343). include/exflow/*.hpp restores the reference C++ signatures on top of
+ * :343). The headers in include/exflow/ restore the reference C++ signatures on top of
  * this header; INTEGRATION.md shows the bindings.
  *
  * Conventions
@@ -114,6 +114,64 @@ exf_status exf_simulate_host(const int32_t* h_paths, int64_t T, int32_t L, int32
                              double intra_node_hop_cost, double inter_node_hop_cost,
                              int32_t tokens_per_gpu, int32_t mode, const int32_t* h_homes,
                              exf_sim_report* out);
+
+/* ------------------------------------------------------------------------
+ * Host (CPU) placement table and integer-program placement solver. These
+ * stay on the CPU (BASELINE.json north_star); they consume the GPU
+ * histogram. counts are gap-1 counts [L-1][E][E]; assign is [L][E].
+ * ---------------------------------------------------------------------- */
+typedef struct { /* proj/include/exflow/placement.hpp:106-114 */
+    int32_t restarts;           /* 8 */
+    int64_t max_iters;          /* 0 -> 20000*L */
+    double initial_temperature; /* 0 -> mean positive weight */
+    double cooling;             /* 0.999 */
+    uint64_t seed;
+} exf_anneal_params;
+
+typedef struct { /* proj/include/exflow/placement.hpp:120-130 */
+    char solver[32];
+    double objective;
+    uint64_t seed;
+    int64_t iterations;
+    int32_t restarts;
+    int32_t has_optimality_gap;
+    double optimality_gap;
+    int32_t has_tiers;
+    double inter_node_crossings;
+    double intra_node_crossings;
+    double weighted_cost;
+} exf_solve_report;
+
+/* contiguous_placement, proj/src/placement.cpp:482-502 */
+exf_status exf_contiguous_placement(int32_t E, int32_t L, int32_t num_nodes,
+                                    int32_t gpus_per_node, int32_t* h_assign);
+/* random_placement, proj/src/placement.cpp:504-526 */
+exf_status exf_random_placement(int32_t E, int32_t L, int32_t num_nodes, int32_t gpus_per_node,
+                                uint64_t seed, int32_t* h_assign);
+/* Placement::validate, proj/src/placement.cpp:434-470 */
+exf_status exf_validate_placement(const int32_t* h_assign, int32_t L, int32_t E,
+                                  int32_t num_nodes, int32_t gpus_per_node);
+/* objective_crossings, proj/src/placement.cpp:618-643; level 0 node, 1 gpu */
+exf_status exf_objective_crossings(const int64_t* h_counts, int32_t L, int32_t E, int32_t gap,
+                                   const int32_t* h_assign, int32_t num_nodes,
+                                   int32_t gpus_per_node, int32_t level, double* out);
+/* balanced_assignment_count, proj/src/placement.cpp:645-667 (-1 on bad args) */
+int64_t exf_balanced_assignment_count(int32_t items, int32_t parts, int64_t cap);
+/* solve_exact_dp, proj/src/placement.cpp:684-700 */
+exf_status exf_solve_exact_dp(const int64_t* h_counts, int32_t L, int32_t E, int32_t partitions,
+                              int64_t state_cap, int32_t* h_assign, exf_solve_report* report);
+/* solve_local_search, proj/src/placement.cpp:702-718 */
+exf_status exf_solve_local_search(const int64_t* h_counts, int32_t L, int32_t E,
+                                  int32_t partitions, const exf_anneal_params* params,
+                                  int32_t* h_assign, exf_solve_report* report);
+/* solve_staged, proj/src/placement.cpp:720-821 */
+exf_status exf_solve_staged(const int64_t* h_counts, int32_t L, int32_t E, int32_t num_nodes,
+                            int32_t gpus_per_node, double intra_node_hop_cost,
+                            double inter_node_hop_cost, const exf_anneal_params* params,
+                            int64_t state_cap, int32_t* h_assign, exf_solve_report* report);
+/* generate_markov_trace, proj/src/synth.cpp:30-53 (forced-routing inputs) */
+exf_status exf_generate_markov_trace(int32_t E, int32_t L, int64_t T, double alpha,
+                                     int32_t planted_groups, uint64_t seed, int32_t* h_paths);
 
 #ifdef __cplusplus
 }

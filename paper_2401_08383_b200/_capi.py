@@ -50,6 +50,20 @@ class SimReportC(C.Structure):
                 ("estimated_latency", C.c_double)]
 
 
+class AnnealParamsC(C.Structure):
+    _fields_ = [("restarts", C.c_int32), ("max_iters", C.c_int64),
+                ("initial_temperature", C.c_double), ("cooling", C.c_double),
+                ("seed", C.c_uint64)]
+
+
+class SolveReportC(C.Structure):
+    _fields_ = [("solver", C.c_char * 32), ("objective", C.c_double), ("seed", C.c_uint64),
+                ("iterations", C.c_int64), ("restarts", C.c_int32),
+                ("has_optimality_gap", C.c_int32), ("optimality_gap", C.c_double),
+                ("has_tiers", C.c_int32), ("inter_node_crossings", C.c_double),
+                ("intra_node_crossings", C.c_double), ("weighted_cost", C.c_double)]
+
+
 _VP = C.c_void_p
 _I32, _I64, _D = C.c_int32, C.c_int64, C.c_double
 
@@ -67,6 +81,15 @@ SIGNATURES = {
                                                _VP]),
     "exf_simulate_host": (C.c_int, [_VP, _I64, _I32, _I32, _VP, _I32, _I32, _D, _D, _I32, _I32,
                                     _VP, _VP]),
+    "exf_contiguous_placement": (C.c_int, [_I32, _I32, _I32, _I32, _VP]),
+    "exf_random_placement": (C.c_int, [_I32, _I32, _I32, _I32, C.c_uint64, _VP]),
+    "exf_validate_placement": (C.c_int, [_VP, _I32, _I32, _I32, _I32]),
+    "exf_objective_crossings": (C.c_int, [_VP, _I32, _I32, _I32, _VP, _I32, _I32, _I32, _VP]),
+    "exf_balanced_assignment_count": (_I64, [_I32, _I32, _I64]),
+    "exf_solve_exact_dp": (C.c_int, [_VP, _I32, _I32, _I32, _I64, _VP, _VP]),
+    "exf_solve_local_search": (C.c_int, [_VP, _I32, _I32, _I32, _VP, _VP, _VP]),
+    "exf_solve_staged": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _D, _D, _VP, _I64, _VP, _VP]),
+    "exf_generate_markov_trace": (C.c_int, [_I32, _I32, _I64, _D, _I32, C.c_uint64, _VP]),
 }
 
 _lib = None
