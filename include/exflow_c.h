@@ -173,6 +173,89 @@ exf_status exf_solve_staged(const int64_t* h_counts, int32_t L, int32_t E, int32
 exf_status exf_generate_markov_trace(int32_t E, int32_t L, int64_t T, double alpha,
                                      int32_t planted_groups, uint64_t seed, int32_t* h_paths);
 
+/* ------------------------------------------------------------------------
+ * Context-coherent expert-parallel MoE decode (the model surface the
+ * reference leaves out; protocol of proj/src/sim.cpp:65-71
+ * and :159-162). One handle per rank/GPU. Per MoE layer: fused gate +
+ * top-1 + affinity histogram (kernel 1+5), atomic-free bucketing fused with
+ * the single dispatch exchange over NVLink (kernels 2+3), grouped expert FFN
+ * on tcgen05 (kernel 4); tokens stay on their expert's GPU (no combine).
+ * Per step: context AllGather of the step's token states (kernel 3b).
+ * Tokens: rank r owns home tokens r + G*i, i < tokens_per_gpu (round robin,
+ * sim.cpp:111). x_in is this rank's [B][d] bf16 home tokens; the output is
+ * the [G*B][d] bf16 final states of ALL tokens, indexed by token id.
+ * ---------------------------------------------------------------------- */
+typedef struct exf_model exf_model;
+
+typedef struct { /* in the style of SynthConfig (proj/include/exflow/synth.hpp:13-23) */
+    int32_t num_experts;     /* E (divisible by world_size, <= 64) */
+    int32_t num_layers;      /* L MoE layers (>= 2) */
+    int32_t d_model;         /* d (multiple of 256) */
+    int32_t d_ffn;           /* expert hidden width (multiple of 128) */
+    int32_t top_k;           /* must be 1 (all paper models are top-1) */
+    int32_t tokens_per_gpu;  /* B decode sequences per rank */
+    int32_t world_size;      /* G ranks (<= 8, one node) */
+    int32_t rank;
+    uint64_t seed;           /* weight-init seed */
+    float init_std;          /* expert weight std (0.02) */
+    float gate_affinity;     /* planted inter-layer gate correlation rho in [0,1] */
+} exf_model_config;
+
+/* assign: [L][E] placement table (exf_contiguous_placement = vanilla,
+ * exf_solve_staged = affinity). Allocates weights (generated on device from
+ * the seed; identical for a (layer, expert) on whichever rank holds it). */
+exf_status exf_model_create(const exf_model_config* config, const int32_t* h_assign,
+                            exf_model** out);
+exf_status exf_model_destroy(exf_model* model);
+/* Peer wiring. Multi-process: exchange 64-byte CUDA-IPC handles (e.g. with
+ * torch.distributed) and pass all G of them (own included) in rank order.
+ * Single process emulating G ranks on one GPU: exf_model_connect_local. */
+exf_status exf_model_ipc_handle(exf_model* model, void* h_handle64);
+exf_status exf_model_connect(exf_model* model, const void* h_handles);
+exf_status exf_model_connect_local(exf_model* const* models, int32_t count);
+/* One decode step (L layers + context AllGather) on `stream`, asynchronous.
+ * d_x_in: [B][d] bf16 device pointer. */
+exf_status exf_model_step(exf_model* model, const void* d_x_in, exf_stream_t stream);
+/* Phased form for lock-step emulation of G ranks in one stream:
+ * phase 0 begin(x_in) | 1 gate+dispatch(layer) | 2 ffn(layer) |
+ * 3 gather send | 4 gather wait. */
+exf_status exf_model_step_phase(exf_model* model, int32_t phase, int32_t layer,
+                                const void* d_x_in, exf_stream_t stream);
+/* Device pointer to the [G*B][d] bf16 step output (token-id order). */
+exf_status exf_model_output(exf_model* model, void** d_out);
+/* Forced routing (routes from a trace, e.g. generate_markov_trace): h_routes
+ * is [G*B][L] int32 indexed by token id; NULL disables. */
+exf_status exf_model_set_forced_routes(exf_model* model, const int32_t* h_routes);
+/* Cumulative statistics since the last reset (synchronous):
+ *  routes  [G*B][L] int32: expert of each token at each layer in the LAST
+ *          step (entries of tokens not resident here are -1 unless the
+ *          rank saw them),
+ *  crossed [L] int64: tokens that changed GPU at each layer (this rank's
+ *          outgoing moves; sum over ranks = SimReport coherent moves),
+ *  counts  [L-1][E][E] int64: fused affinity histogram (sum over ranks =
+ *          count_transitions of the emitted trace). */
+exf_status exf_model_read_routes(exf_model* model, int32_t* h_routes);
+exf_status exf_model_read_crossed(exf_model* model, int64_t* h_crossed);
+exf_status exf_affinity_snapshot(exf_model* model, int64_t* h_counts);
+exf_status exf_model_reset_stats(exf_model* model);
+/* Device error word (0 = ok); non-zero after a peer timeout or capacity fault. */
+exf_status exf_model_check(exf_model* model);
+/* Weights of (layer, global expert) if it is placed on this rank:
+ * w1 [dff][d], b1 [dff], w2 [d][dff], b2 [d], bf16 bits. */
+exf_status exf_model_read_expert(exf_model* model, int32_t layer, int32_t expert, uint16_t* h_w1,
+                                 uint16_t* h_b1, uint16_t* h_w2, uint16_t* h_b2);
+exf_status exf_model_read_gate(exf_model* model, int32_t layer, uint16_t* h_wg /* [E][d] */);
+/* Resident tokens of buffer `which` (layer j reads buffer j%2 and writes
+ * (j+1)%2): h_x [n][d] bf16 bits, h_meta [n][2] int32 {token, prev_expert},
+ * *n_out = n. Buffers must hold G*B rows. Synchronous (tests/diagnostics). */
+exf_status exf_model_read_resident(exf_model* model, int32_t which, uint16_t* h_x,
+                                   int32_t* h_meta, int32_t* n_out);
+/* CUDA-graph capture of one full step reading d_x_in; replay launches it. */
+exf_status exf_model_capture(exf_model* model, const void* d_x_in, exf_stream_t stream);
+exf_status exf_model_replay(exf_model* model, exf_stream_t stream);
+/* Kernel launches one step issues (for bench accounting). */
+int32_t exf_model_launches_per_step(exf_model* model);
+
 #ifdef __cplusplus
 }
 #endif

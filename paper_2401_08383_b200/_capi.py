@@ -90,7 +90,34 @@ SIGNATURES = {
     "exf_solve_local_search": (C.c_int, [_VP, _I32, _I32, _I32, _VP, _VP, _VP]),
     "exf_solve_staged": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _D, _D, _VP, _I64, _VP, _VP]),
     "exf_generate_markov_trace": (C.c_int, [_I32, _I32, _I64, _D, _I32, C.c_uint64, _VP]),
+    "exf_model_create": (C.c_int, [_VP, _VP, _VP]),
+    "exf_model_destroy": (C.c_int, [_VP]),
+    "exf_model_ipc_handle": (C.c_int, [_VP, _VP]),
+    "exf_model_connect": (C.c_int, [_VP, _VP]),
+    "exf_model_connect_local": (C.c_int, [_VP, _I32]),
+    "exf_model_step": (C.c_int, [_VP, _VP, _VP]),
+    "exf_model_step_phase": (C.c_int, [_VP, _I32, _I32, _VP, _VP]),
+    "exf_model_output": (C.c_int, [_VP, _VP]),
+    "exf_model_set_forced_routes": (C.c_int, [_VP, _VP]),
+    "exf_model_read_routes": (C.c_int, [_VP, _VP]),
+    "exf_model_read_crossed": (C.c_int, [_VP, _VP]),
+    "exf_affinity_snapshot": (C.c_int, [_VP, _VP]),
+    "exf_model_reset_stats": (C.c_int, [_VP]),
+    "exf_model_check": (C.c_int, [_VP]),
+    "exf_model_read_expert": (C.c_int, [_VP, _I32, _I32, _VP, _VP, _VP, _VP]),
+    "exf_model_read_gate": (C.c_int, [_VP, _I32, _VP]),
+    "exf_model_read_resident": (C.c_int, [_VP, _I32, _VP, _VP, _VP]),
+    "exf_model_capture": (C.c_int, [_VP, _VP, _VP]),
+    "exf_model_replay": (C.c_int, [_VP, _VP]),
+    "exf_model_launches_per_step": (_I32, [_VP]),
 }
+
+
+class ModelConfigC(C.Structure):
+    _fields_ = [("num_experts", C.c_int32), ("num_layers", C.c_int32), ("d_model", C.c_int32),
+                ("d_ffn", C.c_int32), ("top_k", C.c_int32), ("tokens_per_gpu", C.c_int32),
+                ("world_size", C.c_int32), ("rank", C.c_int32), ("seed", C.c_uint64),
+                ("init_std", C.c_float), ("gate_affinity", C.c_float)]
 
 _lib = None
 

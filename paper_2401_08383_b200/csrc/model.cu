@@ -1,0 +1,651 @@
+// model.cu -- exf_model_*: one rank of the context-coherent expert-parallel
+// MoE decode step. Owns weights, the IPC-shared receive region, the resident
+// token buffers and the per-layer launch sequence
+//   gate(+hist) -> dispatch(P2P) -> GEMM1(tcgen05) -> GEMM2(tcgen05)
+// and the per-step context AllGather (gather_send/gather_wait).
+#include "common.cuh"
+#include "exflow/prng.hpp"
+#include "model.cuh"
+#include "ptx.cuh"
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+namespace exf {
+
+exf_status launch_gate(const LayerArgs& a, cudaStream_t s);
+exf_status launch_dispatch(const LayerArgs& a, cudaStream_t s);
+exf_status launch_step_begin(const __nv_bfloat16* x_in, __nv_bfloat16* res_x, ResMeta* res_meta,
+                             int32_t* n_res, int B, int d, int G, int rank, cudaStream_t s);
+exf_status launch_gather_send(const __nv_bfloat16* res_x, const ResMeta* res_meta,
+                              const int32_t* n_res, uint8_t* const* peers, const Symm& sym, int G,
+                              int rank, int d, int C, const uint64_t* step, int32_t* done_ctr,
+                              int32_t* err, cudaStream_t s);
+exf_status launch_gather_wait(uint8_t* own_sym, const Symm& sym, int G, uint64_t* step,
+                              int32_t* err, cudaStream_t s);
+exf_status make_weight_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols);
+
+exf_status launch_ffn_gemm(const CUtensorMap& map, const FfnArgs& a, int nmax, cudaStream_t s);
+
+namespace {
+
+__device__ __forceinline__ uint64_t hmix(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+
+// Deterministic N(0, std^2) from (seed, key, index): Box-Muller on two
+// 53-bit uniforms of a splitmix64 hash chain.
+__device__ __forceinline__ float hnormal(uint64_t seed, uint64_t key, int64_t i) {
+    const uint64_t h1 = hmix(seed ^ hmix(key * 0xD1B54A32D192ED03ULL + (uint64_t)i));
+    const uint64_t h2 = hmix(h1);
+    const double u1 = ((double)(h1 >> 11) + 1.0) * (1.0 / 9007199254740993.0);
+    const double u2 = (double)(h2 >> 11) * (1.0 / 9007199254740992.0);
+    return (float)(sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2));
+}
+
+__global__ void init_normal_kernel(__nv_bfloat16* out, int64_t n, uint64_t seed, uint64_t key,
+                                   float stdv) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = __float2bfloat16(stdv * hnormal(seed, key, i));
+}
+
+// planted inter-layer gate correlation: cur[perm[e]] = rho*prev[e] + sqrt(1-rho^2)*noise
+__global__ void gate_mix_kernel(const __nv_bfloat16* prev, __nv_bfloat16* cur, const int32_t* perm,
+                                int E, int d, float rho, float stdv, uint64_t seed, uint64_t key) {
+    const float beta = sqrtf(fmaxf(0.f, 1.f - rho * rho));
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)E * d;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int e = (int)(i / d), k = (int)(i - (int64_t)e * d);
+        const int64_t dst = (int64_t)perm[e] * d + k;
+        cur[dst] = __float2bfloat16(rho * __bfloat162float(prev[i]) + beta * stdv * hnormal(seed, key, dst));
+    }
+}
+
+uint64_t weight_key(int layer, int expert, int E, int which) {
+    return ((uint64_t)layer * (uint64_t)E + (uint64_t)expert) * 8u + (uint64_t)which + 1u;
+}
+uint64_t gate_key(int layer) { return 0x6A7E000000000000ULL + (uint64_t)layer; }
+
+int pick_ksplit(int units, int K) {
+    int ks = 1;
+    while (ks < 8 && units * ks < 148 && (K / 64) % (ks * 2) == 0 && K / 64 / (ks * 2) >= 2) ks *= 2;
+    return ks;
+}
+
+}  // namespace
+}  // namespace exf
+
+using namespace exf;
+
+struct exf_model {
+    exf_model_config cfg{};
+    int E_loc = 0, C = 0;
+    int device = 0;
+    // placement
+    std::vector<int32_t> assign;            // [L][E]
+    std::vector<std::vector<int>> local;    // [L] -> global experts on this rank (slot order)
+    int32_t* d_gpu_of = nullptr;            // [L][E]
+    int32_t* d_slot_of = nullptr;           // [L][E]
+    // weights
+    __nv_bfloat16* wg = nullptr;            // [L][E][d]
+    __nv_bfloat16* w1 = nullptr;            // [L][E_loc][dff][d]
+    __nv_bfloat16* b1 = nullptr;            // [L][E_loc][dff]
+    __nv_bfloat16* w2 = nullptr;            // [L][E_loc][d][dff]
+    __nv_bfloat16* b2 = nullptr;            // [L][E_loc][d]
+    std::vector<CUtensorMap> tmap1, tmap2;  // per layer
+    // symmetric region
+    Symm sym{};
+    uint8_t* sym_base = nullptr;
+    std::vector<cudaIpcMemHandle_t> peer_handles;
+    std::vector<uint8_t*> peer_ptrs;        // host copy
+    uint8_t** d_peers = nullptr;
+    std::vector<void*> opened;              // IPC-opened peer bases (to close)
+    bool connected = false;
+    // private
+    __nv_bfloat16* res_x[2] = {nullptr, nullptr};
+    ResMeta* res_meta[2] = {nullptr, nullptr};
+    int32_t* n_res = nullptr;               // [2]
+    int32_t* expert = nullptr;
+    float* prob = nullptr;
+    __nv_bfloat16* H = nullptr;
+    unsigned long long* hist = nullptr;     // [L-1][E][E]
+    unsigned long long* crossed = nullptr;  // [L]
+    int32_t* trace = nullptr;               // [C][L]
+    int32_t* forced = nullptr;              // [C][L]
+    bool forced_on = false;
+    uint64_t* step = nullptr;
+    int32_t* err = nullptr;
+    int32_t* done_ctr = nullptr;            // [2] dispatch, gather
+    int nmax = 64;
+    int ks1 = 1, ks2 = 1;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+};
+
+namespace {
+
+template <class T>
+exf_status dalloc(T** p, size_t count) {
+    EXF_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
+    EXF_CUDA_TRY(cudaMemset(*p, 0, std::max<size_t>(count, 1) * sizeof(T)));
+    return EXF_OK;
+}
+
+exf_status validate_config(const exf_model_config& c) {
+    if (c.num_experts < 1 || c.num_experts > 64) return invalid("num_experts must be in [1,64]");
+    if (c.num_layers < 2) return invalid("num_layers must be >= 2, got " + std::to_string(c.num_layers));
+    if (c.d_model < 256 || c.d_model % 256 != 0) return invalid("d_model must be a positive multiple of 256");
+    if (c.d_ffn < 128 || c.d_ffn % 128 != 0) return invalid("d_ffn must be a positive multiple of 128");
+    if (c.top_k != 1) return invalid("only top-1 gating is supported (paper models are top-1)");
+    if (c.tokens_per_gpu < 1) return invalid("tokens_per_gpu must be >= 1");
+    if (c.world_size < 1 || c.world_size > 8) return invalid("world_size must be in [1,8]");
+    if (c.rank < 0 || c.rank >= c.world_size) return invalid("rank out of range");
+    if (c.num_experts % c.world_size != 0)
+        return invalid("num_experts " + std::to_string(c.num_experts) + " not divisible by total GPUs " +
+                       std::to_string(c.world_size));
+    if (!(c.gate_affinity >= 0.f && c.gate_affinity <= 1.f)) return invalid("gate_affinity must be in [0,1]");
+    if ((int64_t)c.tokens_per_gpu * c.world_size > 16384) return invalid("G*B exceeds 16384 tokens");
+    return EXF_OK;
+}
+
+exf_status build_layout(exf_model* m) {
+    const auto& c = m->cfg;
+    const int G = c.world_size, C = m->C, d = c.d_model;
+    int64_t o = 0;
+    auto take = [&](int64_t bytes) {
+        const int64_t at = o;
+        o += (bytes + 255) & ~int64_t(255);
+        return at;
+    };
+    m->sym.recv_x = take(2LL * G * C * d * 2);
+    m->sym.recv_meta = take(2LL * G * C * (int64_t)sizeof(RecvMeta));
+    m->sym.recv_cnt = take(2LL * G * m->E_loc * 4);
+    m->sym.flags = take(2LL * G * 8);
+    m->sym.gather_x = take((int64_t)C * d * 2);
+    m->sym.gflags = take((int64_t)G * 8);
+    m->sym.total = o;
+    EXF_CUDA_TRY(cudaMalloc(&m->sym_base, (size_t)o));
+    EXF_CUDA_TRY(cudaMemset(m->sym_base, 0, (size_t)o));
+    return EXF_OK;
+}
+
+exf_status set_placement(exf_model* m, const int32_t* h_assign) {
+    const auto& c = m->cfg;
+    const int L = c.num_layers, E = c.num_experts, G = c.world_size;
+    std::vector<int> load(G);
+    for (int j = 0; j < L; ++j) {  // Placement::validate (proj/src/placement.cpp:434-470)
+        std::fill(load.begin(), load.end(), 0);
+        for (int e = 0; e < E; ++e) {
+            const int g = h_assign[j * E + e];
+            if (g < 0 || g >= G)
+                return invalid("gpu id " + std::to_string(g) + " out of range [0," + std::to_string(G) +
+                               ") at layer " + std::to_string(j));
+            load[g]++;
+        }
+        for (int g = 0; g < G; ++g)
+            if (load[g] != m->E_loc)
+                return invalid("layer " + std::to_string(j) + " places " + std::to_string(load[g]) +
+                               " experts on gpu " + std::to_string(g) + ", expected " +
+                               std::to_string(m->E_loc));
+    }
+    m->assign.assign(h_assign, h_assign + (size_t)L * E);
+    std::vector<int32_t> slot((size_t)L * E);
+    m->local.assign(L, {});
+    for (int j = 0; j < L; ++j) {
+        std::fill(load.begin(), load.end(), 0);
+        for (int e = 0; e < E; ++e) {
+            const int g = h_assign[j * E + e];
+            slot[j * E + e] = load[g]++;
+            if (g == c.rank) m->local[j].push_back(e);
+        }
+    }
+    EXF_CUDA_TRY(cudaMemcpy(m->d_gpu_of, m->assign.data(), sizeof(int32_t) * L * E, cudaMemcpyHostToDevice));
+    EXF_CUDA_TRY(cudaMemcpy(m->d_slot_of, slot.data(), sizeof(int32_t) * L * E, cudaMemcpyHostToDevice));
+    return EXF_OK;
+}
+
+exf_status init_weights(exf_model* m) {
+    const auto& c = m->cfg;
+    const int L = c.num_layers, E = c.num_experts, d = c.d_model, f = c.d_ffn;
+    const int blocks = 148 * 8;
+    for (int j = 0; j < L; ++j)
+        for (int s = 0; s < m->E_loc; ++s) {
+            const int e = m->local[j][s];
+            const int64_t ls = (int64_t)j * m->E_loc + s;
+            init_normal_kernel<<<blocks, 256>>>(m->w1 + ls * f * d, (int64_t)f * d, c.seed, weight_key(j, e, E, 0), c.init_std);
+            init_normal_kernel<<<blocks, 256>>>(m->b1 + ls * f, f, c.seed, weight_key(j, e, E, 1), c.init_std);
+            init_normal_kernel<<<blocks, 256>>>(m->w2 + ls * d * f, (int64_t)d * f, c.seed, weight_key(j, e, E, 2), c.init_std);
+            init_normal_kernel<<<blocks, 256>>>(m->b2 + ls * d, d, c.seed, weight_key(j, e, E, 3), c.init_std);
+        }
+    // gate: logits ~ N(0,1) for unit-variance inputs; planted affinity with a
+    // hidden per-layer expert permutation
+    const float gstd = 1.0f / std::sqrt((float)d);
+    init_normal_kernel<<<blocks, 256>>>(m->wg, (int64_t)E * d, c.seed, gate_key(0), gstd);
+    int32_t* d_perm = nullptr;
+    EXF_CUDA_TRY(cudaMalloc(&d_perm, sizeof(int32_t) * E));
+    for (int j = 1; j < L; ++j) {
+        std::vector<int> perm(E);
+        std::iota(perm.begin(), perm.end(), 0);
+        exflow::Rng rng(exflow::seed_stream(c.seed, 1000u + (uint64_t)j));
+        exflow::shuffle(std::span<int>(perm), rng);
+        EXF_CUDA_TRY(cudaMemcpy(d_perm, perm.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice));
+        gate_mix_kernel<<<blocks, 256>>>(m->wg + (int64_t)(j - 1) * E * d, m->wg + (int64_t)j * E * d,
+                                         d_perm, E, d, c.gate_affinity, gstd, c.seed, gate_key(j));
+    }
+    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    cudaFree(d_perm);
+    EXF_LAUNCH_CHECK("init kernels");
+    for (int j = 0; j < L; ++j) {
+        EXF_TRY(make_weight_tmap(&m->tmap1[j], m->w1 + (int64_t)j * m->E_loc * f * d, (int64_t)m->E_loc * f, d));
+        EXF_TRY(make_weight_tmap(&m->tmap2[j], m->w2 + (int64_t)j * m->E_loc * d * f, (int64_t)m->E_loc * d, f));
+    }
+    return EXF_OK;
+}
+
+LayerArgs layer_args(exf_model* m, int j) {
+    const auto& c = m->cfg;
+    LayerArgs a{};
+    a.G = c.world_size;
+    a.rank = c.rank;
+    a.E = c.num_experts;
+    a.E_loc = m->E_loc;
+    a.d = c.d_model;
+    a.dff = c.d_ffn;
+    a.C = m->C;
+    a.L = c.num_layers;
+    a.layer = j;
+    a.forced = m->forced_on ? 1 : 0;
+    a.wg = m->wg + (int64_t)j * c.num_experts * c.d_model;
+    a.gpu_of = m->d_gpu_of + j * c.num_experts;
+    a.slot_of = m->d_slot_of + j * c.num_experts;
+    a.res_x_in = m->res_x[j & 1];
+    a.res_meta_in = m->res_meta[j & 1];
+    a.n_res_in = m->n_res + (j & 1);
+    a.expert = m->expert;
+    a.prob = m->prob;
+    a.hist = m->hist;
+    a.crossed = m->crossed;
+    a.trace = m->trace;
+    a.forced_routes = m->forced;
+    a.step = m->step;
+    a.err = m->err;
+    a.done_ctr = m->done_ctr;
+    a.peers = m->d_peers;
+    a.sym = m->sym;
+    a.parity = 0;  // derived on device from the step counter
+    return a;
+}
+
+FfnArgs ffn_args(exf_model* m, int j, int mode) {
+    const auto& c = m->cfg;
+    FfnArgs a{};
+    a.G = c.world_size;
+    a.rank = c.rank;
+    a.E_loc = m->E_loc;
+    a.C = m->C;
+    a.d = c.d_model;
+    a.dff = c.d_ffn;
+    a.K = mode == 0 ? c.d_model : c.d_ffn;
+    a.M_total = mode == 0 ? c.d_ffn : c.d_model;
+    a.ksplit = mode == 0 ? m->ks1 : m->ks2;
+    a.L = c.num_layers;
+    a.layer = j;
+    a.mode = mode;
+    a.own_sym = m->sym_base;
+    a.sym = m->sym;
+    a.step = m->step;
+    a.H = m->H;
+    a.bias = mode == 0 ? m->b1 + (int64_t)j * m->E_loc * c.d_ffn : m->b2 + (int64_t)j * m->E_loc * c.d_model;
+    a.res_x_out = m->res_x[(j + 1) & 1];
+    a.res_meta_out = m->res_meta[(j + 1) & 1];
+    a.n_res_out = m->n_res + ((j + 1) & 1);
+    a.err = m->err;
+    return a;
+}
+
+exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStream_t s) {
+    const auto& c = m->cfg;
+    if (!m->connected) return invalid("model is not connected to its peers (exf_model_connect)");
+    switch (phase) {
+        case 0:
+            if (!x_in) return invalid("null input");
+            return launch_step_begin(static_cast<const __nv_bfloat16*>(x_in), m->res_x[0], m->res_meta[0],
+                                     m->n_res, c.tokens_per_gpu, c.d_model, c.world_size, c.rank, s);
+        case 1: {
+            if (j < 0 || j >= c.num_layers) return invalid("layer out of range");
+            const LayerArgs a = layer_args(m, j);
+            EXF_TRY(launch_gate(a, s));
+            return launch_dispatch(a, s);
+        }
+        case 2: {
+            if (j < 0 || j >= c.num_layers) return invalid("layer out of range");
+            EXF_TRY(launch_ffn_gemm(m->tmap1[j], ffn_args(m, j, 0), m->nmax, s));
+            return launch_ffn_gemm(m->tmap2[j], ffn_args(m, j, 1), m->nmax, s);
+        }
+        case 3: {
+            const int fin = c.num_layers & 1;
+            return launch_gather_send(m->res_x[fin], m->res_meta[fin], m->n_res + fin, m->d_peers, m->sym,
+                                      c.world_size, c.rank, c.d_model, m->C, m->step, m->done_ctr + 1,
+                                      m->err, s);
+        }
+        case 4:
+            return launch_gather_wait(m->sym_base, m->sym, c.world_size, m->step, m->err, s);
+        default:
+            return invalid("unknown phase");
+    }
+}
+
+exf_status run_step(exf_model* m, const void* x_in, cudaStream_t s) {
+    EXF_TRY(run_phase(m, 0, 0, x_in, s));
+    for (int j = 0; j < m->cfg.num_layers; ++j) {
+        EXF_TRY(run_phase(m, 1, j, nullptr, s));
+        EXF_TRY(run_phase(m, 2, j, nullptr, s));
+    }
+    EXF_TRY(run_phase(m, 3, 0, nullptr, s));
+    return run_phase(m, 4, 0, nullptr, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+exf_status exf_model_create(const exf_model_config* config, const int32_t* h_assign, exf_model** out) {
+    if (!config || !h_assign || !out) return invalid("null argument");
+    EXF_TRY(validate_config(*config));
+    auto* m = new exf_model();
+    m->cfg = *config;
+    const auto& c = m->cfg;
+    m->E_loc = c.num_experts / c.world_size;
+    m->C = c.tokens_per_gpu * c.world_size;
+    cudaGetDevice(&m->device);
+    const int L = c.num_layers, E = c.num_experts, d = c.d_model, f = c.d_ffn, C = m->C;
+    auto fail = [&](exf_status st) {
+        exf_model_destroy(m);
+        return st;
+    };
+    exf_status st = EXF_OK;
+#define EXF_M(expr)                         \
+    do {                                    \
+        st = (expr);                        \
+        if (st != EXF_OK) return fail(st);  \
+    } while (0)
+    EXF_M(dalloc(&m->d_gpu_of, (size_t)L * E));
+    EXF_M(dalloc(&m->d_slot_of, (size_t)L * E));
+    EXF_M(set_placement(m, h_assign));
+    EXF_M(dalloc(&m->wg, (size_t)L * E * d));
+    EXF_M(dalloc(&m->w1, (size_t)L * m->E_loc * f * d));
+    EXF_M(dalloc(&m->b1, (size_t)L * m->E_loc * f));
+    EXF_M(dalloc(&m->w2, (size_t)L * m->E_loc * d * f));
+    EXF_M(dalloc(&m->b2, (size_t)L * m->E_loc * d));
+    m->tmap1.resize(L);
+    m->tmap2.resize(L);
+    for (int i = 0; i < 2; ++i) {
+        EXF_M(dalloc(&m->res_x[i], (size_t)C * d));
+        EXF_M(dalloc(&m->res_meta[i], (size_t)C));
+    }
+    EXF_M(dalloc(&m->n_res, 2));
+    EXF_M(dalloc(&m->expert, (size_t)C));
+    EXF_M(dalloc(&m->prob, (size_t)C));
+    EXF_M(dalloc(&m->H, (size_t)C * f));
+    EXF_M(dalloc(&m->hist, (size_t)(L - 1) * E * E));
+    EXF_M(dalloc(&m->crossed, (size_t)L));
+    EXF_M(dalloc(&m->trace, (size_t)C * L));
+    EXF_M(dalloc(&m->forced, (size_t)C * L));
+    EXF_M(dalloc(&m->step, 1));
+    EXF_M(dalloc(&m->err, 1));
+    EXF_M(dalloc(&m->done_ctr, 2));
+    EXF_M(dalloc(&m->d_peers, (size_t)c.world_size));
+    EXF_M(build_layout(m));
+    if (cudaMemset(m->trace, 0xff, sizeof(int32_t) * C * L) != cudaSuccess) return fail(EXF_CUDA);
+    EXF_M(init_weights(m));
+    // tile policy: token tile from the expected tokens per expert, split-K to fill 148 SMs
+    m->nmax = (2 * C / E <= 64) ? 64 : 128;
+    m->ks1 = pick_ksplit(m->E_loc * (f / 128), d);
+    m->ks2 = pick_ksplit(m->E_loc * (d / 128), f);
+    if (c.world_size == 1) {  // a single rank is its own peer
+        exf_model* self = m;
+        EXF_M(exf_model_connect_local(&self, 1));
+    }
+#undef EXF_M
+    *out = m;
+    return EXF_OK;
+}
+
+exf_status exf_model_destroy(exf_model* m) {
+    if (!m) return EXF_OK;
+    if (m->graph_exec) cudaGraphExecDestroy(m->graph_exec);
+    if (m->graph) cudaGraphDestroy(m->graph);
+    for (void* p : m->opened) cudaIpcCloseMemHandle(p);
+    void* bufs[] = {m->d_gpu_of, m->d_slot_of, m->wg, m->w1, m->b1, m->w2, m->b2, m->res_x[0],
+                    m->res_x[1], m->res_meta[0], m->res_meta[1], m->n_res, m->expert, m->prob, m->H,
+                    m->hist, m->crossed, m->trace, m->forced, m->step, m->err, m->done_ctr,
+                    m->d_peers, m->sym_base};
+    for (void* p : bufs)
+        if (p) cudaFree(p);
+    delete m;
+    return EXF_OK;
+}
+
+exf_status exf_model_ipc_handle(exf_model* m, void* h_handle64) {
+    if (!m || !h_handle64) return invalid("null argument");
+    cudaIpcMemHandle_t h;
+    EXF_CUDA_TRY(cudaIpcGetMemHandle(&h, m->sym_base));
+    static_assert(sizeof(h) == 64, "IPC handle is 64 bytes");
+    std::memcpy(h_handle64, &h, 64);
+    return EXF_OK;
+}
+
+exf_status exf_model_connect(exf_model* m, const void* h_handles) {
+    if (!m || !h_handles) return invalid("null argument");
+    const int G = m->cfg.world_size;
+    m->peer_ptrs.assign(G, nullptr);
+    for (int p = 0; p < G; ++p) {
+        if (p == m->cfg.rank) {
+            m->peer_ptrs[p] = m->sym_base;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const uint8_t*>(h_handles) + 64 * p, 64);
+        void* ptr = nullptr;
+        const cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            set_error(std::string("cudaIpcOpenMemHandle(rank ") + std::to_string(p) + "): " + cudaGetErrorString(e));
+            return EXF_COMM;
+        }
+        m->opened.push_back(ptr);
+        m->peer_ptrs[p] = static_cast<uint8_t*>(ptr);
+    }
+    EXF_CUDA_TRY(cudaMemcpy(m->d_peers, m->peer_ptrs.data(), sizeof(uint8_t*) * G, cudaMemcpyHostToDevice));
+    m->connected = true;
+    return EXF_OK;
+}
+
+exf_status exf_model_connect_local(exf_model* const* models, int32_t count) {
+    if (!models || count < 1) return invalid("null argument");
+    for (int i = 0; i < count; ++i) {
+        if (!models[i] || models[i]->cfg.world_size != count || models[i]->cfg.rank != i)
+            return invalid("connect_local needs the G models of ranks 0..G-1 in order");
+        if (models[i]->sym.total != models[0]->sym.total) return invalid("models disagree on layout");
+    }
+    std::vector<uint8_t*> ptrs(count);
+    for (int i = 0; i < count; ++i) ptrs[i] = models[i]->sym_base;
+    for (int i = 0; i < count; ++i) {
+        models[i]->peer_ptrs = ptrs;
+        EXF_CUDA_TRY(cudaMemcpy(models[i]->d_peers, ptrs.data(), sizeof(uint8_t*) * count, cudaMemcpyHostToDevice));
+        models[i]->connected = true;
+    }
+    return EXF_OK;
+}
+
+exf_status exf_model_step(exf_model* m, const void* d_x_in, exf_stream_t stream) {
+    if (!m) return invalid("null model");
+    return run_step(m, d_x_in, static_cast<cudaStream_t>(stream));
+}
+
+exf_status exf_model_step_phase(exf_model* m, int32_t phase, int32_t layer, const void* d_x_in,
+                                exf_stream_t stream) {
+    if (!m) return invalid("null model");
+    return run_phase(m, phase, layer, d_x_in, static_cast<cudaStream_t>(stream));
+}
+
+exf_status exf_model_output(exf_model* m, void** d_out) {
+    if (!m || !d_out) return invalid("null argument");
+    *d_out = m->sym_base + m->sym.gather_x;
+    return EXF_OK;
+}
+
+exf_status exf_model_set_forced_routes(exf_model* m, const int32_t* h_routes) {
+    if (!m) return invalid("null model");
+    if (!h_routes) {
+        m->forced_on = false;
+        return EXF_OK;
+    }
+    const int64_t n = (int64_t)m->C * m->cfg.num_layers;
+    for (int64_t i = 0; i < n; ++i)
+        if (h_routes[i] < 0 || h_routes[i] >= m->cfg.num_experts)
+            return invalid("expert id out of range [0," + std::to_string(m->cfg.num_experts) + ")");
+    EXF_CUDA_TRY(cudaMemcpy(m->forced, h_routes, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    m->forced_on = true;
+    return EXF_OK;
+}
+
+exf_status exf_model_read_routes(exf_model* m, int32_t* h_routes) {
+    if (!m || !h_routes) return invalid("null argument");
+    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    EXF_CUDA_TRY(cudaMemcpy(h_routes, m->trace, sizeof(int32_t) * m->C * m->cfg.num_layers, cudaMemcpyDeviceToHost));
+    return EXF_OK;
+}
+
+exf_status exf_model_read_crossed(exf_model* m, int64_t* h) {
+    if (!m || !h) return invalid("null argument");
+    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    EXF_CUDA_TRY(cudaMemcpy(h, m->crossed, sizeof(int64_t) * m->cfg.num_layers, cudaMemcpyDeviceToHost));
+    return EXF_OK;
+}
+
+exf_status exf_affinity_snapshot(exf_model* m, int64_t* h_counts) {
+    if (!m || !h_counts) return invalid("null argument");
+    const int E = m->cfg.num_experts;
+    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    EXF_CUDA_TRY(cudaMemcpy(h_counts, m->hist, sizeof(int64_t) * (m->cfg.num_layers - 1) * E * E,
+                            cudaMemcpyDeviceToHost));
+    return EXF_OK;
+}
+
+exf_status exf_model_reset_stats(exf_model* m) {
+    if (!m) return invalid("null model");
+    const int E = m->cfg.num_experts, L = m->cfg.num_layers;
+    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    EXF_CUDA_TRY(cudaMemset(m->hist, 0, sizeof(int64_t) * (L - 1) * E * E));
+    EXF_CUDA_TRY(cudaMemset(m->crossed, 0, sizeof(int64_t) * L));
+    EXF_CUDA_TRY(cudaMemset(m->trace, 0xff, sizeof(int32_t) * m->C * L));
+    return EXF_OK;
+}
+
+exf_status exf_model_check(exf_model* m) {
+    if (!m) return invalid("null model");
+    const cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_status(e, "model step");
+    int32_t code = 0;
+    EXF_CUDA_TRY(cudaMemcpy(&code, m->err, 4, cudaMemcpyDeviceToHost));
+    if (code == ERR_TIMEOUT_DISPATCH || code == ERR_TIMEOUT_GATHER) {
+        set_error("peer exchange timed out (code " + std::to_string(code) + ")");
+        return EXF_COMM;
+    }
+    if (code != 0) {
+        set_error("device error code " + std::to_string(code));
+        return EXF_RUNTIME;
+    }
+    return EXF_OK;
+}
+
+exf_status exf_model_read_expert(exf_model* m, int32_t layer, int32_t expert, uint16_t* h_w1,
+                                 uint16_t* h_b1, uint16_t* h_w2, uint16_t* h_b2) {
+    if (!m) return invalid("null model");
+    const auto& c = m->cfg;
+    if (layer < 0 || layer >= c.num_layers || expert < 0 || expert >= c.num_experts)
+        return invalid("layer/expert out of range");
+    const auto& loc = m->local[layer];
+    const auto it = std::find(loc.begin(), loc.end(), expert);
+    if (it == loc.end()) return invalid("expert is not placed on this rank");
+    const int64_t ls = (int64_t)layer * m->E_loc + (it - loc.begin());
+    const int64_t d = c.d_model, f = c.d_ffn;
+    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    if (h_w1) EXF_CUDA_TRY(cudaMemcpy(h_w1, m->w1 + ls * f * d, f * d * 2, cudaMemcpyDeviceToHost));
+    if (h_b1) EXF_CUDA_TRY(cudaMemcpy(h_b1, m->b1 + ls * f, f * 2, cudaMemcpyDeviceToHost));
+    if (h_w2) EXF_CUDA_TRY(cudaMemcpy(h_w2, m->w2 + ls * d * f, f * d * 2, cudaMemcpyDeviceToHost));
+    if (h_b2) EXF_CUDA_TRY(cudaMemcpy(h_b2, m->b2 + ls * d, d * 2, cudaMemcpyDeviceToHost));
+    return EXF_OK;
+}
+
+exf_status exf_model_read_gate(exf_model* m, int32_t layer, uint16_t* h_wg) {
+    if (!m || !h_wg) return invalid("null argument");
+    if (layer < 0 || layer >= m->cfg.num_layers) return invalid("layer out of range");
+    const int64_t n = (int64_t)m->cfg.num_experts * m->cfg.d_model;
+    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    EXF_CUDA_TRY(cudaMemcpy(h_wg, m->wg + layer * n, n * 2, cudaMemcpyDeviceToHost));
+    return EXF_OK;
+}
+
+exf_status exf_model_read_resident(exf_model* m, int32_t which, uint16_t* h_x, int32_t* h_meta,
+                                   int32_t* n_out) {
+    if (!m || !n_out || which < 0 || which > 1) return invalid("bad argument");
+    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    int32_t n = 0;
+    EXF_CUDA_TRY(cudaMemcpy(&n, m->n_res + which, 4, cudaMemcpyDeviceToHost));
+    if (n < 0 || n > m->C) return runtime_err("resident count out of range");
+    if (h_x) EXF_CUDA_TRY(cudaMemcpy(h_x, m->res_x[which], (size_t)n * m->cfg.d_model * 2, cudaMemcpyDeviceToHost));
+    if (h_meta) EXF_CUDA_TRY(cudaMemcpy(h_meta, m->res_meta[which], (size_t)n * sizeof(ResMeta), cudaMemcpyDeviceToHost));
+    *n_out = n;
+    return EXF_OK;
+}
+
+exf_status exf_model_capture(exf_model* m, const void* d_x_in, exf_stream_t stream) {
+    if (!m) return invalid("null model");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!s) return invalid("graph capture needs a non-default stream");
+    if (m->graph_exec) {
+        cudaGraphExecDestroy(m->graph_exec);
+        m->graph_exec = nullptr;
+    }
+    if (m->graph) {
+        cudaGraphDestroy(m->graph);
+        m->graph = nullptr;
+    }
+    EXF_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    const exf_status st = run_step(m, d_x_in, s);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(s, &g);
+    if (st != EXF_OK) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+    }
+    EXF_CUDA_TRY(e);
+    m->graph = g;
+    EXF_CUDA_TRY(cudaGraphInstantiate(&m->graph_exec, g, 0));
+    return EXF_OK;
+}
+
+exf_status exf_model_replay(exf_model* m, exf_stream_t stream) {
+    if (!m || !m->graph_exec) return invalid("no captured graph (exf_model_capture)");
+    EXF_CUDA_TRY(cudaGraphLaunch(m->graph_exec, static_cast<cudaStream_t>(stream)));
+    return EXF_OK;
+}
+
+int32_t exf_model_launches_per_step(exf_model* m) {
+    if (!m) return 0;
+    return 1 + 4 * m->cfg.num_layers + 2;
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// model.cuh -- device data layout of one rank of the ExFlow MoE decode step.
+//
+// HBM layout per rank (G ranks, B home tokens per rank, C = G*B capacity):
+//  symmetric region (one cudaMalloc, IPC-shared, identical offsets on every rank)
+//    recv_x    [2 parity][G src][C][d]   bf16  tokens dispatched to this rank
+//    recv_meta [2][G][C]                 RecvMeta {token, expert, prob}
+//    recv_cnt  [2][G][E_loc]             int32 per-(src, local expert) counts
+//    flags     [2][G]                    u64   dispatch epoch per src
+//    gather_x  [C][d]                    bf16  context AllGather output (by token id)
+//    gflags    [G]                       u64   AllGather epoch per src
+//  private
+//    res_x[2][C][d], res_meta[2][C], n_res[2]  resident tokens (ping-pong)
+//    expert[C], prob[C]                         gate outputs
+//    H[C][dff]                                  FFN hidden (canonical order)
+//    weights: Wg[L][E][d]; W1[L][E_loc][dff][d]; b1[L][E_loc][dff];
+//             W2[L][E_loc][d][dff]; b2[L][E_loc][d]       (all bf16)
+//    gpu_of/slot_of [L][E], hist[L-1][E][E] i64, crossed[L] i64,
+//    trace[C][L] i32 (token-id indexed), step counter, error word
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+namespace exf {
+
+struct RecvMeta {
+    int32_t token;   // global token id (home rank = token % G)
+    int32_t expert;  // global expert id chosen at this layer
+    float prob;      // softmax probability of that expert (output scale)
+    int32_t pad;
+};
+
+struct ResMeta {
+    int32_t token;
+    int32_t prev_expert;  // expert of the previous layer (-1 before layer 0)
+};
+
+struct Symm {  // byte offsets inside the symmetric region
+    int64_t recv_x, recv_meta, recv_cnt, flags, gather_x, gflags, total;
+};
+
+// Everything a kernel needs, passed by value.
+struct LayerArgs {
+    int32_t G, rank, E, E_loc, d, dff, C, L, layer, forced;
+    // rank-local
+    const __nv_bfloat16* wg;        // [E][d] of this layer
+    const int32_t* gpu_of;          // [E] of this layer
+    const int32_t* slot_of;         // [E] of this layer
+    __nv_bfloat16* res_x_in;        // [C][d]
+    const ResMeta* res_meta_in;     // [C]
+    const int32_t* n_res_in;        // device scalar
+    int32_t* expert;                // [C]
+    float* prob;                    // [C]
+    unsigned long long* hist;       // [L-1][E][E] (nullptr -> no fused histogram)
+    unsigned long long* crossed;    // [L]
+    int32_t* trace;                 // [C][L] token-id indexed (nullptr -> off)
+    const int32_t* forced_routes;   // [C][L] token-id indexed forced experts
+    const uint64_t* step;           // device step counter
+    int32_t* err;
+    int32_t* done_ctr;              // last-CTA-done counter for dispatch
+    // peers' symmetric regions (index = rank), and this layer's parity
+    uint8_t* const* peers;          // device array [G]
+    Symm sym;
+    int32_t parity;
+};
+
+// Arguments of one grouped-FFN GEMM launch (ffn_tcgen05.cu).
+struct FfnArgs {
+    int32_t G, rank, E_loc, C, d, dff, K, M_total, ksplit, L, layer, mode;
+    uint8_t* own_sym;
+    Symm sym;
+    const uint64_t* step;
+    __nv_bfloat16* H;            // [C][dff]
+    const __nv_bfloat16* bias;   // [E_loc][M_total] of this layer
+    __nv_bfloat16* res_x_out;    // [C][d]  (GEMM2)
+    ResMeta* res_meta_out;       // [C]     (GEMM2)
+    int32_t* n_res_out;          //         (GEMM2)
+    int32_t* err;
+};
+
+__host__ __device__ inline int64_t bytes_bf16(int64_t n) { return n * 2; }
+
+// error codes written to the device error word before a trap
+enum : int {
+    ERR_NONE = 0,
+    ERR_TIMEOUT_DISPATCH = 1,
+    ERR_TIMEOUT_GATHER = 2,
+    ERR_TIMEOUT_PIPE = 3,
+    ERR_CAPACITY = 4,
+    ERR_BAD_EXPERT = 5,
+};
+
+}  // namespace exf
