@@ -29,9 +29,16 @@ def slots_of(assign_row: np.ndarray, G: int) -> np.ndarray:
     return slot
 
 
-def route(x_bits: np.ndarray, wg: np.ndarray):
+def route(x_bits: np.ndarray, wg: np.ndarray, forced=None):
+    """Gate routing; with `forced` expert ids the decision is overridden and the
+    scale is the softmax probability of the forced expert."""
     logits = orc.gate_logits(x_bits, wg)
-    return orc.gate_top1(logits)
+    if forced is None:
+        return orc.gate_top1(logits)
+    e = np.asarray(forced, np.int32)
+    z = np.exp(logits.astype(np.float64) - logits.max(axis=1, keepdims=True))
+    p = (z[np.arange(len(e)), e] / z.sum(axis=1)).astype(np.float32)
+    return e, p
 
 
 def dispatch(resident, experts, assign_row, G):
