@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Bench: ExFlow context-coherent MoE decode on B200 (BASELINE.json configs[1]).
+
+One step = one decode step of the GPT-MoE 350M-class stack (24 MoE layers,
+8 experts top-1, d_model 1024, d_ffn 4096) over B synthetic tokens per GPU:
+per layer fused gate+top-1+affinity histogram, atomic-free bucketing fused
+with the single P2P dispatch exchange, tcgen05 grouped expert FFN; per step
+the context AllGather. Random-init weights (seeded, N(0, 0.02^2)) with a
+planted inter-layer gate affinity, synthetic N(0,1) tokens.
+
+  python bench.py [--gpus N --steps K --warmup W]           # our arm
+  torchrun --nproc-per-node N bench.py --gpus N ...          # N > 1
+  python bench.py --impl reference ...                       # CPU reference arm
+
+Prints ONE JSON line (rank 0). Weights (24 x 8 x 16.8 MB at N=1) exceed the
+126 MB L2, so every step streams them from HBM ("inputs larger than L2").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE inference tokens/s at 1/2/4/8 B200; cross-GPU routed-token fraction"
+UNIT = "tokens/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--batch", type=int, default=64, help="decode tokens per GPU")
+    p.add_argument("--experts", type=int, default=8)
+    p.add_argument("--layers", type=int, default=24)
+    p.add_argument("--d-model", type=int, default=1024)
+    p.add_argument("--d-ffn", type=int, default=4096)
+    p.add_argument("--gate-affinity", type=float, default=0.8)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def workload(a, n):
+    return {"workload": "GPT-MoE 350M-class decode (BASELINE configs[1])",
+            "model": "gpt-moe-350m-e8", "num_layers": a.layers, "num_experts": a.experts,
+            "top_k": 1, "d_model": a.d_model, "d_ffn": a.d_ffn,
+            "tokens_per_gpu": a.batch, "global_batch": a.batch * n, "seq_len": 1,
+            "parallelism": f"ep{n} context-coherent (1 dispatch exchange/layer, no combine)",
+            "experts_per_gpu": a.experts // n, "l2_policy": "weights > L2 (streamed every step)"}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[0]) for r in rows if len(r) >= 7 and r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 7 and r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) < 7:
+                continue
+            for k, nm in enumerate(names):
+                if r[3 + k].strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(a, rank, n):
+    """CPU arm: the reference's own CPU path (count_transitions + coherent
+    simulate, C restatement) plus the CPU port of the gate/FFN it lacks, on
+    all host cores, same config/metric/unit as our arm."""
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import cpu_path, oracle as orc
+    assign = orc.contiguous_placement(a.experts, a.layers, n)
+    tokens = a.batch * n
+    layers_sample = 2
+    tps, dt, sample, threads = cpu_path.time_cpu_path(a.experts, a.layers, a.d_model, a.d_ffn,
+                                                      tokens, n, assign, layers_sample,
+                                                      max(1, a.steps // 4))
+    routes = orc.generate_markov_trace(a.experts, a.layers, 1 << 18, 0.8, 4, 1)
+    routing_tps = cpu_path.time_reference_routing(routes, a.experts, assign, n, threads)
+    line = {"impl": "reference", "metric": METRIC, "value": tps, "unit": UNIT, "n_gpus": n,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": tokens / tps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": workload(a, n),
+            "cpu_baseline": {"value": tps, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": sample},
+            "reference_routing_only": {"value": routing_tps, "unit": UNIT, "cores": threads,
+                                       "what": "count_transitions + coherent simulate on a "
+                                               "2^18-token trace (the reference's own CPU code "
+                                               "path, C restatement)"},
+            "e2e": {"value": tps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    a = parse()
+    n_env = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n = max(n_env, 1)
+    if a.impl == "reference":
+        return run_reference(a, rank, n)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2401_08383_b200 import _capi, affinity, placement as pl
+    from paper_2401_08383_b200.model import MoeModel, MoeModelConfig
+
+    torch.cuda.set_device(local_rank)
+    if n > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    assert _capi.load().exf_device_ok() == 1, "libexflow_b200.so cannot see an sm_100 GPU"
+    dev = torch.device("cuda", local_rank)
+
+    def barrier():
+        if n > 1:
+            dist.barrier()
+
+    def allmax(v):
+        if n == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum_i64(arr):
+        if n == 1:
+            return arr
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+        dist.all_reduce(t)
+        return t.cpu().numpy()
+
+    def make_model(assign):
+        cfg = MoeModelConfig(num_experts=a.experts, num_layers=a.layers, d_model=a.d_model,
+                             d_ffn=a.d_ffn, tokens_per_gpu=a.batch, world_size=n, rank=rank,
+                             seed=1234, gate_affinity=a.gate_affinity)
+        m = MoeModel(cfg, assign)
+        if n > 1:
+            hs = [None] * n
+            dist.all_gather_object(hs, m.ipc_handle())
+            m.connect(hs)
+        return m
+
+    gen = torch.Generator(device="cpu").manual_seed(100 + rank)
+    x_host = torch.randn(a.batch, a.d_model, generator=gen).to(torch.bfloat16).pin_memory()
+    x_dev = x_host.to(dev)
+    stream = torch.cuda.Stream(device=dev)
+    topo = affinity.Topology(1, n)
+
+    # ---- vanilla placement + profiling pass for the affinity histogram
+    vanilla = pl.contiguous_placement(a.experts, a.layers, topo)
+    model = make_model(vanilla)
+    with torch.cuda.stream(stream):
+        for _ in range(4):
+            model.step(x_dev, stream)
+    stream.synchronize()
+    model.check()
+    counts = allsum_i64(model.affinity_counts())
+    aff_assign, solve = pl.solve_staged(counts, topo, pl.AnnealParams(seed=7))
+    # G=8 view of the same routes (replay on the GPU): how much cross-GPU
+    # routing each placement would cause on the 8xB200 box
+    routes = model.routes()
+    if n > 1:
+        allr = [None] * n
+        dist.all_gather_object(allr, routes)
+        routes = np.max(np.stack(allr), axis=0)
+    g8 = affinity.Topology(1, 8)
+    g8_counts = affinity.count_transitions(routes, a.experts).matrices
+    g8_aff, _ = pl.solve_staged(g8_counts, g8, pl.AnnealParams(seed=7))
+    rep_v8 = affinity.simulate(routes, pl.contiguous_placement(a.experts, a.layers, g8),
+                               affinity.SimConfig(mode=affinity.COHERENT, topology=g8))
+    rep_a8 = affinity.simulate(routes, g8_aff, affinity.SimConfig(mode=affinity.COHERENT,
+                                                                   topology=g8))
+
+    results = {}
+    clocks = None
+    for name, assign in (("vanilla", vanilla), ("affinity", aff_assign)):
+        if name == "affinity":
+            model.close()
+            model = make_model(assign)
+        model.capture(x_dev, stream)
+        for _ in range(a.warmup):
+            model.replay(stream)
+        stream.synchronize()
+        model.check()
+        model.reset_stats()
+        barrier()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local_rank) if name == "affinity" else None
+        if sampler:
+            sampler.start()
+            time.sleep(0.3)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(a.steps):
+            model.replay(stream)
+        ev1.record(stream)
+        stream.synchronize()
+        if sampler:
+            clocks = sampler.stop()
+        model.check()
+        ms = allmax(ev0.elapsed_time(ev1)) / a.steps
+        barrier()
+        crossed = allsum_i64(model.crossed())
+        frac = float(crossed.sum()) / (a.batch * n * a.layers * a.steps)
+        results[name] = {"value": a.batch * n / (ms * 1e-3), "ms_per_step": ms,
+                         "routed_fraction": frac}
+        log(f"[bench] {name}: {ms:.3f} ms/step, {results[name]['value']:.0f} tok/s, "
+            f"routed fraction {frac:.4f}")
+
+    # ---- e2e through the public API with host buffers (affinity placement)
+    out_host = torch.empty(a.batch * n, a.d_model, dtype=torch.bfloat16).pin_memory()
+    out_dev = model.output()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for _ in range(a.steps):
+            x_dev.copy_(x_host, non_blocking=True)
+            model.replay(stream)
+            out_host.copy_(out_dev, non_blocking=True)
+        ev1.record(stream)
+    stream.synchronize()
+    model.check()
+    e2e_ms = allmax(ev0.elapsed_time(ev1)) / a.steps
+    h2d = a.batch * a.d_model * 2
+    d2h = a.batch * n * a.d_model * 2
+
+    # ---- FFN kernel timing (events around GEMM1+GEMM2 of every layer)
+    from paper_2401_08383_b200.model import (PHASE_BEGIN, PHASE_DISPATCH, PHASE_FFN,
+                                             PHASE_GATHER_SEND, PHASE_GATHER_WAIT)
+    reps = max(2, min(a.steps, 5))
+    ffn_ms = []
+    gate_ms = []
+    barrier()
+    for _ in range(reps):
+        model.reset_stats()
+        model.phase(PHASE_BEGIN, 0, x_dev, stream)
+        for j in range(a.layers):
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            model.phase(PHASE_DISPATCH, j, None, stream)
+            e1.record(stream)
+            model.phase(PHASE_FFN, j, None, stream)
+            e2.record(stream)
+            stream.synchronize()
+            gate_ms.append(e0.elapsed_time(e1))
+            ffn_ms.append(e1.elapsed_time(e2))
+        model.phase(PHASE_GATHER_SEND, 0, None, stream)
+        model.phase(PHASE_GATHER_WAIT, 0, None, stream)
+        stream.synchronize()
+    model.check()
+    r_local = model.routes()
+    # algorithmic bytes of one FFN pair on this rank: weights of every local
+    # expert that received tokens + token-side traffic
+    assign_f = aff_assign
+    d, f, E_loc = a.d_model, a.d_ffn, a.experts // n
+    bytes_layers = []
+    for j in range(a.layers):
+        toks = r_local[:, j][r_local[:, j] >= 0]
+        mine = toks[assign_f[j][toks] == rank]
+        active = len(set(mine.tolist()))
+        nt = len(mine)
+        bytes_layers.append(active * (2 * d * f * 2 + (d + f) * 2) + nt * (2 * d + 4 * f + 4 * d))
+    ffn_avg_ms = statistics.mean(ffn_ms)
+    ffn_bytes = statistics.mean(bytes_layers)
+    achieved = ffn_bytes / (ffn_avg_ms * 1e-3) / 1e9
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    launches = model.launches_per_step()
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and n == 1 and not a.no_cpu_baseline:
+        from oracle import cpu_path
+        tps, dt, sample, threads = cpu_path.time_cpu_path(
+            a.experts, a.layers, a.d_model, a.d_ffn, a.batch, 1,
+            np.zeros((a.layers, a.experts), np.int32), 2, 2)
+        cpu = {"value": tps, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+
+    aff = results["affinity"]
+    line = {
+        "metric": METRIC, "value": aff["value"], "unit": UNIT, "n_gpus": n, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": aff["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": workload(a, n),
+        "routed_fraction": aff["routed_fraction"],
+        "placements": results,
+        "g8_replay_routed_fraction": {"vanilla": rep_v8.p_star, "affinity": rep_a8.p_star,
+                                      "note": "p_star of this run's routes replayed on a 1x8 "
+                                              "topology (GPU replay kernel)"},
+        "affinity_solve": {"solver": solve.solver, "objective": solve.objective},
+        "e2e": {"value": a.batch * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "roofline": {"kernel": "ffn_gemm_kernel (GEMM1+GEMM2 per layer, tcgen05)",
+                     "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "bytes_per_launch": ffn_bytes, "ms_per_launch": ffn_avg_ms,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
+                     "gate_dispatch_ms_per_layer": statistics.mean(gate_ms)},
+        "clocks": clocks,
+        "gpu_launches": launches * (a.steps) * n,
+        "cpu_baseline": cpu,
+    }
+    model.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if n > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
