@@ -320,6 +320,7 @@ def main():
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     launches = model.launches_per_step()
+    plan = model.describe()
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -335,7 +336,7 @@ def main():
         "metric": METRIC, "value": aff["value"], "unit": UNIT, "n_gpus": n, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": aff["ms_per_step"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": workload(a, n),
+        "config": dict(workload(a, n), launch_plan=plan),
         "routed_fraction": aff["routed_fraction"],
         "placements": results,
         "g8_replay_routed_fraction": {"vanilla": rep_v8.p_star, "affinity": rep_a8.p_star,

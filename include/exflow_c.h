@@ -255,6 +255,9 @@ exf_status exf_model_capture(exf_model* model, const void* d_x_in, exf_stream_t 
 exf_status exf_model_replay(exf_model* model, exf_stream_t stream);
 /* Kernel launches one step issues (for bench accounting). */
 int32_t exf_model_launches_per_step(exf_model* model);
+/* JSON description of the launch plan (token tile, split-K, persistent
+ * clusters per GEMM) into buf (NUL-terminated, truncated to len). */
+exf_status exf_model_describe(exf_model* model, char* buf, int32_t len);
 
 #ifdef __cplusplus
 }

@@ -110,6 +110,7 @@ SIGNATURES = {
     "exf_model_capture": (C.c_int, [_VP, _VP, _VP]),
     "exf_model_replay": (C.c_int, [_VP, _VP]),
     "exf_model_launches_per_step": (_I32, [_VP]),
+    "exf_model_describe": (C.c_int, [_VP, _VP, _I32]),
 }
 
 

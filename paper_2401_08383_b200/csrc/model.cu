@@ -32,7 +32,10 @@ exf_status launch_gather_wait(uint8_t* own_sym, const Symm& sym, int G, uint64_t
                               int32_t* err, cudaStream_t s);
 exf_status make_weight_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols);
 
-exf_status launch_ffn_gemm(const CUtensorMap& map, const FfnArgs& a, int nmax, cudaStream_t s);
+exf_status launch_ffn_gemm(const CUtensorMap& map, const CUtensorMap& mapB, const FfnArgs& a,
+                           int nmax, int clusters, cudaStream_t s);
+exf_status make_gather_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols);
+exf_status plan_ffn_gemm(int nmax, int mode, int items, int K, int* ksplit, int* clusters);
 
 namespace {
 
@@ -77,12 +80,6 @@ uint64_t weight_key(int layer, int expert, int E, int which) {
 }
 uint64_t gate_key(int layer) { return 0x6A7E000000000000ULL + (uint64_t)layer; }
 
-int pick_ksplit(int units, int K) {
-    int ks = 1;
-    while (ks < 8 && units * ks < 148 && (K / 64) % (ks * 2) == 0 && K / 64 / (ks * 2) >= 2) ks *= 2;
-    return ks;
-}
-
 }  // namespace
 }  // namespace exf
 
@@ -103,7 +100,8 @@ struct exf_model {
     __nv_bfloat16* b1 = nullptr;            // [L][E_loc][dff]
     __nv_bfloat16* w2 = nullptr;            // [L][E_loc][d][dff]
     __nv_bfloat16* b2 = nullptr;            // [L][E_loc][d]
-    std::vector<CUtensorMap> tmap1, tmap2;  // per layer
+    std::vector<CUtensorMap> tmap1, tmap2;  // per layer (weights, TMA tiles)
+    CUtensorMap gmap_recv{}, gmap_h{};      // token rows for TMA gather4
     // symmetric region
     Symm sym{};
     uint8_t* sym_base = nullptr;
@@ -128,7 +126,8 @@ struct exf_model {
     int32_t* err = nullptr;
     int32_t* done_ctr = nullptr;            // [2] dispatch, gather
     int nmax = 64;
-    int ks1 = 1, ks2 = 1;
+    int ks1 = 1, ks2 = 1;   // split-K (cluster size) of GEMM1 / GEMM2
+    int cl1 = 1, cl2 = 1;   // persistent clusters of GEMM1 / GEMM2
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
 };
@@ -330,8 +329,8 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
         }
         case 2: {
             if (j < 0 || j >= c.num_layers) return invalid("layer out of range");
-            EXF_TRY(launch_ffn_gemm(m->tmap1[j], ffn_args(m, j, 0), m->nmax, s));
-            return launch_ffn_gemm(m->tmap2[j], ffn_args(m, j, 1), m->nmax, s);
+            EXF_TRY(launch_ffn_gemm(m->tmap1[j], m->gmap_recv, ffn_args(m, j, 0), m->nmax, m->cl1, s));
+            return launch_ffn_gemm(m->tmap2[j], m->gmap_h, ffn_args(m, j, 1), m->nmax, m->cl2, s);
         }
         case 3: {
             const int fin = c.num_layers & 1;
@@ -407,12 +406,14 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     EXF_M(dalloc(&m->done_ctr, 2));
     EXF_M(dalloc(&m->d_peers, (size_t)c.world_size));
     EXF_M(build_layout(m));
+    EXF_M(make_gather_tmap(&m->gmap_recv, m->sym_base + m->sym.recv_x, 2LL * c.world_size * C, d));
+    EXF_M(make_gather_tmap(&m->gmap_h, m->H, C, f));
     if (cudaMemset(m->trace, 0xff, sizeof(int32_t) * C * L) != cudaSuccess) return fail(EXF_CUDA);
     EXF_M(init_weights(m));
     // tile policy: token tile from the expected tokens per expert, split-K to fill 148 SMs
     m->nmax = (2 * C / E <= 64) ? 64 : 128;
-    m->ks1 = pick_ksplit(m->E_loc * (f / 128), d);
-    m->ks2 = pick_ksplit(m->E_loc * (d / 128), f);
+    EXF_M(plan_ffn_gemm(m->nmax, 0, m->E_loc * (f / 128), d, &m->ks1, &m->cl1));
+    EXF_M(plan_ffn_gemm(m->nmax, 1, m->E_loc * (d / 128), f, &m->ks2, &m->cl2));
     if (c.world_size == 1) {  // a single rank is its own peer
         exf_model* self = m;
         EXF_M(exf_model_connect_local(&self, 1));
@@ -646,6 +647,20 @@ exf_status exf_model_replay(exf_model* m, exf_stream_t stream) {
 int32_t exf_model_launches_per_step(exf_model* m) {
     if (!m) return 0;
     return 1 + 4 * m->cfg.num_layers + 2;
+}
+
+exf_status exf_model_describe(exf_model* m, char* buf, int32_t len) {
+    if (!m || !buf || len < 1) return invalid("bad argument");
+    const std::string s = "{\"token_tile\": " + std::to_string(m->nmax) +
+                          ", \"gemm1\": {\"ksplit\": " + std::to_string(m->ks1) +
+                          ", \"clusters\": " + std::to_string(m->cl1) +
+                          "}, \"gemm2\": {\"ksplit\": " + std::to_string(m->ks2) +
+                          ", \"clusters\": " + std::to_string(m->cl2) +
+                          "}, \"experts_per_rank\": " + std::to_string(m->E_loc) +
+                          ", \"capacity_tokens\": " + std::to_string(m->C) + "}";
+    std::strncpy(buf, s.c_str(), (size_t)len - 1);
+    buf[len - 1] = 0;
+    return EXF_OK;
 }
 
 }  // extern "C"

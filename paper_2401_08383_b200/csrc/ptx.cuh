@@ -146,6 +146,19 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(cache_hint)
         : "memory");
 }
+// TMA gather4: rows r0..r3 (each boxDim[0] elements starting at column c0) of
+// a 2-D tensor map with boxDim[1] == 1, written as a 4-row box (512 B with
+// SWIZZLE_128B) -- the Blackwell indexed-row load used for MoE token gathers.
+__device__ __forceinline__ void tma_gather4(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                            int32_t c0, int32_t r0, int32_t r1, int32_t r2,
+                                            int32_t r3) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+        "r"(smem_u32(bar))
+        : "memory");
+}
 // L2 eviction-priority policies (createpolicy.fractional)
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;

@@ -177,6 +177,12 @@ class MoeModel:
     def launches_per_step(self) -> int:
         return int(_capi.load().exf_model_launches_per_step(self._h))
 
+    def describe(self) -> dict:
+        import json
+        buf = C.create_string_buffer(512)
+        _capi.call("exf_model_describe", self._h, buf, 512)
+        return json.loads(buf.value.decode())
+
     def close(self) -> None:
         if self._h:
             _capi.call("exf_model_destroy", self._h)
