@@ -258,6 +258,13 @@ int32_t exf_model_launches_per_step(exf_model* model);
 /* JSON description of the launch plan (token tile, split-K, persistent
  * clusters per GEMM) into buf (NUL-terminated, truncated to len). */
 exf_status exf_model_describe(exf_model* model, char* buf, int32_t len);
+/* Diagnostics: per-CTA globaltimer stamps of the last GEMM1/GEMM2 launches
+ * ([2][ctas][16] u64; requires EXF_FFN_TIMELINE=1 at create time). */
+exf_status exf_model_read_ffn_timeline(exf_model* model, uint64_t* h_stamps, int32_t ctas);
+/* Diagnostics: per (layer, kernel in {gate_dispatch, GEMM1, GEMM2}) globaltimer
+ * [first CTA entry, first wait-return, last wait-return, last CTA exit,
+ * phase marks 4..7] ([L][3][8] u64); reset != 0 re-arms the timeline. */
+exf_status exf_model_read_step_timeline(exf_model* model, uint64_t* h_stamps, int32_t reset);
 
 #ifdef __cplusplus
 }

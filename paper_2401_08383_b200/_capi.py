@@ -111,6 +111,8 @@ SIGNATURES = {
     "exf_model_replay": (C.c_int, [_VP, _VP]),
     "exf_model_launches_per_step": (_I32, [_VP]),
     "exf_model_describe": (C.c_int, [_VP, _VP, _I32]),
+    "exf_model_read_ffn_timeline": (C.c_int, [_VP, _VP, _I32]),
+    "exf_model_read_step_timeline": (C.c_int, [_VP, _VP, _I32]),
 }
 
 

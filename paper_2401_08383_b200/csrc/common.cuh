@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 #include <string>
 
 #include "exflow_c.h"
@@ -47,6 +48,43 @@ exf_status cuda_status(cudaError_t err, const char* what);
 
 // Launch check: catches configuration errors right after a <<<>>> launch.
 #define EXF_LAUNCH_CHECK(what) EXF_CUDA_TRY(cudaPeekAtLastError())
+
+namespace exf {
+// Kernel launch with programmatic dependent launch (PDL) enabled: the grid may
+// start while the previous grid in the stream finishes; kernels call
+// griddepcontrol.wait before consuming the previous grid's output. Optional
+// thread-block cluster dimension.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, int cluster, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[2];
+    int n = 0;
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+    if (cluster > 0) {
+        at[n].id = cudaLaunchAttributeClusterDimension;
+        at[n].val.clusterDim.x = cluster;
+        at[n].val.clusterDim.y = 1;
+        at[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+// One fixed L1/shared carveout (max shared) for every step kernel, so the SMs
+// never reconfigure between back-to-back kernels of a decode step.
+template <typename K>
+inline void max_carveout(K kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+}  // namespace exf
 
 namespace exf {
 

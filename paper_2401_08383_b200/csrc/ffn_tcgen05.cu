@@ -88,6 +88,48 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant
     const int kbs = a.K / kBK / ks;  // k-blocks of this split
     const int kb0 = (int)crank * kbs;
 
+    uint64_t* ts = a.tstamp ? a.tstamp + (int64_t)blockIdx.x * 16 : nullptr;
+    if (ts && tid == 0) ts[0] = ptx::globaltimer();
+    if (tid == 0) tl_mark(a.tl, 0);
+
+    // ---- independent prologue (overlaps the previous kernel under PDL):
+    //      barriers, TMEM, and the first weight stages of this CTA's first item
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(&full[s], 2);  // A producer + B producer (expect_tx each)
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&tmem_full[b], 1);
+            ptx::mbar_init(&tmem_empty[b], 128);
+        }
+        ptx::mbar_init(red_full, ks);
+        ptx::mbar_init(red_empty, ks);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(&misc[0], 2 * NMAX);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem = misc[0];
+    // weights do not depend on the previous kernel: prefetch the first
+    // min(kbs, STAGES) k-blocks of the first item (its first chunk always runs)
+    const int npre = cluster_id < items ? min(kbs, STAGES) : 0;
+    const uint64_t pol_a = ptx::policy_evict_first();
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmapA);
+        const int e0 = cluster_id / mtiles, mt0 = cluster_id - e0 * mtiles;
+        for (int kb = 0; kb < npre; ++kb) {
+            ptx::mbar_arrive_expect_tx(&full[kb], S::kA);
+            ptx::tma_load_2d(smem + S::kOffA + kb * S::kA, &tmapA, &full[kb], (kb0 + kb) * kBK,
+                             e0 * a.M_total + mt0 * kBM, pol_a);
+        }
+    }
+
+    // ---- dependent part: the previous kernel's outputs become visible here
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    if (tid == 0) tl_mark(a.tl, 1);
     const uint64_t q = *a.step * (uint64_t)a.L + (uint64_t)a.layer;
     const int parity = (int)(q & 1);
     const uint64_t epoch = q + 1;
@@ -135,44 +177,32 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant
         while (s + 1 < a.G && t[2 + s + 1] <= i) ++s;
         return ((int64_t)parity * a.G + s) * a.C + t[11 + s] + (i - t[2 + s]);
     };
-
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            ptx::mbar_init(&full[s], 2);  // A producer + B producer (expect_tx each)
-            ptx::mbar_init(&empty[s], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            ptx::mbar_init(&tmem_full[b], 1);
-            ptx::mbar_init(&tmem_empty[b], 128);
-        }
-        ptx::mbar_init(red_full, ks);
-        ptx::mbar_init(red_empty, ks);
-        ptx::fence_mbar_init();
-    }
-    if (warp == 1) ptx::tmem_alloc(&misc[0], 2 * NMAX);
-    ptx::tc_fence_before();
-    ptx::cluster_sync();  // also publishes the tables (all threads, all CTAs)
-    ptx::tc_fence_after();
-    const uint32_t tmem = misc[0];
+    // chunks of item w: the CTA's first item always runs >= 1 chunk (its first
+    // weight stages were prefetched before the token counts were known)
+    auto nchunks = [&](int w, int n_e) {
+        const int c = (n_e + NMAX - 1) / NMAX;
+        return (w == cluster_id && c == 0) ? 1 : c;
+    };
+    __syncthreads();  // tables visible to every role of this CTA
+    if (ts && tid == 0) ts[1] = ptx::globaltimer();
 
     if (warp == 0) {
         // ================= A producer (weights via TMA) =================
         if (lane == 0) {
-            ptx::tma_prefetch_desc(&tmapA);
-            const uint64_t pol = ptx::policy_evict_first();
             int it = 0;
             for (int w = cluster_id; w < items; w += num_clusters) {
                 const int e = w / mtiles, mt = w - e * mtiles;
-                const int n_e = tab[e * S::kTabInts];
+                const int nch = nchunks(w, tab[e * S::kTabInts]);
                 const int row0 = e * a.M_total + mt * kBM;
-                for (int cb = 0; cb < n_e; cb += NMAX)
+                for (int c = 0; c < nch; ++c)
                     for (int kb = 0; kb < kbs; ++kb, ++it) {
+                        if (it < npre) continue;  // prefetched in the prologue
                         const int st = it % STAGES;
                         const uint32_t ph = (it / STAGES) & 1;
                         ptx::mbar_wait(&empty[st], ph ^ 1, a.err, ERR_TIMEOUT_PIPE);
                         ptx::mbar_arrive_expect_tx(&full[st], S::kA);
                         ptx::tma_load_2d(smem + S::kOffA + st * S::kA, &tmapA, &full[st],
-                                         (kb0 + kb) * kBK, row0, pol);
+                                         (kb0 + kb) * kBK, row0, pol_a);
                     }
             }
         }
@@ -182,9 +212,10 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant
         for (int w = cluster_id; w < items; w += num_clusters) {
             const int e = w / mtiles;
             const int n_e = tab[e * S::kTabInts];
-            for (int cb = 0; cb < n_e; cb += NMAX, ++job) {
-                const int nc = min(NMAX, n_e - cb);
-                const int ncol = (nc + 15) & ~15;
+            const int nch = nchunks(w, n_e);
+            for (int c = 0; c < nch; ++c, ++job) {
+                const int nc = max(0, min(NMAX, n_e - c * NMAX));
+                const int ncol = max(16, (nc + 15) & ~15);
                 const uint32_t idesc = ptx::umma_idesc_bf16(kBM, ncol);
                 const int buf = job & 1;
                 if (job >= 2) ptx::mbar_wait(&tmem_empty[buf], ((job >> 1) - 1) & 1, a.err, ERR_TIMEOUT_PIPE);
@@ -203,6 +234,8 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant
                             ptx::umma_bf16(d_tmem, da + 2 * kk, db + 2 * kk, idesc, (kb | kk) ? 1u : 0u);
                         ptx::umma_commit(&empty[st]);
                         if (kb == kbs - 1) ptx::umma_commit(&tmem_full[buf]);
+                        if (ts && kb == 0 && job < 6) ts[2 + 2 * job] = ptx::globaltimer();
+                        if (ts && kb == kbs - 1 && job < 6) ts[3 + 2 * job] = ptx::globaltimer();
                     }
                     __syncwarp();
                 }
@@ -219,16 +252,20 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant
             const int e = w / mtiles;
             const int n_e = tab[e * S::kTabInts];
             const int off_e = tab[e * S::kTabInts + 1];
-            for (int cb = 0; cb < n_e; cb += NMAX) {
-                const int nc = min(NMAX, n_e - cb);
-                const int ncol = (nc + 15) & ~15;
+            const int nch = nchunks(w, n_e);
+            const int row_lim = MODE == 0 ? 2 * a.G * a.C : a.C;
+            for (int c = 0; c < nch; ++c) {
+                const int cb = c * NMAX;
+                const int nc = max(0, min(NMAX, n_e - cb));
+                const int ncol = max(16, (nc + 15) & ~15);
                 const int ng = ncol >> 2;
                 int32_t rows[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int r = 4 * lane + u;
                     const int i = cb + (r < nc ? r : 0);
-                    rows[u] = MODE == 0 ? (int32_t)recv_row(e, i) : off_e + i;
+                    const int64_t row = MODE == 0 ? recv_row(e, i) : (int64_t)(off_e + i);
+                    rows[u] = (int32_t)(row < 0 ? 0 : (row >= row_lim ? row_lim - 1 : row));
                 }
                 for (int kb = 0; kb < kbs; ++kb, ++it) {
                     const int st = it % STAGES;
@@ -266,9 +303,11 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant
             }
             const int m_glob = mt * kBM + my_row;
             const float bias = n_e ? __bfloat162float(a.bias[(int64_t)e * a.M_total + m_glob]) : 0.f;
-            for (int cb = 0; cb < n_e; cb += NMAX, ++job) {
-                const int nc = min(NMAX, n_e - cb);
-                const int ncol = (nc + 15) & ~15;
+            const int nch = nchunks(w, n_e);
+            for (int c = 0; c < nch; ++c, ++job) {
+                const int cb = c * NMAX;
+                const int nc = max(0, min(NMAX, n_e - cb));
+                const int ncol = max(16, (nc + 15) & ~15);
                 const int buf = job & 1;
                 ptx::mbar_wait(&tmem_full[buf], (job >> 1) & 1, a.err, ERR_TIMEOUT_PIPE);
                 ptx::tc_fence_after();
@@ -319,8 +358,11 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant
         }
         // peers must be done reading this CTA's partial before it exits
         if (job > 0) ptx::mbar_wait_cluster(red_empty, (job - 1) & 1, a.err, ERR_TIMEOUT_PIPE);
+        if (ts && et == 0) ts[14] = ptx::globaltimer();
     }
     __syncthreads();
+    if (ts && tid == 0) ts[15] = ptx::globaltimer();
+    if (tid == 0) tl_mark(a.tl, 3);
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, 2 * NMAX);
@@ -358,6 +400,7 @@ struct Launcher {
         if (max_clusters[1]) return EXF_OK;
         EXF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes));
         EXF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        max_carveout(kern);
         for (int ks = 1; ks <= 16; ks *= 2) {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(ks * 148);
@@ -404,27 +447,27 @@ struct Launcher {
 
     exf_status launch(const CUtensorMap& map, const CUtensorMap& mapB, FfnArgs a, int clusters,
                       cudaStream_t s) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(clusters * a.ksplit);
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = S::kBytes;
-        cfg.stream = s;
-        cudaLaunchAttribute attrs[1];
-        attrs[0].id = cudaLaunchAttributeClusterDimension;
-        attrs[0].val.clusterDim.x = a.ksplit;
-        attrs[0].val.clusterDim.y = 1;
-        attrs[0].val.clusterDim.z = 1;
-        cfg.attrs = attrs;
-        cfg.numAttrs = 1;
-        EXF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, map, mapB, a));
+        EXF_CUDA_TRY(launch_pdl(kern, dim3(clusters * a.ksplit), dim3(kThreads), S::kBytes, s,
+                                a.ksplit, map, mapB, a));
         return EXF_OK;
     }
 };
 
-Launcher<64, 6, 0> g_l64_0;
-Launcher<64, 6, 1> g_l64_1;
+// token tile x ring depth: smaller token tiles leave room for more weight
+// stages in flight (A bytes in flight per SM = STAGES * 16 KB)
+Launcher<32, 10, 0> g_l32_0;
+Launcher<32, 10, 1> g_l32_1;
+Launcher<64, 7, 0> g_l64_0;
+Launcher<64, 7, 1> g_l64_1;
 Launcher<128, 4, 0> g_l128_0;
 Launcher<128, 4, 1> g_l128_1;
+
+template <class F>
+exf_status with_launcher(int nmax, int mode, F&& f) {
+    if (nmax <= 32) return mode == 0 ? f(g_l32_0) : f(g_l32_1);
+    if (nmax <= 64) return mode == 0 ? f(g_l64_0) : f(g_l64_1);
+    return mode == 0 ? f(g_l128_0) : f(g_l128_1);
+}
 
 }  // namespace
 
@@ -465,14 +508,11 @@ exf_status make_gather_tmap(CUtensorMap* map, const void* base, int64_t rows, in
 // Chooses (split-K, clusters) for a GEMM of `items` 128-row tiles over `K`.
 exf_status plan_ffn_gemm(int nmax, int mode, int items, int K, int* ksplit, int* clusters) {
     const int kblocks = K / kBK;
-    if (nmax <= 64) {
-        if (mode == 0) { EXF_TRY(g_l64_0.prepare()); g_l64_0.plan(items, kblocks, ksplit, clusters); }
-        else { EXF_TRY(g_l64_1.prepare()); g_l64_1.plan(items, kblocks, ksplit, clusters); }
-    } else {
-        if (mode == 0) { EXF_TRY(g_l128_0.prepare()); g_l128_0.plan(items, kblocks, ksplit, clusters); }
-        else { EXF_TRY(g_l128_1.prepare()); g_l128_1.plan(items, kblocks, ksplit, clusters); }
-    }
-    return EXF_OK;
+    return with_launcher(nmax, mode, [&](auto& l) {
+        EXF_TRY(l.prepare());
+        l.plan(items, kblocks, ksplit, clusters);
+        return EXF_OK;
+    });
 }
 
 exf_status launch_ffn_gemm(const CUtensorMap& map, const CUtensorMap& mapB, const FfnArgs& a,
@@ -482,14 +522,10 @@ exf_status launch_ffn_gemm(const CUtensorMap& map, const CUtensorMap& mapB, cons
     if (a.K % (kBK * a.ksplit) != 0) return invalid("FFN K must be a multiple of 64*ksplit");
     if (a.G > kMaxSrc) return invalid("at most 8 ranks per dispatch group");
     if (a.E_loc > kMaxLocal) return invalid("at most 64 local experts");
-    if (nmax <= 64) {
-        if (a.mode == 0) { EXF_TRY(g_l64_0.prepare()); return g_l64_0.launch(map, mapB, a, clusters, s); }
-        EXF_TRY(g_l64_1.prepare());
-        return g_l64_1.launch(map, mapB, a, clusters, s);
-    }
-    if (a.mode == 0) { EXF_TRY(g_l128_0.prepare()); return g_l128_0.launch(map, mapB, a, clusters, s); }
-    EXF_TRY(g_l128_1.prepare());
-    return g_l128_1.launch(map, mapB, a, clusters, s);
+    return with_launcher(nmax, a.mode, [&](auto& l) {
+        EXF_TRY(l.prepare());
+        return l.launch(map, mapB, a, clusters, s);
+    });
 }
 
 }  // namespace exf

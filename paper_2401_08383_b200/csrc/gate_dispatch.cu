@@ -1,23 +1,26 @@
-// gate_dispatch.cu -- per-layer token-side kernels of the ExFlow decode step.
+// gate_dispatch.cu -- per-layer token-side kernel of the ExFlow decode step,
+// plus step begin and the context AllGather.
 //
-//  (1) gate_kernel: fused gate GEMM + softmax/top-1 + affinity histogram
-//      (kernel 5, fused form) + routing-trace emission. One warp per token;
-//      the logits use the fixed fp32 reduction order documented in
-//      oracle/exflow_model_oracle.c (32 lane partials accumulated c-major /
-//      i-minor with FMA, then a xor-butterfly), so routing is bit-identical
-//      to the CPU oracle. Top-1 ties -> lowest expert index.
-//  (2)+(3) dispatch_kernel: deterministic, atomic-free bucketing of the
-//      resident tokens by (destination GPU, local expert slot) with a
-//      warp-aggregated prefix scan (__match_any_sync + popc(lanemask_lt),
-//      then a per-key scan over warps), fused with ExFlow's single dispatch
-//      "Alltoall": rows are stored straight into the destination rank's
-//      symmetric receive region over NVLink (P2P stores through CUDA-IPC
-//      mapped pointers), followed by a system-scope release flag. Tokens stay
-//      on their expert's GPU afterwards (coherent mode, no combine step;
-//      proj/src/sim.cpp:65-71).
-//  (3b) gather_send/gather_wait: the per-step context AllGather; every rank
-//      scatters its resident tokens' hidden states into every peer's
-//      token-id-indexed output buffer, then waits for all peers' flags.
+// gate_dispatch_kernel (kernels 1 + 5' + 2 + 3 fused, latency-optimised):
+//  (1) gate: the layer's gate matrix Wg [E][d] is staged in shared memory;
+//      one warp per token computes the logits in the fixed fp32 reduction
+//      order documented in oracle/exflow_model_oracle.c (32 lane partials,
+//      c-major / i-minor FMA, xor-butterfly), so routing is bit-identical to
+//      the CPU oracle; top-1 ties -> lowest expert index; softmax prob.
+//  (5') fused affinity histogram hist[j-1][prev][e] += 1 and trace emission.
+//  (2) deterministic, atomic-free bucketing by (destination GPU, local slot):
+//      each CTA owns a contiguous token slice; warp-aggregated ranks
+//      (__match_any_sync + popc(lanemask_lt)) give per-CTA key counts; one
+//      grid barrier publishes them; every CTA prefix-sums the counts of the
+//      CTAs before it -> stable global positions (token order within a key).
+//  (3) ExFlow's single dispatch exchange: rows are stored straight into the
+//      destination rank's symmetric receive region over NVLink (P2P stores
+//      through CUDA-IPC mapped pointers); the last CTA writes the per-(src,
+//      slot) counts and release-flags every destination. Tokens stay on their
+//      expert's GPU (coherent mode, proj/src/sim.cpp:65-71; no combine).
+// gather_send/gather_wait (3b): the per-step context AllGather; every rank
+// scatters its resident tokens' states into every peer's token-id-indexed
+// output buffer, then waits for all peers' flags.
 #include "common.cuh"
 #include "model.cuh"
 #include "ptx.cuh"
@@ -46,18 +49,102 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Sense-reversal grid barrier over all CTAs of the launch (they are all
+// co-resident: the grid is capped well below one CTA per SM).
+__device__ void grid_barrier(uint32_t* gbar, uint32_t nctas, int32_t* err) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t gen = ld_acquire_gpu_u32(gbar + 1);
+        __threadfence();
+        const uint32_t prev = atomicAdd(gbar, 1u);
+        if (prev == nctas - 1) {
+            gbar[0] = 0;
+            __threadfence();
+            atomicAdd(gbar + 1, 1u);
+        } else {
+            ptx::SpinGuard g;
+            while (ld_acquire_gpu_u32(gbar + 1) == gen) g.step(err, ERR_TIMEOUT_PIPE);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 }  // namespace
 
-// ------------------------------------------------------------------ gate
+constexpr int kGdThreads = 512;
+constexpr int kGdWarps = kGdThreads / 32;
+constexpr int kMaxKeys = 64;
+
 template <int EMAX>
-__global__ void __launch_bounds__(256) gate_kernel(LayerArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
+__global__ void __launch_bounds__(kGdThreads) gate_dispatch_kernel(LayerArgs a, int wg_in_smem) {
+    // dynamic smem: X [tpc][d] bf16 | meta [tpc] ResMeta | Wg [E][d] bf16 (when it fits)
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ int32_t s_exp[256];
+    __shared__ float s_prob[256];
+    __shared__ int32_t s_pos[256];
+    __shared__ int32_t s_cnt[kMaxKeys];   // this CTA's per-key counts (running)
+    __shared__ int32_t s_tot[kMaxKeys];   // all CTAs
+    __shared__ int32_t s_before[kMaxKeys];
+    __shared__ int32_t s_start[kMaxKeys + 1];
+    __shared__ int32_t s_last;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) tl_mark(a.tl, 0);
+    ptx::pdl_wait();
+    ptx::pdl_trigger();  // GEMM1 may start its prologue + weight prefetch now
+    if (tid == 0) tl_mark(a.tl, 1);
+
     const int n = *a.n_res_in;
+    const uint64_t q = *a.step * (uint64_t)a.L + (uint64_t)a.layer;
+    const int parity = (int)(q & 1);
+    const uint64_t epoch = q + 1;
+    const int t0 = blockIdx.x * a.tpc;
+    const int nt = max(0, min(a.tpc, n - t0));
+    const int E = a.E;
+    if (n > a.C) {
+        if (tid == 0) atomicExch(a.err, ERR_CAPACITY);
+        return;  // uniform: every CTA reads the same n
+    }
+    // only CTAs that own tokens take part (CTA 0 always: it publishes counts
+    // and flags even when no token is resident)
+    const uint32_t nactive = (uint32_t)max(1, (n + a.tpc - 1) / a.tpc);
+    if (blockIdx.x >= nactive) return;
+
+    // ---- stage this CTA's token rows, their metadata and Wg in shared memory
+    //      with one batch of independent 16-byte loads
+    const int vec = a.d >> 3;  // int4 per row
+    __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(smem);
+    ResMeta* smeta = reinterpret_cast<ResMeta*>(smem + (size_t)a.tpc * a.d * 2);
+    const __nv_bfloat16* wg = a.wg;
+    {
+        const int4* xs = reinterpret_cast<const int4*>(a.res_x_in + (int64_t)t0 * a.d);
+        int4* xd = reinterpret_cast<int4*>(sx);
+        for (int i = tid; i < nt * vec; i += kGdThreads) xd[i] = xs[i];
+        for (int i = tid; i < nt; i += kGdThreads) smeta[i] = a.res_meta_in[t0 + i];
+        if (wg_in_smem && nt > 0) {
+            __nv_bfloat16* swg = reinterpret_cast<__nv_bfloat16*>(smem + (size_t)a.tpc * (a.d * 2 + 8));
+            const int4* src = reinterpret_cast<const int4*>(a.wg);
+            int4* dst = reinterpret_cast<int4*>(swg);
+            for (int i = tid; i < E * vec; i += kGdThreads) dst[i] = __ldg(src + i);
+            wg = swg;
+        }
+    }
+    if (tid < kMaxKeys) s_cnt[tid] = 0;
+    __syncthreads();
+    if (tid == 0) tl_mark(a.tl, 4);
+
+    // ---- (1) gate, one warp per token
     const int chunks = a.d >> 8;
-    for (int t = gw; t < n; t += nw) {
-        const __nv_bfloat16* x = a.res_x_in + (int64_t)t * a.d;
+    for (int i = warp; i < nt; i += kGdWarps) {
+        const int t = t0 + i;
+        const __nv_bfloat16* x = sx + (int64_t)i * a.d;
         float acc[EMAX];
 #pragma unroll
         for (int e = 0; e < EMAX; ++e) acc[e] = 0.f;
@@ -66,13 +153,11 @@ __global__ void __launch_bounds__(256) gate_kernel(LayerArgs a) {
             unpack8(*reinterpret_cast<const int4*>(x + c * 256 + lane * 8), xf);
 #pragma unroll
             for (int e = 0; e < EMAX; ++e) {
-                if (e < a.E) {
+                if (e < E) {
                     float wf[8];
-                    unpack8(__ldg(reinterpret_cast<const int4*>(a.wg + (int64_t)e * a.d + c * 256 +
-                                                                 lane * 8)),
-                            wf);
+                    unpack8(*reinterpret_cast<const int4*>(wg + (int64_t)e * a.d + c * 256 + lane * 8), wf);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) acc[e] = fmaf(xf[i], wf[i], acc[e]);
+                    for (int k = 0; k < 8; ++k) acc[e] = fmaf(xf[k], wf[k], acc[e]);
                 }
             }
         }
@@ -86,20 +171,20 @@ __global__ void __launch_bounds__(256) gate_kernel(LayerArgs a) {
             float mx = acc[0];
 #pragma unroll
             for (int e = 1; e < EMAX; ++e)
-                if (e < a.E && acc[e] > mx) {
+                if (e < E && acc[e] > mx) {
                     mx = acc[e];
                     best = e;
                 }
             float s = 0.f;
 #pragma unroll
             for (int e = 0; e < EMAX; ++e)
-                if (e < a.E) s += expf(acc[e] - mx);
-            const ResMeta m = a.res_meta_in[t];
+                if (e < E) s += expf(acc[e] - mx);
+            const ResMeta m = smeta[i];
             int sel = best;
             float p = 1.f / s;
             if (a.forced) {
                 sel = a.forced_routes[(int64_t)m.token * a.L + a.layer];
-                if ((unsigned)sel >= (unsigned)a.E) {
+                if ((unsigned)sel >= (unsigned)E) {
                     atomicExch(a.err, ERR_BAD_EXPERT);
                     sel = best;
                 }
@@ -109,151 +194,118 @@ __global__ void __launch_bounds__(256) gate_kernel(LayerArgs a) {
                     if (e == sel) ls = acc[e];
                 p = expf(ls - mx) / s;
             }
+            s_exp[i] = sel;
+            s_prob[i] = p;
             a.expert[t] = sel;
             a.prob[t] = p;
             if (a.hist && a.layer > 0 && m.prev_expert >= 0)
-                atomicAdd(&a.hist[((int64_t)(a.layer - 1) * a.E + m.prev_expert) * a.E + sel], 1ull);
+                atomicAdd(&a.hist[((int64_t)(a.layer - 1) * E + m.prev_expert) * E + sel], 1ull);
             if (a.trace) a.trace[(int64_t)m.token * a.L + a.layer] = sel;
         }
     }
-}
+    __syncthreads();
+    if (tid == 0) tl_mark(a.tl, 5);
 
-// ------------------------------------------------------------------ dispatch
-// Dynamic smem: key[C] (int16 packed in int32), pos[C], warp counts, per-key
-// running totals. Every CTA runs the (cheap) scan redundantly, then copies its
-// share of rows; the last CTA to finish releases the per-destination flags.
-constexpr int kDispThreads = 512;
-constexpr int kDispWarps = kDispThreads / 32;
-constexpr int kMaxKeys = 64;
-
-__global__ void __launch_bounds__(kDispThreads) dispatch_kernel(LayerArgs a) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    int32_t* s_pos = reinterpret_cast<int32_t*>(smem);        // [C]
-    int32_t* s_key = s_pos + a.C;                              // [C]
-    __shared__ int32_t s_wcnt[kDispWarps][kMaxKeys];
-    __shared__ int32_t s_run[kMaxKeys];
-    __shared__ int32_t s_start[kMaxKeys + 1];
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int n = *a.n_res_in;
-    const int K = a.E;  // keys = G * E_loc = E
-    const uint64_t step = *a.step;
-    const int64_t q = (int64_t)step * a.L + a.layer;
-    const int parity = (int)(q & 1);
-    const uint64_t epoch = (uint64_t)q + 1;
-    if (n > a.C) {
-        if (tid == 0) atomicExch(a.err, ERR_CAPACITY);
-        return;
-    }
-
-    if (tid < kMaxKeys) s_run[tid] = 0;
-    // pass 1: keys and per-key totals (warp-aggregated, atomic-free)
-    for (int base = 0; base < n; base += kDispThreads) {
-        const int t = base + tid;
-        int key = -1;
-        if (t < n) {
-            const int e = a.expert[t];
-            key = a.gpu_of[e] * a.E_loc + a.slot_of[e];
-            s_key[t] = key;
+    // ---- (2a) stable ranks inside this CTA's slice (warp 0, 32 tokens at a
+    //      time, atomic-free) and per-key counts
+    if (warp == 0) {
+        for (int b = 0; b < nt; b += 32) {
+            const int i = b + lane;
+            int key = -1;
+            if (i < nt) {
+                const int e = s_exp[i];
+                key = a.gpu_of[e] * a.E_loc + a.slot_of[e];
+            }
+            const uint32_t peers = __match_any_sync(0xffffffffu, key);
+            const int rank = __popc(peers & lanemask_lt());
+            if (key >= 0) s_pos[i] = (s_cnt[key] + rank) | (key << 20);  // in-CTA rank | key
+            __syncwarp();
+            if (key >= 0 && rank == 0) s_cnt[key] += __popc(peers);
+            __syncwarp();
         }
-        for (int k = lane; k < kMaxKeys; k += 32) s_wcnt[warp][k] = 0;
-        __syncwarp();
-        const uint32_t peers = __match_any_sync(0xffffffffu, key);
-        if (key >= 0 && (peers & lanemask_lt()) == 0) s_wcnt[warp][key] = __popc(peers);
-        __syncthreads();
-        if (tid < K) {
-            int s = 0;
-            for (int w = 0; w < kDispWarps; ++w) s += s_wcnt[w][tid];
-            s_run[tid] += s;
-        }
-        __syncthreads();
+        for (int k = lane; k < E; k += 32) a.cta_cnt[blockIdx.x * E + k] = s_cnt[k];
     }
+    // ---- (2b) publish counts, barrier over the active CTAs, key offsets
+    if (nactive > 1) grid_barrier(a.gbar, nactive, a.err);
+    else __syncthreads();
+    if (tid == 0) tl_mark(a.tl, 6);
+    if (tid < E) {
+        int tot = 0, before = 0;
+        for (int c = 0; c < (int)nactive; ++c) {
+            const int v = a.cta_cnt[c * E + tid];
+            tot += v;
+            before += (c < (int)blockIdx.x) ? v : 0;
+        }
+        s_tot[tid] = tot;
+        s_before[tid] = before;
+    }
+    __syncthreads();
     if (tid == 0) {
         int acc = 0;
-        for (int k = 0; k < K; ++k) {
+        for (int k = 0; k < E; ++k) {
             s_start[k] = acc;
-            acc += s_run[k];
+            acc += s_tot[k];
         }
-        s_start[K] = acc;
+        s_start[E] = acc;
     }
     __syncthreads();
-    // keep the per-key totals, reuse s_run as the running write cursor
-    int my_total = 0;
-    if (tid < K) {
-        my_total = s_run[tid];
-        s_run[tid] = s_start[tid];
-    }
-    __syncthreads();
-    // pass 2: stable positions = start[key] + tokens of this key in earlier
-    // chunks + earlier warps of this chunk + rank within the warp
-    for (int base = 0; base < n; base += kDispThreads) {
-        const int t = base + tid;
-        const int key = t < n ? s_key[t] : -1;
-        for (int k = lane; k < kMaxKeys; k += 32) s_wcnt[warp][k] = 0;
-        __syncwarp();
-        const uint32_t peers = __match_any_sync(0xffffffffu, key);
-        const int rank = __popc(peers & lanemask_lt());
-        if (key >= 0 && rank == 0) s_wcnt[warp][key] = __popc(peers);
-        __syncthreads();
-        if (tid < K) {  // exclusive prefix over warps for key `tid`
-            int run = s_run[tid];
-            for (int w = 0; w < kDispWarps; ++w) {
-                const int c = s_wcnt[w][tid];
-                s_wcnt[w][tid] = run;
-                run += c;
-            }
-            s_run[tid] = run;
-        }
-        __syncthreads();
-        if (key >= 0) s_pos[t] = s_wcnt[warp][key] + rank;
-        __syncthreads();
-    }
 
-    // copy rows: warp-granular, tokens strided over the whole grid
+    // ---- (3) rows straight from shared memory into the destination's
+    //      receive region (P2P stores for remote destinations)
     const int64_t row_bytes = (int64_t)a.d * 2;
-    const int vec_per_row = a.d >> 3;  // int4 per row
-    for (int t = blockIdx.x * kDispWarps + warp; t < n; t += gridDim.x * kDispWarps) {
-        const int key = s_key[t];
+    for (int i = warp; i < nt; i += kGdWarps) {
+        const int key = s_pos[i] >> 20;
         const int dest = key / a.E_loc;
-        const int local = s_pos[t] - s_start[dest * a.E_loc];
+        const int pos = s_start[key] + s_before[key] + (s_pos[i] & 0xFFFFF);
+        const int local = pos - s_start[dest * a.E_loc];
         uint8_t* pbase = a.peers[dest];
         const int64_t slot_row = ((int64_t)(parity * a.G + a.rank) * a.C + local);
         int4* dst = reinterpret_cast<int4*>(pbase + a.sym.recv_x + slot_row * row_bytes);
-        const int4* src = reinterpret_cast<const int4*>(a.res_x_in + (int64_t)t * a.d);
-        for (int v = lane; v < vec_per_row; v += 32) dst[v] = src[v];
+        const int4* src = reinterpret_cast<const int4*>(sx + (int64_t)i * a.d);
+        for (int v = lane; v < vec; v += 32) dst[v] = src[v];
         if (lane == 0) {
             RecvMeta m;
-            m.token = a.res_meta_in[t].token;
-            m.expert = a.expert[t];
-            m.prob = a.prob[t];
+            m.token = smeta[i].token;
+            m.expert = s_exp[i];
+            m.prob = s_prob[i];
             m.pad = 0;
             reinterpret_cast<RecvMeta*>(pbase + a.sym.recv_meta)[slot_row] = m;
         }
     }
-    // per-(src = me, slot) counts into every destination
-    if (blockIdx.x == 0 && tid < K) {
-        const int dest = tid / a.E_loc, slot = tid - dest * a.E_loc;
-        int32_t* cnt = reinterpret_cast<int32_t*>(a.peers[dest] + a.sym.recv_cnt);
-        cnt[((int64_t)parity * a.G + a.rank) * a.E_loc + slot] = my_total;
-    }
-    if (blockIdx.x == 0 && tid == 0) {
-        int stay = 0;
-        for (int s = 0; s < a.E_loc; ++s) stay += s_run[a.rank * a.E_loc + s] - s_start[a.rank * a.E_loc + s];
-        atomicAdd(&a.crossed[a.layer], (unsigned long long)(n - stay));
-    }
-    __threadfence_system();
     __syncthreads();
+    if (tid == 0) tl_mark(a.tl, 7);
+    // completion: one fence per CTA (cumulative over the CTA's stores through
+    // the barrier above) before the done-counter; the last CTA publishes
     if (tid == 0) {
-        const int prev = atomicAdd(a.done_ctr, 1);
-        if (prev == (int)gridDim.x - 1) {
-            __threadfence_system();
-            for (int p = 0; p < a.G; ++p) {
-                uint64_t* f = reinterpret_cast<uint64_t*>(a.peers[p] + a.sym.flags);
-                ptx::st_release_sys(f + parity * a.G + a.rank, epoch);
-            }
-            *a.done_ctr = 0;
+        if (nactive == 1) {
+            s_last = 1;
+        } else {
+            if (a.G > 1) __threadfence_system(); else __threadfence();
+            s_last = atomicAdd(a.done_ctr, 1) == (int)nactive - 1;
+            if (s_last) __threadfence();
         }
     }
+    __syncthreads();
+    if (tid == 0) tl_mark(a.tl, 3);
+    if (!s_last) return;
+    // ---- last CTA: per-(src = me, slot) counts, stats, release flags
+    if (tid < E) {
+        const int dest = tid / a.E_loc, slot = tid - dest * a.E_loc;
+        int32_t* cnt = reinterpret_cast<int32_t*>(a.peers[dest] + a.sym.recv_cnt);
+        cnt[((int64_t)parity * a.G + a.rank) * a.E_loc + slot] = s_tot[tid];
+    }
+    if (tid == 0) {
+        int stay = 0;
+        for (int s = 0; s < a.E_loc; ++s) stay += s_tot[a.rank * a.E_loc + s];
+        atomicAdd(&a.crossed[a.layer], (unsigned long long)(n - stay));
+    }
+    __syncthreads();  // counts and rows precede the release stores below
+    if (tid < a.G) {
+        uint64_t* f = reinterpret_cast<uint64_t*>(a.peers[tid] + a.sym.flags);
+        ptx::st_release_sys(f + parity * a.G + a.rank, epoch);
+    }
+    if (tid == 0 && nactive > 1) *a.done_ctr = 0;
+    if (tid == 0) tl_mark(a.tl, 3);
 }
 
 // ------------------------------------------------------------------ step begin
@@ -262,6 +314,8 @@ __global__ void __launch_bounds__(kDispThreads) dispatch_kernel(LayerArgs a) {
 __global__ void step_begin_kernel(const __nv_bfloat16* __restrict__ x_in, __nv_bfloat16* res_x,
                                   ResMeta* res_meta, int32_t* n_res, int B, int d, int G,
                                   int rank) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const int vec = d >> 3;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)B * vec;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -278,6 +332,8 @@ __global__ void __launch_bounds__(512) gather_send_kernel(
     const __nv_bfloat16* __restrict__ res_x, const ResMeta* __restrict__ res_meta,
     const int32_t* n_res, uint8_t* const* peers, Symm sym, int G, int rank, int d, int C,
     const uint64_t* step, int32_t* done_ctr, int32_t* err) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
     const int n = *n_res;
     const int vec = d >> 3;
@@ -293,12 +349,12 @@ __global__ void __launch_bounds__(512) gather_send_kernel(
         const int4* src = reinterpret_cast<const int4*>(res_x + (int64_t)r * d);
         for (int v = lane; v < vec; v += 32) dst[v] = src[v];
     }
-    __threadfence_system();
+    if (G > 1) __threadfence_system(); else __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
         const int prev = atomicAdd(done_ctr, 1);
         if (prev == (int)gridDim.x - 1) {
-            __threadfence_system();
+            if (G > 1) __threadfence_system(); else __threadfence();
             const uint64_t epoch = *step + 1;
             for (int p = 0; p < G; ++p)
                 ptx::st_release_sys(reinterpret_cast<uint64_t*>(peers[p] + sym.gflags) + rank, epoch);
@@ -309,6 +365,8 @@ __global__ void __launch_bounds__(512) gather_send_kernel(
 
 __global__ void gather_wait_kernel(uint8_t* own_sym, Symm sym, int G, uint64_t* step,
                                    int32_t* err) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
     const uint64_t epoch = *step + 1;
     if ((int)threadIdx.x < G) {
         const uint64_t* f = reinterpret_cast<const uint64_t*>(own_sym + sym.gflags) + threadIdx.x;
@@ -320,40 +378,54 @@ __global__ void gather_wait_kernel(uint8_t* own_sym, Symm sym, int G, uint64_t* 
 }
 
 // ------------------------------------------------------------------ launchers
-exf_status launch_gate(const LayerArgs& a, cudaStream_t s) {
-    const int blocks = (int)std::min<int64_t>(4 * 148, ((int64_t)a.C + 7) / 8);
-    const int bl = blocks < 1 ? 1 : blocks;
-    if (a.E <= 8) gate_kernel<8><<<bl, 256, 0, s>>>(a);
-    else if (a.E <= 16) gate_kernel<16><<<bl, 256, 0, s>>>(a);
-    else if (a.E <= 32) gate_kernel<32><<<bl, 256, 0, s>>>(a);
-    else gate_kernel<64><<<bl, 256, 0, s>>>(a);
-    EXF_LAUNCH_CHECK("gate_kernel");
-    return EXF_OK;
+// Tokens per CTA of gate_dispatch: the CTA stages its token rows (and, when
+// they fit, Wg) in shared memory; at most 128 CTAs so that all active CTAs
+// are co-resident for the grid barrier (model creation enforces C <= 128*tpc).
+constexpr size_t kGdSmemBudget = 200 * 1024;
+// one token per warp (16) so the gate spreads over ceil(n/16) SMs; larger
+// capacities grow the slice so the grid stays <= 128 CTAs
+int gate_dispatch_tpc(int C) {
+    int tpc = (C + 127) / 128;
+    tpc = ((tpc + 15) / 16) * 16;
+    return std::max(16, std::min(tpc, 256));
 }
 
-int dispatch_grid(int C) {
-    int g = (C + kDispWarps - 1) / kDispWarps;  // ~1 row per warp
-    return g < 1 ? 1 : (g > 132 ? 132 : g);
-}
-
-exf_status launch_dispatch(const LayerArgs& a, cudaStream_t s) {
-    const size_t smem = (size_t)a.C * 8;
-    static bool attr_done = false;
-    if (!attr_done) {
-        EXF_CUDA_TRY(cudaFuncSetAttribute(dispatch_kernel,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-        attr_done = true;
+exf_status launch_gate_dispatch(const LayerArgs& a, cudaStream_t s) {
+    if (a.E > kMaxKeys) return invalid("at most 64 experts");
+    if (a.tpc < 16 || a.tpc > 256) return invalid("bad gate_dispatch tile");
+    const int grid = (a.C + a.tpc - 1) / a.tpc;
+    if (grid > 128) return invalid("G*B exceeds the gate_dispatch capacity (128 CTAs)");
+    const size_t x_bytes = (size_t)a.tpc * (2 * a.d + 8);
+    if (x_bytes > kGdSmemBudget) return invalid("gate_dispatch token slice does not fit in shared memory");
+    const size_t wg_bytes = (size_t)a.E * a.d * 2;
+    const int in_smem = x_bytes + wg_bytes <= kGdSmemBudget ? 1 : 0;
+    const size_t smem = x_bytes + (in_smem ? wg_bytes : 0);
+    void (*k)(LayerArgs, int) = a.E <= 8    ? gate_dispatch_kernel<8>
+                                : a.E <= 16 ? gate_dispatch_kernel<16>
+                                : a.E <= 32 ? gate_dispatch_kernel<32>
+                                            : gate_dispatch_kernel<64>;
+    static bool attr = false;
+    if (!attr) {
+        for (auto kk : {gate_dispatch_kernel<8>, gate_dispatch_kernel<16>, gate_dispatch_kernel<32>,
+                        gate_dispatch_kernel<64>}) {
+            EXF_CUDA_TRY(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)kGdSmemBudget));
+            max_carveout(kk);
+        }
+        max_carveout(step_begin_kernel);
+        max_carveout(gather_send_kernel);
+        max_carveout(gather_wait_kernel);
+        attr = true;
     }
-    dispatch_kernel<<<dispatch_grid(a.C), kDispThreads, smem, s>>>(a);
-    EXF_LAUNCH_CHECK("dispatch_kernel");
+    EXF_CUDA_TRY(launch_pdl(k, dim3(grid), dim3(kGdThreads), smem, s, 0, a, in_smem));
     return EXF_OK;
 }
 
 exf_status launch_step_begin(const __nv_bfloat16* x_in, __nv_bfloat16* res_x, ResMeta* res_meta,
                              int32_t* n_res, int B, int d, int G, int rank, cudaStream_t s) {
     const int blocks = std::max(1, std::min(148, (int)(((int64_t)B * (d >> 3) + 255) / 256)));
-    step_begin_kernel<<<blocks, 256, 0, s>>>(x_in, res_x, res_meta, n_res, B, d, G, rank);
-    EXF_LAUNCH_CHECK("step_begin_kernel");
+    EXF_CUDA_TRY(launch_pdl(step_begin_kernel, dim3(blocks), dim3(256), 0, s, 0, x_in, res_x,
+                            res_meta, n_res, B, d, G, rank));
     return EXF_OK;
 }
 
@@ -362,16 +434,15 @@ exf_status launch_gather_send(const __nv_bfloat16* res_x, const ResMeta* res_met
                               int rank, int d, int C, const uint64_t* step, int32_t* done_ctr,
                               int32_t* err, cudaStream_t s) {
     const int blocks = std::max(1, std::min(132, (C * G + 15) / 16));
-    gather_send_kernel<<<blocks, 512, 0, s>>>(res_x, res_meta, n_res, peers, sym, G, rank, d, C,
-                                              step, done_ctr, err);
-    EXF_LAUNCH_CHECK("gather_send_kernel");
+    EXF_CUDA_TRY(launch_pdl(gather_send_kernel, dim3(blocks), dim3(512), 0, s, 0, res_x, res_meta,
+                            n_res, peers, sym, G, rank, d, C, step, done_ctr, err));
     return EXF_OK;
 }
 
 exf_status launch_gather_wait(uint8_t* own_sym, const Symm& sym, int G, uint64_t* step,
                               int32_t* err, cudaStream_t s) {
-    gather_wait_kernel<<<1, 32 * ((G + 31) / 32), 0, s>>>(own_sym, sym, G, step, err);
-    EXF_LAUNCH_CHECK("gather_wait_kernel");
+    EXF_CUDA_TRY(launch_pdl(gather_wait_kernel, dim3(1), dim3(32 * ((G + 31) / 32)), 0, s, 0,
+                            own_sym, sym, G, step, err));
     return EXF_OK;
 }
 

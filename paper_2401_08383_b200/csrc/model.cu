@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -20,8 +21,8 @@
 
 namespace exf {
 
-exf_status launch_gate(const LayerArgs& a, cudaStream_t s);
-exf_status launch_dispatch(const LayerArgs& a, cudaStream_t s);
+exf_status launch_gate_dispatch(const LayerArgs& a, cudaStream_t s);
+int gate_dispatch_tpc(int C);
 exf_status launch_step_begin(const __nv_bfloat16* x_in, __nv_bfloat16* res_x, ResMeta* res_meta,
                              int32_t* n_res, int B, int d, int G, int rank, cudaStream_t s);
 exf_status launch_gather_send(const __nv_bfloat16* res_x, const ResMeta* res_meta,
@@ -85,6 +86,8 @@ uint64_t gate_key(int layer) { return 0x6A7E000000000000ULL + (uint64_t)layer; }
 
 using namespace exf;
 
+constexpr int kTimelineCtas = 4096;
+
 struct exf_model {
     exf_model_config cfg{};
     int E_loc = 0, C = 0;
@@ -125,11 +128,15 @@ struct exf_model {
     uint64_t* step = nullptr;
     int32_t* err = nullptr;
     int32_t* done_ctr = nullptr;            // [2] dispatch, gather
+    int32_t* cta_cnt = nullptr;             // [128][E] gate_dispatch per-CTA key counts
+    uint32_t* gbar = nullptr;               // [2] gate_dispatch grid barrier
     int nmax = 64;
     int ks1 = 1, ks2 = 1;   // split-K (cluster size) of GEMM1 / GEMM2
     int cl1 = 1, cl2 = 1;   // persistent clusters of GEMM1 / GEMM2
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
+    uint64_t* tstamp = nullptr;             // FFN timeline stamps (EXF_FFN_TIMELINE=1)
+    unsigned long long* tl = nullptr;       // step timeline [L][3][4] (EXF_FFN_TIMELINE=1)
 };
 
 namespace {
@@ -154,7 +161,12 @@ exf_status validate_config(const exf_model_config& c) {
         return invalid("num_experts " + std::to_string(c.num_experts) + " not divisible by total GPUs " +
                        std::to_string(c.world_size));
     if (!(c.gate_affinity >= 0.f && c.gate_affinity <= 1.f)) return invalid("gate_affinity must be in [0,1]");
-    if ((int64_t)c.tokens_per_gpu * c.world_size > 16384) return invalid("G*B exceeds 16384 tokens");
+    {
+        const int64_t C = (int64_t)c.tokens_per_gpu * c.world_size;
+        if (C > 128LL * 256 || (int64_t)gate_dispatch_tpc((int)C) * (2 * c.d_model + 8) > 200 * 1024)
+            return invalid("G*B = " + std::to_string(C) + " tokens exceeds the dispatch capacity for d_model " +
+                           std::to_string(c.d_model));
+    }
     return EXF_OK;
 }
 
@@ -280,6 +292,10 @@ LayerArgs layer_args(exf_model* m, int j) {
     a.step = m->step;
     a.err = m->err;
     a.done_ctr = m->done_ctr;
+    a.cta_cnt = m->cta_cnt;
+    a.gbar = m->gbar;
+    a.tpc = gate_dispatch_tpc(m->C);
+    a.tl = m->tl ? m->tl + (int64_t)(j * 3) * 8 : nullptr;
     a.peers = m->d_peers;
     a.sym = m->sym;
     a.parity = 0;  // derived on device from the step counter
@@ -310,6 +326,8 @@ FfnArgs ffn_args(exf_model* m, int j, int mode) {
     a.res_meta_out = m->res_meta[(j + 1) & 1];
     a.n_res_out = m->n_res + ((j + 1) & 1);
     a.err = m->err;
+    a.tstamp = m->tstamp ? m->tstamp + (int64_t)mode * kTimelineCtas * 16 : nullptr;
+    a.tl = m->tl ? m->tl + (int64_t)(j * 3 + 1 + mode) * 8 : nullptr;
     return a;
 }
 
@@ -324,8 +342,7 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
         case 1: {
             if (j < 0 || j >= c.num_layers) return invalid("layer out of range");
             const LayerArgs a = layer_args(m, j);
-            EXF_TRY(launch_gate(a, s));
-            return launch_dispatch(a, s);
+            return launch_gate_dispatch(a, s);
         }
         case 2: {
             if (j < 0 || j >= c.num_layers) return invalid("layer out of range");
@@ -404,6 +421,12 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     EXF_M(dalloc(&m->step, 1));
     EXF_M(dalloc(&m->err, 1));
     EXF_M(dalloc(&m->done_ctr, 2));
+    EXF_M(dalloc(&m->cta_cnt, (size_t)128 * E));
+    EXF_M(dalloc(&m->gbar, 2));
+    if (std::getenv("EXF_FFN_TIMELINE")) {
+        EXF_M(dalloc(&m->tstamp, (size_t)2 * kTimelineCtas * 16));
+        EXF_M(dalloc(&m->tl, (size_t)L * 3 * 8));
+    }
     EXF_M(dalloc(&m->d_peers, (size_t)c.world_size));
     EXF_M(build_layout(m));
     EXF_M(make_gather_tmap(&m->gmap_recv, m->sym_base + m->sym.recv_x, 2LL * c.world_size * C, d));
@@ -411,7 +434,10 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     if (cudaMemset(m->trace, 0xff, sizeof(int32_t) * C * L) != cudaSuccess) return fail(EXF_CUDA);
     EXF_M(init_weights(m));
     // tile policy: token tile from the expected tokens per expert, split-K to fill 148 SMs
-    m->nmax = (2 * C / E <= 64) ? 64 : 128;
+    // expected tokens per expert under balanced routing is C/E; keep the tile
+    // at >= 2x that so skewed experts rarely need a second pass
+    m->nmax = (2 * C / E <= 32) ? 32 : ((2 * C / E <= 64) ? 64 : 128);
+    if (const char* env = std::getenv("EXF_TOKEN_TILE")) m->nmax = std::atoi(env);
     EXF_M(plan_ffn_gemm(m->nmax, 0, m->E_loc * (f / 128), d, &m->ks1, &m->cl1));
     EXF_M(plan_ffn_gemm(m->nmax, 1, m->E_loc * (d / 128), f, &m->ks2, &m->cl2));
     if (c.world_size == 1) {  // a single rank is its own peer
@@ -431,7 +457,8 @@ exf_status exf_model_destroy(exf_model* m) {
     void* bufs[] = {m->d_gpu_of, m->d_slot_of, m->wg, m->w1, m->b1, m->w2, m->b2, m->res_x[0],
                     m->res_x[1], m->res_meta[0], m->res_meta[1], m->n_res, m->expert, m->prob, m->H,
                     m->hist, m->crossed, m->trace, m->forced, m->step, m->err, m->done_ctr,
-                    m->d_peers, m->sym_base};
+                    m->cta_cnt, m->gbar, m->tl,
+                    m->d_peers, m->sym_base, m->tstamp};
     for (void* p : bufs)
         if (p) cudaFree(p);
     delete m;
@@ -646,7 +673,31 @@ exf_status exf_model_replay(exf_model* m, exf_stream_t stream) {
 
 int32_t exf_model_launches_per_step(exf_model* m) {
     if (!m) return 0;
-    return 1 + 4 * m->cfg.num_layers + 2;
+    return 1 + 3 * m->cfg.num_layers + 2;  // begin, L x (gate_dispatch, GEMM1, GEMM2), gather x2
+}
+
+exf_status exf_model_read_step_timeline(exf_model* m, uint64_t* h, int32_t reset) {
+    if (!m) return invalid("null model");
+    if (!m->tl) return invalid("timeline not enabled (set EXF_FFN_TIMELINE=1 before create)");
+    const int n = m->cfg.num_layers * 3;
+    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    if (h) EXF_CUDA_TRY(cudaMemcpy(h, m->tl, sizeof(uint64_t) * n * 8, cudaMemcpyDeviceToHost));
+    if (reset) {
+        std::vector<unsigned long long> init((size_t)n * 8, 0ull);
+        for (int i = 0; i < n; ++i) init[i * 8] = init[i * 8 + 1] = ~0ull;
+        EXF_CUDA_TRY(cudaMemcpy(m->tl, init.data(), sizeof(uint64_t) * n * 8, cudaMemcpyHostToDevice));
+    }
+    return EXF_OK;
+}
+
+exf_status exf_model_read_ffn_timeline(exf_model* m, uint64_t* h, int32_t ctas) {
+    if (!m || !h || ctas < 1 || ctas > kTimelineCtas) return invalid("bad argument");
+    if (!m->tstamp) return invalid("timeline not enabled (set EXF_FFN_TIMELINE=1 before create)");
+    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    for (int g = 0; g < 2; ++g)
+        EXF_CUDA_TRY(cudaMemcpy(h + (int64_t)g * ctas * 16, m->tstamp + (int64_t)g * kTimelineCtas * 16,
+                                sizeof(uint64_t) * ctas * 16, cudaMemcpyDeviceToHost));
+    return EXF_OK;
 }
 
 exf_status exf_model_describe(exf_model* m, char* buf, int32_t len) {

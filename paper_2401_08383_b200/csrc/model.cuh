@@ -59,11 +59,26 @@ struct LayerArgs {
     const uint64_t* step;           // device step counter
     int32_t* err;
     int32_t* done_ctr;              // last-CTA-done counter for dispatch
+    int32_t* cta_cnt;               // [grid][E] per-CTA key counts (gate_dispatch)
+    uint32_t* gbar;                 // [2] grid barrier {count, generation}
+    int32_t tpc;                    // tokens per CTA of gate_dispatch
     // peers' symmetric regions (index = rank), and this layer's parity
     uint8_t* const* peers;          // device array [G]
     Symm sym;
     int32_t parity;
+    unsigned long long* tl;         // optional step timeline [4] (diagnostics)
 };
+
+// Step timeline (diagnostics, EXF_FFN_TIMELINE=1): per (layer, kernel)
+// [0] min CTA entry, [1] min wait-return, [2] max wait-return, [3] max exit.
+__device__ __forceinline__ void tl_mark(unsigned long long* tl, int which) {
+    if (!tl) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if (which == 0 || which == 1) atomicMin(tl + which, t);
+    if (which == 1) atomicMax(tl + 2, t);
+    if (which >= 3) atomicMax(tl + which, t);  // 3 = exit, 4..7 = phase marks
+}
 
 // Arguments of one grouped-FFN GEMM launch (ffn_tcgen05.cu).
 struct FfnArgs {
@@ -77,6 +92,8 @@ struct FfnArgs {
     ResMeta* res_meta_out;       // [C]     (GEMM2)
     int32_t* n_res_out;          //         (GEMM2)
     int32_t* err;
+    uint64_t* tstamp;            // optional per-CTA globaltimer stamps [grid][16] (diagnostics)
+    unsigned long long* tl;      // optional step timeline [4] (diagnostics)
 };
 
 __host__ __device__ inline int64_t bytes_bf16(int64_t n) { return n * 2; }
