@@ -355,11 +355,14 @@ def main():
         "gpu_launches": launches * (a.steps) * n,
         "cpu_baseline": cpu,
     }
-    model.close()
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        sys.stdout.write(json.dumps(line) + "\n")
+        sys.stdout.flush()
+    log(f"[bench] rank {rank} done")
     if n > 1:
         dist.barrier()
+    model.close()
+    if n > 1:
         dist.destroy_process_group()
 
 
