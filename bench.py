@@ -158,6 +158,9 @@ def main():
 
     torch.cuda.set_device(local_rank)
     if n > 1:
+        # NCCL only carries control-plane traffic (IPC handles, histogram sum,
+        # max-over-ranks timing); keep its banner off stdout (one JSON line)
+        os.environ["NCCL_DEBUG"] = "WARN"
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     assert _capi.load().exf_device_ok() == 1, "libexflow_b200.so cannot see an sm_100 GPU"
     dev = torch.device("cuda", local_rank)

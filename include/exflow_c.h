@@ -218,6 +218,8 @@ exf_status exf_model_connect_local(exf_model* const* models, int32_t count);
 exf_status exf_model_step(exf_model* model, const void* d_x_in, exf_stream_t stream);
 /* Phased form for lock-step emulation of G ranks in one stream:
  * phase 0 begin(x_in) | 1 gate+dispatch(layer) | 2 ffn(layer) |
+ * 5 fused layer (gate..GEMM2 in one launch; needs every rank's kernel to run
+ * concurrently, i.e. one process or GPU per rank) |
  * 3 gather send | 4 gather wait. */
 exf_status exf_model_step_phase(exf_model* model, int32_t phase, int32_t layer,
                                 const void* d_x_in, exf_stream_t stream);

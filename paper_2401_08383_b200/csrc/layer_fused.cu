@@ -1,0 +1,866 @@
+// layer_fused.cu -- one MoE layer of the context-coherent decode step as ONE
+// persistent sm_100a kernel (one CTA per SM):
+//
+//   token phase (all warps of all CTAs)
+//     (1) gate GEMM + softmax/top-1 (fixed-order fp32, bit-exact with the
+//         oracle), fused affinity histogram and trace emission;
+//     (2) atomic-free stable bucketing by (dest GPU, local slot): per-CTA
+//         warp-aggregated ranks, one grid barrier, prefix over CTAs;
+//     (3) ExFlow's single dispatch exchange: rows stored straight into the
+//         destination rank's receive region (P2P over NVLink), last CTA
+//         publishes counts and release-flags every destination;
+//   expert phase (warp-specialised roles)
+//     (4) grouped expert FFN, GEMM1 then GEMM2, as uniform split-K "pieces"
+//         (item = expert x 128-row tile, k-range = kbp 64-wide blocks)
+//         statically round-robined over the CTAs: TMA weight tiles (A),
+//         TMA gather4 token rows (B), tcgen05.mma into double-buffered TMEM,
+//         epilogue either finishes the tile (1 piece) or parks an fp32 partial
+//         in a workspace slot; the last-arriving piece of a tile sums the
+//         partials in k order (deterministic) and applies bias+GELU (GEMM1)
+//         or bias, gate-prob scale and residual (GEMM2). GEMM2 pieces of an
+//         expert start once all its GEMM1 tiles are complete (per-expert
+//         counters; every CTA runs its GEMM1 pieces first and all CTAs are
+//         co-resident, so the wait always resolves).
+// Weights do not depend on the previous layer: the first weight stages are
+// prefetched before griddepcontrol.wait (PDL), overlapping the previous
+// kernel's tail. One launch per layer replaces gate/dispatch/GEMM1/GEMM2.
+#include "common.cuh"
+#include "model.cuh"
+#include "ptx.cuh"
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+namespace exf {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxLocal = 64;
+constexpr int kMaxKeys = 64;
+
+__device__ __forceinline__ void unpack8(const int4& v, float (&f)[8]) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 p = __bfloat1622float2(h[i]);
+        f[2 * i] = p.x;
+        f[2 * i + 1] = p.y;
+    }
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %lanemask_lt;" : "=r"(m));
+    return m;
+}
+__device__ __forceinline__ uint32_t ld_acq_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int32_t ld_acq_s32(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int32_t atom_add_acq_rel(int32_t* p, int32_t v) {
+    int32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void red_add_release(int32_t* p, int32_t v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ float gelu_erf(float v) {
+    return 0.5f * v * (1.0f + erff(v * 0.70710678118654752440f));
+}
+
+// All-to-all flag barrier: every CTA release-stores its own epoch slot, then
+// P threads acquire-poll all slots in parallel. No same-address atomics (a
+// 148-way atomic counter serialises for ~8 us at one L2 slice).
+__device__ void flag_barrier(uint64_t* slots, uint64_t epoch, int32_t* err) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(slots + blockIdx.x), "l"(epoch) : "memory");
+    }
+    if (threadIdx.x < gridDim.x) {
+        ptx::SpinGuard g;
+        for (;;) {
+            uint64_t v;
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(slots + threadIdx.x) : "memory");
+            if (v >= epoch) break;
+            g.step(err, ERR_TIMEOUT_PIPE);
+        }
+    }
+    __syncthreads();
+}
+
+__device__ void grid_barrier(uint32_t* gbar, int32_t* err) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t gen = ld_acq_u32(gbar + 1);
+        __threadfence();
+        const uint32_t prev = atomicAdd(gbar, 1u);
+        if (prev == gridDim.x - 1) {
+            gbar[0] = 0;
+            __threadfence();
+            atomicAdd(gbar + 1, 1u);
+        } else {
+            ptx::SpinGuard g;
+            while (ld_acq_u32(gbar + 1) == gen) g.step(err, ERR_TIMEOUT_PIPE);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// A (weights) and B (token rows) run in separate rings: the tiny token tiles
+// get a deeper ring so their gathers run ahead of the weight stream.
+template <int NMAX, int STAGES, int BST>
+struct Smem {
+    static constexpr int kA = kBM * kBK * 2;
+    static constexpr int kB = NMAX * kBK * 2;
+    static constexpr int kOffA = 0;
+    static constexpr int kOffB = STAGES * kA;
+    static constexpr int kOffTab = kOffB + BST * kB;
+    static constexpr int kTabInts = 20;  // n, off, seg_prefix[9], seg_start[8]
+    static constexpr int kOffBar = kOffTab + kMaxLocal * kTabInts * 4;
+    // fullA[S], emptyA[S], fullB[BST], emptyB[BST], tmem_full[NBUF<=4],
+    // tmem_empty[NBUF<=4], wg_bar
+    static constexpr int kOffMisc = kOffBar + (2 * STAGES + 2 * BST + 10) * 8;
+    static constexpr int kBytes = kOffMisc + 64 + 1024;
+};
+
+}  // namespace
+
+template <int NMAX, int STAGES, int BST, int EMAX, int NBUF = (NMAX <= 64 ? 4 : 2)>
+__global__ void __launch_bounds__(kThreads, 1)
+layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
+                   const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
+                   const FusedArgs a) {
+    using S = Smem<NMAX, STAGES, BST>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kOffBar);  // A ring
+    uint64_t* empty = full + STAGES;
+    uint64_t* fullB = empty + STAGES;  // B ring
+    uint64_t* emptyB = fullB + BST;
+    uint64_t* tmem_full = emptyB + BST;
+    uint64_t* tmem_empty = tmem_full + NBUF;
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + S::kOffMisc);
+    int32_t* tab = reinterpret_cast<int32_t*>(smem + S::kOffTab);
+
+    __shared__ int32_t s_exp[256];
+    __shared__ float s_prob[256];
+    __shared__ int32_t s_pos[256];
+    __shared__ int32_t s_cnt[kMaxKeys];
+    __shared__ int32_t s_tot[kMaxKeys];
+    __shared__ int32_t s_before[kMaxKeys];
+    __shared__ int32_t s_start[kMaxKeys + 1];
+    __shared__ int32_t s_flag;
+    __shared__ int64_t s_rrow[NMAX];
+    __shared__ float s_rprob[NMAX];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int P = gridDim.x;
+    const int mt1 = a.dff / kBM, mt2 = a.d / kBM;
+    const int NP1 = a.E_loc * mt1 * a.S1;
+    const int NP = NP1 + a.E_loc * mt2 * a.S2;
+    const int kbp = a.kbp;
+    if (tid == 0) tl_mark(a.tl, 0);
+    uint64_t* ts = a.tstamp ? a.tstamp + (int64_t)blockIdx.x * 16 : nullptr;
+    if (ts && tid == 0) ts[0] = ptx::globaltimer();
+    // second stamp row (diagnostics): [0..7] B producer at it = 0,2,..,14,
+    // [9]/[10] job-0 epilogue start/done, [11] job-1 epilogue start,
+    // [12] last epilogue done, [13] B done, [14] A done, [15] MMA done
+    uint64_t* ts2 = ts ? ts + 4096 * 16 : nullptr;
+
+    // piece p -> (gemm, expert, tile, k-part)
+    auto decode = [&](int p, int& g, int& e, int& mt, int& kp) {
+        if (p < NP1) {
+            g = 0;
+            kp = p % a.S1;
+            const int it = p / a.S1;
+            e = it / mt1;
+            mt = it - e * mt1;
+        } else {
+            g = 1;
+            const int q2 = p - NP1;
+            kp = q2 % a.S2;
+            const int it = q2 / a.S2;
+            e = it / mt2;
+            mt = it - e * mt2;
+        }
+    };
+
+    // ---------------- independent prologue (overlaps the previous kernel)
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < BST; ++s) {
+            ptx::mbar_init(&fullB[s], 32);  // one cp.async arrival per B-producer lane
+            ptx::mbar_init(&emptyB[s], 1);
+        }
+        for (int b = 0; b < NBUF; ++b) {
+            ptx::mbar_init(&tmem_full[b], 1);
+            ptx::mbar_init(&tmem_empty[b], 128);
+        }
+        ptx::mbar_init(&tmem_empty[NBUF], 1);  // Wg staging barrier
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(&misc[0], NBUF * NMAX);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = misc[0];
+    const int first_p = blockIdx.x < NP ? (int)blockIdx.x : -1;
+    const int npre = first_p >= 0 ? min(kbp, STAGES) : 0;
+    const uint64_t pol_a = ptx::policy_evict_first();
+    // the layer's gate matrix is a weight too: bulk-copy it into the B-stage
+    // region (unused until the expert phase) when it fits, before the wait
+    uint64_t* wg_bar = &tmem_empty[NBUF];
+    const uint32_t wg_bytes = (uint32_t)a.E * a.d * 2;
+    const bool wg_smem = wg_bytes <= (uint32_t)(BST * S::kB) && blockIdx.x * a.tpc < a.C;
+    if (warp == 0 && lane == 0) {
+        if (wg_smem) {
+            ptx::mbar_arrive_expect_tx(wg_bar, wg_bytes);
+            for (uint32_t o = 0; o < wg_bytes; o += 32768)
+                ptx::bulk_load(smem + S::kOffB + o, reinterpret_cast<const uint8_t*>(a.wg) + o,
+                               min(32768u, wg_bytes - o), wg_bar);
+        }
+        ptx::tma_prefetch_desc(&tmA1);
+        ptx::tma_prefetch_desc(&tmA2);
+        if (first_p >= 0) {
+            int g, e, mt, kp;
+            decode(first_p, g, e, mt, kp);
+            const CUtensorMap* tm = g == 0 ? &tmA1 : &tmA2;
+            const int rows = g == 0 ? a.dff : a.d;
+            for (int kb = 0; kb < npre; ++kb) {
+                ptx::mbar_arrive_expect_tx(&full[kb], S::kA);
+                ptx::tma_load_2d(smem + S::kOffA + kb * S::kA, tm, &full[kb], (kp * kbp + kb) * kBK,
+                                 e * rows + mt * kBM, pol_a);
+            }
+        }
+    }
+
+    // ---------------- dependent part
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    if (tid == 0) tl_mark(a.tl, 1);
+    const uint64_t q = *a.step * (uint64_t)a.L + (uint64_t)a.layer;
+    const int parity = (int)(q & 1);
+    const uint64_t epoch = q + 1;
+    const int n = *a.n_res_in;
+    if (n > a.C) {  // uniform: every CTA reads the same n
+        if (tid == 0) atomicExch(a.err, ERR_CAPACITY);
+        __trap();
+    }
+    // the next layer's GEMM1 counters start from zero
+    if (blockIdx.x == 0 && tid < a.E_loc) a.hdone[((parity ^ 1) * a.E_loc) + tid] = 0;
+
+    // ---------------- (1) gate, one warp per token
+    const int E = a.E;
+    const int t0 = blockIdx.x * a.tpc;
+    const int nt = max(0, min(a.tpc, n - t0));
+    if (tid < kMaxKeys) s_cnt[tid] = 0;
+    const int chunks = a.d >> 8;
+    const __nv_bfloat16* wgp = a.wg;
+    if (wg_smem) {
+        if (nt > 0) ptx::mbar_wait(wg_bar, 0, a.err, ERR_TIMEOUT_PIPE);
+        wgp = reinterpret_cast<const __nv_bfloat16*>(smem + S::kOffB);
+    }
+    for (int i = warp; i < nt; i += kWarps) {
+        const int t = t0 + i;
+        const __nv_bfloat16* x = a.res_x_in + (int64_t)t * a.d;
+        int4 xv[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            if (c < chunks) xv[c] = *reinterpret_cast<const int4*>(x + c * 256 + lane * 8);
+        float acc[EMAX];
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) acc[e] = 0.f;
+        // experts in groups of 8: issue all of a group's Wg loads for a chunk
+        // before the FMAs (independent L1/L2 round trips in flight); the
+        // per-expert accumulation order (c-major, k-minor) is unchanged
+#pragma unroll
+        for (int e0 = 0; e0 < EMAX; e0 += 8) {
+            if (e0 < E) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    if (c < chunks) {
+                        int4 wv[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (e0 + u < E)
+                                wv[u] = *reinterpret_cast<const int4*>(
+                                    wgp + (int64_t)(e0 + u) * a.d + c * 256 + lane * 8);
+                        float xf[8];
+                        unpack8(xv[c], xf);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            if (e0 + u < E) {
+                                float wf[8];
+                                unpack8(wv[u], wf);
+#pragma unroll
+                                for (int k = 0; k < 8; ++k) acc[e0 + u] = fmaf(xf[k], wf[k], acc[e0 + u]);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], off);
+        }
+        if (lane == 0) {
+            int best = 0;
+            float mx = acc[0];
+#pragma unroll
+            for (int e = 1; e < EMAX; ++e)
+                if (e < E && acc[e] > mx) {
+                    mx = acc[e];
+                    best = e;
+                }
+            float s = 0.f;
+#pragma unroll
+            for (int e = 0; e < EMAX; ++e)
+                if (e < E) s += expf(acc[e] - mx);
+            const ResMeta m = a.res_meta_in[t];
+            int sel = best;
+            float p = 1.f / s;
+            if (a.forced) {
+                sel = a.forced_routes[(int64_t)m.token * a.L + a.layer];
+                if ((unsigned)sel >= (unsigned)E) {
+                    atomicExch(a.err, ERR_BAD_EXPERT);
+                    sel = best;
+                }
+                float ls = acc[0];
+#pragma unroll
+                for (int e = 0; e < EMAX; ++e)
+                    if (e == sel) ls = acc[e];
+                p = expf(ls - mx) / s;
+            }
+            s_exp[i] = sel;
+            s_prob[i] = p;
+            if (a.hist && a.layer > 0 && m.prev_expert >= 0)
+                atomicAdd(&a.hist[((int64_t)(a.layer - 1) * E + m.prev_expert) * E + sel], 1ull);
+            if (a.trace) a.trace[(int64_t)m.token * a.L + a.layer] = sel;
+        }
+    }
+    __syncthreads();
+    // ---------------- (2) stable ranks within the CTA slice, per-key counts
+    if (warp == 0) {
+        for (int b = 0; b < nt; b += 32) {
+            const int i = b + lane;
+            int key = -1;
+            if (i < nt) {
+                const int e = s_exp[i];
+                key = a.gpu_of[e] * a.E_loc + a.slot_of[e];
+            }
+            const uint32_t peers = __match_any_sync(0xffffffffu, key);
+            const int rank = __popc(peers & lanemask_lt());
+            if (key >= 0) s_pos[i] = (s_cnt[key] + rank) | (key << 20);
+            __syncwarp();
+            if (key >= 0 && rank == 0) s_cnt[key] += __popc(peers);
+            __syncwarp();
+        }
+        for (int k = lane; k < E; k += 32) a.cta_cnt[blockIdx.x * E + k] = s_cnt[k];
+    }
+    if (tid == 0) tl_mark(a.tl, 4);
+    // launch epoch: slots [0, P) are per-CTA barrier flags, slot 256 the counter
+    uint64_t* bslots = reinterpret_cast<uint64_t*>(a.gbar);
+    const uint64_t bepoch = bslots[256] + 1;
+    flag_barrier(bslots, bepoch, a.err);
+    if (tid == 0) tl_mark(a.tl, 5);
+    if (tid < E) {
+        int tot = 0, before = 0;
+        for (int c = 0; c < P; ++c) {
+            const int v = a.cta_cnt[c * E + tid];
+            tot += v;
+            before += (c < (int)blockIdx.x) ? v : 0;
+        }
+        s_tot[tid] = tot;
+        s_before[tid] = before;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int acc = 0;
+        for (int k = 0; k < E; ++k) {
+            s_start[k] = acc;
+            acc += s_tot[k];
+        }
+        s_start[E] = acc;
+    }
+    __syncthreads();
+    // ---------------- (3) dispatch: rows straight into the destination region
+    {
+        const int64_t row_bytes = (int64_t)a.d * 2;
+        const int vec = a.d >> 3;
+        for (int i = warp; i < nt; i += kWarps) {
+            const int t = t0 + i;
+            const int key = s_pos[i] >> 20;
+            const int dest = key / a.E_loc;
+            const int pos = s_start[key] + s_before[key] + (s_pos[i] & 0xFFFFF);
+            const int local = pos - s_start[dest * a.E_loc];
+            uint8_t* pbase = a.peers[dest];
+            const int64_t slot_row = ((int64_t)(parity * a.G + a.rank) * a.C + local);
+            int4* dst = reinterpret_cast<int4*>(pbase + a.sym.recv_x + slot_row * row_bytes);
+            const int4* src = reinterpret_cast<const int4*>(a.res_x_in + (int64_t)t * a.d);
+            int4 buf[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (u * 32 + lane < vec) buf[u] = src[u * 32 + lane];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (u * 32 + lane < vec) dst[u * 32 + lane] = buf[u];
+            for (int v = 256 + lane; v < vec; v += 32) dst[v] = src[v];
+            if (lane == 0) {
+                RecvMeta m;
+                m.token = a.res_meta_in[t].token;
+                m.expert = s_exp[i];
+                m.prob = s_prob[i];
+                m.pad = 0;
+                reinterpret_cast<RecvMeta*>(pbase + a.sym.recv_meta)[slot_row] = m;
+            }
+        }
+    }
+    __syncthreads();
+    // completion among the CTAs that own tokens (CTA 0 always takes part)
+    const int nact = max(1, (n + a.tpc - 1) / a.tpc);
+    if (tid == 0) {
+        if (nact == 1) {
+            s_flag = blockIdx.x == 0;
+        } else if ((int)blockIdx.x < nact) {
+            if (a.G > 1) __threadfence_system(); else __threadfence();
+            s_flag = atomicAdd(a.done_ctr, 1) == nact - 1;
+            if (s_flag) __threadfence();
+        } else {
+            s_flag = 0;
+        }
+    }
+    __syncthreads();
+    if (s_flag) {  // last CTA: per-(src = me, slot) counts, stats, release flags
+        if (tid < E) {
+            const int dest = tid / a.E_loc, slot = tid - dest * a.E_loc;
+            int32_t* cnt = reinterpret_cast<int32_t*>(a.peers[dest] + a.sym.recv_cnt);
+            cnt[((int64_t)parity * a.G + a.rank) * a.E_loc + slot] = s_tot[tid];
+        }
+        if (tid == 0) {
+            int stay = 0;
+            for (int s2 = 0; s2 < a.E_loc; ++s2) stay += s_tot[a.rank * a.E_loc + s2];
+            atomicAdd(&a.crossed[a.layer], (unsigned long long)(n - stay));
+            *a.done_ctr = 0;
+        }
+        __syncthreads();
+        if (tid < a.G) {
+            uint64_t* f = reinterpret_cast<uint64_t*>(a.peers[tid] + a.sym.flags);
+            ptx::st_release_sys(f + parity * a.G + a.rank, epoch);
+        }
+    }
+    if (tid == 0) tl_mark(a.tl, 6);
+    // ---------------- wait for every source's dispatch, build the tables
+    if (tid < a.G) {
+        const uint64_t* f = reinterpret_cast<const uint64_t*>(a.own_sym + a.sym.flags) + parity * a.G + tid;
+        ptx::SpinGuard g;
+        while (ptx::ld_acquire_sys(f) < epoch) g.step(a.err, ERR_TIMEOUT_DISPATCH);
+    }
+    __syncthreads();
+    const int32_t* cnt = reinterpret_cast<const int32_t*>(a.own_sym + a.sym.recv_cnt) +
+                         (int64_t)parity * a.G * a.E_loc;
+    if (tid < a.E_loc) {
+        const int e = tid;
+        int32_t* t = tab + e * S::kTabInts;
+        int nn = 0, off = 0;
+        for (int s2 = 0; s2 < a.G; ++s2) {
+            int st = 0;
+            for (int x = 0; x < e; ++x) st += cnt[s2 * a.E_loc + x];
+            off += st;
+            t[2 + s2] = nn;
+            t[11 + s2] = st;
+            nn += cnt[s2 * a.E_loc + e];
+        }
+        t[2 + a.G] = nn;
+        t[0] = nn;
+        t[1] = off;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        int total = 0;
+        for (int i = 0; i < a.G * a.E_loc; ++i) total += cnt[i];
+        *a.n_res_out = total;
+    }
+    __syncthreads();
+    if (tid == 0) tl_mark(a.tl, 7);
+    if (ts && tid == 0) ts[1] = ptx::globaltimer();
+
+    const RecvMeta* rmeta = reinterpret_cast<const RecvMeta*>(a.own_sym + a.sym.recv_meta);
+    const __nv_bfloat16* rx = reinterpret_cast<const __nv_bfloat16*>(a.own_sym + a.sym.recv_x);
+    auto recv_row = [&](int e, int i) -> int64_t {
+        const int32_t* t = tab + e * S::kTabInts;
+        int s2 = 0;
+        while (s2 + 1 < a.G && t[2 + s2 + 1] <= i) ++s2;
+        return ((int64_t)parity * a.G + s2) * a.C + t[11 + s2] + (i - t[2 + s2]);
+    };
+    // chunks of piece p (the CTA's first piece always runs >= 1: prefetched)
+    auto nchunks = [&](int p, int e) {
+        const int c = (tab[e * S::kTabInts] + NMAX - 1) / NMAX;
+        return (p == first_p && c == 0) ? 1 : c;
+    };
+    auto slot_of_tile = [&](int g, int e, int mt, int c) -> int64_t {
+        const int64_t base = g == 0 ? 0 : (int64_t)a.E_loc * mt1 * a.max_chunks;
+        const int mts = g == 0 ? mt1 : mt2;
+        return base + ((int64_t)e * mts + mt) * a.max_chunks + c;
+    };
+
+    if (warp == 0) {
+        // ================= A producer: weight tiles via TMA =================
+        if (lane == 0) {
+            int it = 0;
+            for (int p = blockIdx.x; p < NP; p += P) {
+                int g, e, mt, kp;
+                decode(p, g, e, mt, kp);
+                const int nch = nchunks(p, e);
+                const CUtensorMap* tm = g == 0 ? &tmA1 : &tmA2;
+                const int rows = g == 0 ? a.dff : a.d;
+                for (int c = 0; c < nch; ++c)
+                    for (int kb = 0; kb < kbp; ++kb, ++it) {
+                        if (it < npre) continue;
+                        const int st = it % STAGES;
+                        const uint32_t ph = (it / STAGES) & 1;
+                        ptx::mbar_wait(&empty[st], ph ^ 1, a.err, ERR_TIMEOUT_PIPE);
+                        if (ts && it == kbp) ts[12] = ptx::globaltimer();  // job 1's first A tile
+                        ptx::mbar_arrive_expect_tx(&full[st], S::kA);
+                        if (a.a_probe) {
+                            const int kt = (g == 0 ? a.d : a.dff) / kBK;
+                            const __nv_bfloat16* wt = (g == 0 ? a.w1 : a.w2) +
+                                (((int64_t)e * (rows / kBM) + mt) * kt + kp * kbp + kb) * (kBM * kBK);
+                            ptx::bulk_load(smem + S::kOffA + st * S::kA, wt, S::kA, &full[st]);
+                        } else {
+                            ptx::tma_load_2d(smem + S::kOffA + st * S::kA, tm, &full[st],
+                                             (kp * kbp + kb) * kBK, e * rows + mt * kBM, pol_a);
+                        }
+                    }
+            }
+            if (ts2) ts2[14] = ptx::globaltimer();
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer =================
+        int it = 0, job = 0;
+        for (int p = blockIdx.x; p < NP; p += P) {
+            int g, e, mt, kp;
+            decode(p, g, e, mt, kp);
+            const int n_e = tab[e * S::kTabInts];
+            const int nch = nchunks(p, e);
+            for (int c = 0; c < nch; ++c, ++job) {
+                const int nc = max(0, min(NMAX, n_e - c * NMAX));
+                const int ncol = max(16, (nc + 15) & ~15);
+                const uint32_t idesc = ptx::umma_idesc_bf16(kBM, ncol);
+                const int buf = job % NBUF;
+                if (job >= NBUF) ptx::mbar_wait(&tmem_empty[buf], ((job / NBUF) - 1) & 1, a.err, ERR_TIMEOUT_PIPE);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem + buf * NMAX;
+                for (int kb = 0; kb < kbp; ++kb, ++it) {
+                    const int st = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    const int sb = it % BST;
+                    ptx::mbar_wait(&fullB[sb], (it / BST) & 1, a.err, ERR_TIMEOUT_PIPE);
+                    if (ts2 && lane == 0 && it == kbp) ts2[8] = ptx::globaltimer();
+                    ptx::mbar_wait(&full[st], ph, a.err, ERR_TIMEOUT_PIPE);
+                    if (ts2 && lane == 0 && it == kbp) ts2[9] = ptx::globaltimer();
+                    ptx::tc_fence_after();
+                    ptx::fence_proxy_async_smem();  // cp.async (generic) rows -> tensor-core reads
+                    if (lane == 0) {
+                        const uint64_t da = ptx::umma_desc_sw128(ptx::smem_u32(smem + S::kOffA + st * S::kA));
+                        const uint64_t db = ptx::umma_desc_sw128(ptx::smem_u32(smem + S::kOffB + sb * S::kB));
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 16; ++kk)
+                            ptx::umma_bf16(d_tmem, da + 2 * kk, db + 2 * kk, idesc, (kb | kk) ? 1u : 0u);
+                        ptx::umma_commit(&empty[st]);
+                        ptx::umma_commit(&emptyB[sb]);
+                        if (kb == kbp - 1) ptx::umma_commit(&tmem_full[buf]);
+                        if (ts && kb == 0 && job < 6) ts[2 + 2 * job] = ptx::globaltimer();
+                        if (ts && kb == kbp - 1 && job < 6) ts[3 + 2 * job] = ptx::globaltimer();
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        if (ts2 && lane == 0) ts2[15] = ptx::globaltimer();
+    } else if (warp == 2) {
+        // ====== B producer: the expert's token rows via cp.async (LSU path) ======
+        // Token tiles are tiny (NMAX rows x 128 B per k-block); as TMA gathers
+        // they queued behind the 16 KB weight boxes and stalled the MMA at every
+        // job boundary. Each lane copies 16-byte chunk (lane & 7) of rows
+        // (lane >> 3) + 4j into the SW128 layout the UMMA descriptor expects,
+        // and arrives on fullB (count 32) when its copies land.
+        const int cc = lane & 7;
+        int it = 0;
+        int waited_e = -1;
+        for (int p = blockIdx.x; p < NP; p += P) {
+            int g, e, mt, kp;
+            decode(p, g, e, mt, kp);
+            const int n_e = tab[e * S::kTabInts];
+            const int off_e = tab[e * S::kTabInts + 1];
+            const int nch = nchunks(p, e);
+            if (g == 1 && nch > 0 && waited_e != e) {
+                // all GEMM1 (tile, chunk) units of expert e must be complete
+                const int target = mt1 * ((n_e + NMAX - 1) / NMAX);
+                ptx::SpinGuard sg;
+                while (ld_acq_s32(a.hdone + parity * a.E_loc + e) < target) sg.step(a.err, ERR_TIMEOUT_PIPE);
+                waited_e = e;
+            }
+            const __nv_bfloat16* src = g == 0 ? rx : a.H;
+            const int ld = g == 0 ? a.d : a.dff;
+            const int row_lim = g == 0 ? 2 * a.G * a.C : a.C;
+            for (int c = 0; c < nch; ++c) {
+                const int cb = c * NMAX;
+                const int nc = max(0, min(NMAX, n_e - cb));
+                const int ncol = max(16, (nc + 15) & ~15);
+                int32_t rows[NMAX / 4];
+#pragma unroll
+                for (int j = 0; j < NMAX / 4; ++j) {
+                    const int r = (lane >> 3) + 4 * j;
+                    const int i = cb + (r < nc ? r : 0);
+                    const int64_t row = g == 0 ? recv_row(e, i) : (int64_t)(off_e + i);
+                    rows[j] = (int32_t)(row < 0 ? 0 : (row >= row_lim ? row_lim - 1 : row));
+                }
+                for (int kb = 0; kb < kbp; ++kb, ++it) {
+                    const int sb = it % BST;
+                    ptx::mbar_wait(&emptyB[sb], ((it / BST) & 1) ^ 1, a.err, ERR_TIMEOUT_PIPE);
+                    if (ts && lane == 0 && it == kbp) ts[13] = ptx::globaltimer();  // job 1's first B rows
+                    if (ts2 && lane == 0 && it < 16 && !(it & 1)) ts2[it >> 1] = ptx::globaltimer();
+                    uint8_t* sbase = smem + S::kOffB + sb * S::kB;
+                    const __nv_bfloat16* kcol = src + (int64_t)(kp * kbp + kb) * kBK + cc * 8;
+#pragma unroll
+                    for (int j = 0; j < NMAX / 4; ++j) {
+                        const int r = (lane >> 3) + 4 * j;
+                        if (4 * j < ncol)
+                            ptx::cp_async16(sbase + r * 128 + ((cc ^ (r & 7)) << 4), kcol + (int64_t)rows[j] * ld);
+                    }
+                    ptx::cp_async_arrive_noinc(&fullB[sb]);
+                }
+            }
+        }
+        if (ts2 && lane == 0) ts2[13] = ptx::globaltimer();
+    } else if (warp >= 4) {
+        // ================= epilogue =================
+        const int et = tid - 128;  // TMEM lane == weight row within the tile
+        const int lane_base = (warp & 3) * 32;
+        int job = 0;
+        for (int p = blockIdx.x; p < NP; p += P) {
+            int g, e, mt, kp;
+            decode(p, g, e, mt, kp);
+            const int n_e = tab[e * S::kTabInts];
+            const int off_e = tab[e * S::kTabInts + 1];
+            const int nch = nchunks(p, e);
+            const int Sg = g == 0 ? a.S1 : a.S2;
+            const int mrows = g == 0 ? a.dff : a.d;
+            const int m_glob = mt * kBM + et;
+            const float bias = __bfloat162float((g == 0 ? a.b1 : a.b2)[(int64_t)e * mrows + m_glob]);
+            for (int c = 0; c < nch; ++c, ++job) {
+                const int cb = c * NMAX;
+                const int nc = max(0, min(NMAX, n_e - cb));
+                const int buf = job % NBUF;
+                if (ts2 && et == 0 && job == 1) ts2[11] = ptx::globaltimer();
+                ptx::mbar_wait(&tmem_full[buf], (job / NBUF) & 1, a.err, ERR_TIMEOUT_PIPE);
+                if (ts2 && et == 0 && job == 0) ts2[10] = ptx::globaltimer();
+                ptx::tc_fence_after();
+                const uint32_t t_base = tmem + buf * NMAX + ((uint32_t)lane_base << 16);
+                float accv[NMAX];
+#pragma unroll
+                for (int col = 0; col < NMAX; col += 16) {
+                    if (col < nc) {
+                        uint32_t r[16];
+                        ptx::tmem_ld_32x32b_x16(t_base + col, r);
+                        ptx::tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) accv[col + i] = __uint_as_float(r[i]);
+                    }
+                }
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&tmem_empty[buf]);
+                if (nc == 0) continue;  // prefetched first piece of an empty expert
+                bool finish = true;
+                const int64_t slot = slot_of_tile(g, e, mt, c);
+                if (Sg > 1) {
+                    // park the partial; the last-arriving piece of this tile
+                    // reduces all partials in k order (deterministic)
+                    const int Smax = max(a.S1, a.S2);
+                    float* wsp = a.ws + ((slot * Smax + kp) * NMAX) * kBM;
+#pragma unroll
+                    for (int i = 0; i < NMAX; ++i)
+                        if (i < nc) __stcg(wsp + i * kBM + et, accv[i]);
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (et == 0) {
+                        const int prev = atom_add_acq_rel(a.item_ctr + slot, 1);  // release partials
+                        s_flag = (prev == Sg - 1);
+                        if (s_flag) a.item_ctr[slot] = 0;  // next use is a later launch
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    finish = s_flag;
+                    if (finish) {
+                        // k-ordered sum; one batch of independent loads per
+                        // (k, 16 tokens) instead of a dependent chain per token
+                        const float* w0 = a.ws + (slot * Smax * NMAX) * kBM;
+#pragma unroll
+                        for (int i = 0; i < NMAX; ++i) accv[i] = 0.f;
+                        for (int k = 0; k < Sg; ++k) {
+                            const float* wk = w0 + (int64_t)k * NMAX * kBM + et;
+#pragma unroll
+                            for (int i0 = 0; i0 < NMAX; i0 += 16) {
+                                if (i0 < nc) {
+                                    float v[16];
+#pragma unroll
+                                    for (int i = 0; i < 16; ++i) v[i] = i0 + i < nc ? __ldcg(wk + (i0 + i) * kBM) : 0.f;
+#pragma unroll
+                                    for (int i = 0; i < 16; ++i) accv[i0 + i] += v[i];
+                                }
+                            }
+                        }
+                    }
+                }
+                if (!finish) continue;
+                if (g == 0) {
+#pragma unroll
+                    for (int i = 0; i < NMAX; ++i)
+                        if (i < nc)
+                            a.H[(int64_t)(off_e + cb + i) * a.dff + m_glob] = __float2bfloat16(gelu_erf(accv[i] + bias));
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (et == 0) red_add_release(a.hdone + parity * a.E_loc + e, 1);
+                } else {
+                    // per-token receive row and gate prob, resolved once per job
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (et < nc) {
+                        const int64_t rr = recv_row(e, cb + et);
+                        s_rrow[et] = rr;
+                        s_rprob[et] = rmeta[rr].prob;
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+                    for (int i0 = 0; i0 < NMAX; i0 += 16) {
+                        if (i0 < nc) {
+                            __nv_bfloat16 xin[16];  // batch the residual loads
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (i0 + i < nc) xin[i] = rx[s_rrow[i0 + i] * a.d + m_glob];
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (i0 + i < nc)
+                                    a.res_x_out[(int64_t)(off_e + cb + i0 + i) * a.d + m_glob] = __float2bfloat16(
+                                        __bfloat162float(xin[i]) + s_rprob[i0 + i] * (accv[i0 + i] + bias));
+                        }
+                    }
+                    if (mt == 0 && et < nc) {
+                        const RecvMeta m = rmeta[recv_row(e, cb + et)];
+                        a.res_meta_out[off_e + cb + et] = ResMeta{m.token, m.expert};
+                    }
+                }
+            }
+        }
+        if (ts2 && et == 0) ts2[12] = ptx::globaltimer();
+    }
+    __syncthreads();
+    if (tid == 0) tl_mark(a.tl, 3);
+    if (ts && tid == 0) ts[15] = ptx::globaltimer();
+    // every CTA read the launch epoch before arriving at the barrier, which
+    // CTA 0 passed before getting here: safe to advance it
+    if (blockIdx.x == 0 && tid == 0) bslots[256] = bepoch;
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, NBUF * NMAX);
+    }
+}
+
+// ------------------------------------------------------------------ host side
+namespace {
+
+template <int NMAX, int STAGES, int BST, int EMAX>
+struct FusedLauncher {
+    using Sm = Smem<NMAX, STAGES, BST>;
+    static constexpr auto kern = layer_fused_kernel<NMAX, STAGES, BST, EMAX>;
+    int ctas = 0;
+    exf_status prepare() {
+        if (ctas) return EXF_OK;
+        EXF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Sm::kBytes));
+        max_carveout(kern);
+        int per_sm = 0;
+        EXF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, Sm::kBytes));
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (per_sm < 1) return runtime_err("fused layer kernel cannot be resident");
+        ctas = sms;  // one persistent CTA per SM (all co-resident: grid barrier)
+        return EXF_OK;
+    }
+    exf_status launch(const CUtensorMap* maps, const FusedArgs& a, cudaStream_t s) {
+        EXF_TRY(prepare());
+        EXF_CUDA_TRY(launch_pdl(kern, dim3(ctas), dim3(kThreads), Sm::kBytes, s, 0, maps[0], maps[1],
+                                maps[2], maps[3], a));
+        return EXF_OK;
+    }
+};
+
+template <int NMAX, int STAGES, int BST>
+exf_status launch_nmax(const CUtensorMap* maps, const FusedArgs& a, cudaStream_t s) {
+    static FusedLauncher<NMAX, STAGES, BST, 8> l8;
+    static FusedLauncher<NMAX, STAGES, BST, 16> l16;
+    static FusedLauncher<NMAX, STAGES, BST, 32> l32;
+    static FusedLauncher<NMAX, STAGES, BST, 64> l64;
+    if (a.E <= 8) return l8.launch(maps, a, s);
+    if (a.E <= 16) return l16.launch(maps, a, s);
+    if (a.E <= 32) return l32.launch(maps, a, s);
+    return l64.launch(maps, a, s);
+}
+
+}  // namespace
+
+int fused_ctas() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+// Uniform split-K piece size: the largest kbp (64-wide k-blocks per piece)
+// dividing both K's that minimises rounds(pieces / CTAs) * kbp.
+void plan_fused(int E_loc, int d, int dff, int ctas, int* kbp_out, int* S1, int* S2) {
+    const int k1 = d / kBK, k2 = dff / kBK;
+    long best = -1;
+    int best_kbp = 1;
+    for (int kbp = 32; kbp >= 1; kbp /= 2) {
+        if (k1 % kbp || k2 % kbp) continue;
+        const long np = (long)E_loc * (dff / kBM) * (k1 / kbp) + (long)E_loc * (d / kBM) * (k2 / kbp);
+        // each piece also pays a pipeline/epilogue overhead worth ~4 k-blocks
+        const long cost = ((np + ctas - 1) / ctas) * (kbp + 4);
+        if (best < 0 || cost < best) {
+            best = cost;
+            best_kbp = kbp;
+        }
+    }
+    *kbp_out = best_kbp;
+    *S1 = k1 / best_kbp;
+    *S2 = k2 / best_kbp;
+}
+
+exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int nmax, cudaStream_t s) {
+    if (a.E > kMaxKeys || a.E_loc > kMaxLocal) return invalid("at most 64 experts");
+    if (a.d > 2048) return invalid("fused layer kernel supports d_model <= 2048");
+    if (a.tpc > 256) return invalid("token slice too large for the fused layer kernel");
+    // (token tile, weight stages, token stages): ~208 KB of rings each
+    if (nmax <= 32) return launch_nmax<32, 10, 12>(maps, a, s);
+    if (nmax <= 64) return launch_nmax<64, 8, 10>(maps, a, s);
+    return launch_nmax<128, 6, 7>(maps, a, s);
+}
+
+}  // namespace exf

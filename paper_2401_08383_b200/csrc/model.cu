@@ -37,6 +37,9 @@ exf_status launch_ffn_gemm(const CUtensorMap& map, const CUtensorMap& mapB, cons
                            int nmax, int clusters, cudaStream_t s);
 exf_status make_gather_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols);
 exf_status plan_ffn_gemm(int nmax, int mode, int items, int K, int* ksplit, int* clusters);
+exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int nmax, cudaStream_t s);
+void plan_fused(int E_loc, int d, int dff, int ctas, int* kbp, int* S1, int* S2);
+int fused_ctas();
 
 namespace {
 
@@ -130,6 +133,14 @@ struct exf_model {
     int32_t* done_ctr = nullptr;            // [2] dispatch, gather
     int32_t* cta_cnt = nullptr;             // [128][E] gate_dispatch per-CTA key counts
     uint32_t* gbar = nullptr;               // [2] gate_dispatch grid barrier
+    // fused layer kernel (one launch per layer)
+    bool fused = true;
+    int f_ctas = 148, f_tpc = 8, f_kbp = 8, f_S1 = 1, f_S2 = 1, f_max_chunks = 1;
+    float* ws = nullptr;                    // split-K partials
+    int32_t* item_ctr = nullptr;            // split-K arrivals per tile/chunk
+    int32_t* hdone = nullptr;               // [2][E_loc]
+    uint32_t* fbar = nullptr;               // [2] grid barrier of the fused kernel
+    int32_t* f_cta_cnt = nullptr;           // [ctas][E]
     int nmax = 64;
     int ks1 = 1, ks2 = 1;   // split-K (cluster size) of GEMM1 / GEMM2
     int cl1 = 1, cl2 = 1;   // persistent clusters of GEMM1 / GEMM2
@@ -331,10 +342,68 @@ FfnArgs ffn_args(exf_model* m, int j, int mode) {
     return a;
 }
 
+FusedArgs fused_args(exf_model* m, int j) {
+    const auto& c = m->cfg;
+    FusedArgs a{};
+    a.G = c.world_size;
+    a.rank = c.rank;
+    a.E = c.num_experts;
+    a.E_loc = m->E_loc;
+    a.d = c.d_model;
+    a.dff = c.d_ffn;
+    a.C = m->C;
+    a.L = c.num_layers;
+    a.layer = j;
+    a.forced = m->forced_on ? 1 : 0;
+    a.tpc = m->f_tpc;
+    a.wg = m->wg + (int64_t)j * c.num_experts * c.d_model;
+    a.gpu_of = m->d_gpu_of + j * c.num_experts;
+    a.slot_of = m->d_slot_of + j * c.num_experts;
+    a.res_x_in = m->res_x[j & 1];
+    a.res_meta_in = m->res_meta[j & 1];
+    a.n_res_in = m->n_res + (j & 1);
+    a.hist = m->hist;
+    a.crossed = m->crossed;
+    a.trace = m->trace;
+    a.forced_routes = m->forced;
+    a.step = m->step;
+    a.err = m->err;
+    a.done_ctr = m->done_ctr;
+    a.cta_cnt = m->f_cta_cnt;
+    a.gbar = m->fbar;
+    a.peers = m->d_peers;
+    a.own_sym = m->sym_base;
+    a.sym = m->sym;
+    a.H = m->H;
+    a.b1 = m->b1 + (int64_t)j * m->E_loc * c.d_ffn;
+    a.b2 = m->b2 + (int64_t)j * m->E_loc * c.d_model;
+    a.w1 = m->w1 + (int64_t)j * m->E_loc * c.d_ffn * c.d_model;
+    a.w2 = m->w2 + (int64_t)j * m->E_loc * c.d_ffn * c.d_model;
+    a.a_probe = getenv("EXF_A_PROBE") ? 1 : 0;
+    a.res_x_out = m->res_x[(j + 1) & 1];
+    a.res_meta_out = m->res_meta[(j + 1) & 1];
+    a.n_res_out = m->n_res + ((j + 1) & 1);
+    a.ws = m->ws;
+    a.item_ctr = m->item_ctr;
+    a.hdone = m->hdone;
+    a.S1 = m->f_S1;
+    a.S2 = m->f_S2;
+    a.kbp = m->f_kbp;
+    a.max_chunks = m->f_max_chunks;
+    a.tl = m->tl ? m->tl + (int64_t)(j * 3) * 8 : nullptr;
+    a.tstamp = m->tstamp;
+    return a;
+}
+
 exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStream_t s) {
     const auto& c = m->cfg;
     if (!m->connected) return invalid("model is not connected to its peers (exf_model_connect)");
     switch (phase) {
+        case 5: {  // fused layer kernel (gate..GEMM2 in one launch)
+            if (j < 0 || j >= c.num_layers) return invalid("layer out of range");
+            const CUtensorMap maps[4] = {m->tmap1[j], m->tmap2[j], m->gmap_recv, m->gmap_h};
+            return launch_layer_fused(maps, fused_args(m, j), m->nmax, s);
+        }
         case 0:
             if (!x_in) return invalid("null input");
             return launch_step_begin(static_cast<const __nv_bfloat16*>(x_in), m->res_x[0], m->res_meta[0],
@@ -365,8 +434,12 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
 exf_status run_step(exf_model* m, const void* x_in, cudaStream_t s) {
     EXF_TRY(run_phase(m, 0, 0, x_in, s));
     for (int j = 0; j < m->cfg.num_layers; ++j) {
-        EXF_TRY(run_phase(m, 1, j, nullptr, s));
-        EXF_TRY(run_phase(m, 2, j, nullptr, s));
+        if (m->fused) {
+            EXF_TRY(run_phase(m, 5, j, nullptr, s));
+        } else {
+            EXF_TRY(run_phase(m, 1, j, nullptr, s));
+            EXF_TRY(run_phase(m, 2, j, nullptr, s));
+        }
     }
     EXF_TRY(run_phase(m, 3, 0, nullptr, s));
     return run_phase(m, 4, 0, nullptr, s);
@@ -423,6 +496,25 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     EXF_M(dalloc(&m->done_ctr, 2));
     EXF_M(dalloc(&m->cta_cnt, (size_t)128 * E));
     EXF_M(dalloc(&m->gbar, 2));
+    // token tile: expected tokens per expert under balanced routing is C/E;
+    // keep the tile at >= 2x that so skewed experts rarely need a second pass
+    m->nmax = (2 * C / E <= 32) ? 32 : ((2 * C / E <= 64) ? 64 : 128);
+    if (const char* env = std::getenv("EXF_TOKEN_TILE")) m->nmax = std::atoi(env);
+    {  // fused layer kernel plan and scratch
+        if (const char* env = std::getenv("EXF_FUSED")) m->fused = std::atoi(env) != 0;
+        m->f_ctas = fused_ctas();
+        m->f_tpc = std::max(8, ((C + m->f_ctas - 1) / m->f_ctas + 7) / 8 * 8);
+        const int nmax_f = m->nmax <= 32 ? 32 : (m->nmax <= 64 ? 64 : 128);
+        plan_fused(m->E_loc, d, f, m->f_ctas, &m->f_kbp, &m->f_S1, &m->f_S2);
+        m->f_max_chunks = (C + nmax_f - 1) / nmax_f;
+        const int64_t slots = (int64_t)m->E_loc * (f / 128 + d / 128) * m->f_max_chunks;
+        const int smax = std::max(m->f_S1, m->f_S2);
+        EXF_M(dalloc(&m->ws, smax > 1 ? (size_t)(slots * smax * nmax_f * 128) : 1));
+        EXF_M(dalloc(&m->item_ctr, (size_t)slots));
+        EXF_M(dalloc(&m->hdone, (size_t)2 * m->E_loc));
+        EXF_M(dalloc(&m->fbar, 2 * 260));  // 256 per-CTA barrier slots + epoch (u64)
+        EXF_M(dalloc(&m->f_cta_cnt, (size_t)m->f_ctas * E));
+    }
     if (std::getenv("EXF_FFN_TIMELINE")) {
         EXF_M(dalloc(&m->tstamp, (size_t)2 * kTimelineCtas * 16));
         EXF_M(dalloc(&m->tl, (size_t)L * 3 * 8));
@@ -433,11 +525,7 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     EXF_M(make_gather_tmap(&m->gmap_h, m->H, C, f));
     if (cudaMemset(m->trace, 0xff, sizeof(int32_t) * C * L) != cudaSuccess) return fail(EXF_CUDA);
     EXF_M(init_weights(m));
-    // tile policy: token tile from the expected tokens per expert, split-K to fill 148 SMs
-    // expected tokens per expert under balanced routing is C/E; keep the tile
-    // at >= 2x that so skewed experts rarely need a second pass
-    m->nmax = (2 * C / E <= 32) ? 32 : ((2 * C / E <= 64) ? 64 : 128);
-    if (const char* env = std::getenv("EXF_TOKEN_TILE")) m->nmax = std::atoi(env);
+    // split-K / persistent-cluster plan of the two-kernel (phased) path
     EXF_M(plan_ffn_gemm(m->nmax, 0, m->E_loc * (f / 128), d, &m->ks1, &m->cl1));
     EXF_M(plan_ffn_gemm(m->nmax, 1, m->E_loc * (d / 128), f, &m->ks2, &m->cl2));
     if (c.world_size == 1) {  // a single rank is its own peer
@@ -457,7 +545,8 @@ exf_status exf_model_destroy(exf_model* m) {
     void* bufs[] = {m->d_gpu_of, m->d_slot_of, m->wg, m->w1, m->b1, m->w2, m->b2, m->res_x[0],
                     m->res_x[1], m->res_meta[0], m->res_meta[1], m->n_res, m->expert, m->prob, m->H,
                     m->hist, m->crossed, m->trace, m->forced, m->step, m->err, m->done_ctr,
-                    m->cta_cnt, m->gbar, m->tl,
+                    m->cta_cnt, m->gbar, m->tl, m->ws, m->item_ctr, m->hdone, m->fbar,
+                    m->f_cta_cnt,
                     m->d_peers, m->sym_base, m->tstamp};
     for (void* p : bufs)
         if (p) cudaFree(p);

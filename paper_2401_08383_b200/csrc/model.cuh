@@ -96,6 +96,46 @@ struct FfnArgs {
     unsigned long long* tl;      // optional step timeline [4] (diagnostics)
 };
 
+// Arguments of the fused per-layer kernel (layer_fused.cu).
+struct FusedArgs {
+    // token side
+    int32_t G, rank, E, E_loc, d, dff, C, L, layer, forced, tpc;
+    const __nv_bfloat16* wg;
+    const int32_t* gpu_of;
+    const int32_t* slot_of;
+    const __nv_bfloat16* res_x_in;
+    const ResMeta* res_meta_in;
+    const int32_t* n_res_in;
+    unsigned long long* hist;
+    unsigned long long* crossed;
+    int32_t* trace;
+    const int32_t* forced_routes;
+    const uint64_t* step;
+    int32_t* err;
+    int32_t* done_ctr;
+    int32_t* cta_cnt;
+    uint32_t* gbar;
+    uint8_t* const* peers;
+    uint8_t* own_sym;
+    Symm sym;
+    // expert side
+    __nv_bfloat16* H;
+    const __nv_bfloat16* b1;  // [E_loc][dff] of this layer
+    const __nv_bfloat16* b2;  // [E_loc][d] of this layer
+    __nv_bfloat16* res_x_out;
+    ResMeta* res_meta_out;
+    int32_t* n_res_out;
+    float* ws;           // split-K partials
+    int32_t* item_ctr;   // arrivals per (gemm, expert, tile, chunk)
+    int32_t* hdone;      // [2 parity][E_loc] completed GEMM1 (tile, chunk) units
+    int32_t S1, S2, kbp, max_chunks;
+    const __nv_bfloat16* w1;  // [E_loc][dff][d] of this layer
+    const __nv_bfloat16* w2;  // [E_loc][d][dff] of this layer
+    int32_t a_probe;          // diagnostics: contiguous 16 KB A loads (wrong numerics)
+    unsigned long long* tl;
+    uint64_t* tstamp;    // optional per-CTA stamps [grid][16] (diagnostics)
+};
+
 __host__ __device__ inline int64_t bytes_bf16(int64_t n) { return n * 2; }
 
 // error codes written to the device error word before a trap

@@ -159,6 +159,30 @@ __device__ __forceinline__ void tma_gather4(void* smem_dst, const CUtensorMap* m
         "r"(smem_u32(bar))
         : "memory");
 }
+// 1-D bulk copy global -> shared (size multiple of 16), completion on mbarrier.
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// cp.async (LDGSTS) 16-byte copies with commit groups: token rows go through
+// the LSU path, not the TMA queue that streams the weight tiles.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// arrive on `bar` once every cp.async this thread issued so far has landed
+// (noinc: the barrier's expected count includes these arrivals)
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // L2 eviction-priority policies (createpolicy.fractional)
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;

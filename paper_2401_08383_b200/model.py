@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _capi
 
-PHASE_BEGIN, PHASE_DISPATCH, PHASE_FFN, PHASE_GATHER_SEND, PHASE_GATHER_WAIT = range(5)
+PHASE_BEGIN, PHASE_DISPATCH, PHASE_FFN, PHASE_GATHER_SEND, PHASE_GATHER_WAIT, PHASE_FUSED = range(6)
 
 
 @dataclass

@@ -1,0 +1,69 @@
+"""Per-CTA timeline of the fused layer kernel (diagnostics): GEMM-phase start,
+per-job MMA start/end (first/last k-block issued) and exit, for the last
+layer of a decode step at the bench config. Usage: python tools/fused_timeline.py"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("EXF_FFN_TIMELINE", "1")
+
+
+def main():
+    import numpy as np
+    import torch
+    from paper_2401_08383_b200 import _capi, placement as pl
+    from paper_2401_08383_b200.affinity import Topology
+    from paper_2401_08383_b200.model import MoeModel, MoeModelConfig
+    E = int(os.environ.get("E", "8"))
+    B = int(os.environ.get("B", "64"))
+    cfg = MoeModelConfig(num_experts=E, num_layers=4, d_model=1024, d_ffn=4096, tokens_per_gpu=B,
+                         seed=1234, gate_affinity=0.8)
+    m = MoeModel(cfg, pl.contiguous_placement(E, 4, Topology(1, 1)))
+    x = torch.randn(B, 1024).to(torch.bfloat16).cuda()
+    s = torch.cuda.Stream()
+    for _ in range(3):
+        m.step(x, s)
+    s.synchronize()
+    m.check()
+    ctas = 148
+    buf = np.zeros((2, ctas, 16), np.uint64)
+    _capi.call("exf_model_read_ffn_timeline", m.handle, buf.ctypes.data, ctas)
+    t = buf[0].astype(np.int64)
+    t0 = t[:, 0].min()
+    rel = (t - t0) / 1000.0
+    print(f"span {rel[:, 15].max():.2f} us; GEMM phase start mean {rel[:, 1].mean():.2f} "
+          f"(min {rel[:, 1].min():.2f} max {rel[:, 1].max():.2f})")
+    prev_end = rel[:, 1]
+    for j in range(6):
+        st, en = rel[:, 2 + 2 * j], rel[:, 3 + 2 * j]
+        ok = t[:, 2 + 2 * j] > 0
+        if not ok.any():
+            break
+        print(f"job {j}: ctas {ok.sum():3d}  start {st[ok].mean():6.2f} (wait after prev "
+              f"{(st - prev_end)[ok].mean():5.2f})  mma span {(en - st)[ok].mean():5.2f} "
+              f"[{(en - st)[ok].min():5.2f},{(en - st)[ok].max():5.2f}]  end {en[ok].mean():6.2f} "
+              f"max {en[ok].max():6.2f}")
+        prev_end = np.where(ok, en, prev_end)
+    print(f"exit mean {rel[:, 15].mean():.2f} max {rel[:, 15].max():.2f}")
+    t2 = buf[1].astype(np.int64)
+    r2 = (t2 - t0) / 1000.0
+    j0 = rel[:, 2]
+    print("B producer pass at it=0,2,..,14 rel. job-0 first MMA:",
+          " ".join(f"{(r2[:, k] - j0).mean():.2f}" for k in range(8)))
+    print(f"job 1 MMA: fullB ready {(r2[:, 8] - rel[:, 3]).mean():.2f}, A ready {(r2[:, 9] - rel[:, 3]).mean():.2f} "
+          f"after job 0 last MMA")
+    print(f"job 0 epilogue: tmem_full at {(r2[:, 10] - rel[:, 3]).mean():.2f} after last MMA, "
+          f"done {(r2[:, 11] - r2[:, 10]).mean():.2f} later")
+    for k, nm in ((12, "epilogue"), (13, "B producer"), (14, "A producer"), (15, "MMA")):
+        print(f"{nm} done mean {r2[:, k].mean():.2f} max {r2[:, k].max():.2f} (argmax cta {r2[:, k].argmax()})")
+    w = rel[:, 15].argmax()
+    print(f"slowest cta {w}: jobs", [(round(rel[w, 2 + 2 * j], 2), round(rel[w, 3 + 2 * j], 2)) for j in range(5)
+                                    if t[w, 2 + 2 * j] > 0])
+    ok = t[:, 12] > 0
+    print(f"job 1 first A TMA issued {(rel[:, 12] - rel[:, 3])[ok].mean():.2f} us after job 0's last MMA; "
+          f"first B gather {(rel[:, 13] - rel[:, 3])[ok].mean():.2f}; job 1 first MMA "
+          f"{(rel[:, 4] - rel[:, 3])[ok].mean():.2f}")
+
+
+if __name__ == "__main__":
+    main()
