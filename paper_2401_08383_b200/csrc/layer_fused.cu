@@ -53,6 +53,14 @@ __device__ __forceinline__ void unpack8(const int4& v, float (&f)[8]) {
         f[2 * i + 1] = p.y;
     }
 }
+__device__ __forceinline__ int4 lds128(uint32_t addr) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %lanemask_lt;" : "=r"(m));
@@ -141,7 +149,7 @@ struct Smem {
 
 }  // namespace
 
-template <int NMAX, int STAGES, int BST, int EMAX, int NBUF = (NMAX <= 64 ? 4 : 2)>
+template <int NMAX, int STAGES, int BST, int NBUF = (NMAX <= 64 ? 4 : 2)>
 __global__ void __launch_bounds__(kThreads, 1)
 layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
                    const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
@@ -161,6 +169,9 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     __shared__ int32_t s_exp[256];
     __shared__ float s_prob[256];
     __shared__ int32_t s_pos[256];
+    __shared__ int32_t s_tok[256];
+    __shared__ int32_t s_key[kMaxKeys];  // expert -> (dest GPU, local slot) key
+    __shared__ ResMeta s_meta_spec[kWarps];
     __shared__ int32_t s_cnt[kMaxKeys];
     __shared__ int32_t s_tot[kMaxKeys];
     __shared__ int32_t s_before[kMaxKeys];
@@ -182,6 +193,14 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // [9]/[10] job-0 epilogue start/done, [11] job-1 epilogue start,
     // [12] last epilogue done, [13] B done, [14] A done, [15] MMA done
     uint64_t* ts2 = ts ? ts + 4096 * 16 : nullptr;
+    // token-phase row by layer parity: [0] entry, [1] PDL wait returned,
+    // [2] gate done, [3] ranks done, [4] barrier passed, [5] dispatch stored,
+    // [6] completion done, [7] flags seen / tables built, [15] exit
+    uint64_t* ts3 = ts ? ts + (int64_t)(2 + (a.layer & 1)) * 4096 * 16 : nullptr;
+    auto mark3 = [&](int k) {
+        if (ts3 && threadIdx.x == 0) ts3[k] = ptx::globaltimer();
+    };
+    mark3(0);
 
     // piece p -> (gemm, expert, tile, k-part)
     auto decode = [&](int p, int& g, int& e, int& mt, int& kp) {
@@ -230,7 +249,23 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // region (unused until the expert phase) when it fits, before the wait
     uint64_t* wg_bar = &tmem_empty[NBUF];
     const uint32_t wg_bytes = (uint32_t)a.E * a.d * 2;
-    const bool wg_smem = wg_bytes <= (uint32_t)(BST * S::kB) && blockIdx.x * a.tpc < a.C;
+    const bool gate_cta = (int)blockIdx.x * a.tpc < a.C;  // may own tokens this layer
+    // placement tables are stream-ordered host writes, never written by the
+    // previous kernel: safe to read before the PDL wait
+    if (tid < a.E) s_key[tid] = a.gpu_of[tid] * a.E_loc + a.slot_of[tid];
+    const bool wg_smem = wg_bytes <= (uint32_t)(BST * S::kB) && gate_cta;
+    auto prefetch_a = [&]() {  // first weight stages of the CTA's first piece
+        if (first_p < 0) return;
+        int g, e, mt, kp;
+        decode(first_p, g, e, mt, kp);
+        const CUtensorMap* tm = g == 0 ? &tmA1 : &tmA2;
+        const int rows = g == 0 ? a.dff : a.d;
+        for (int kb = 0; kb < npre; ++kb) {
+            ptx::mbar_arrive_expect_tx(&full[kb], S::kA);
+            ptx::tma_load_2d(smem + S::kOffA + kb * S::kA, tm, &full[kb], (kp * kbp + kb) * kBK,
+                             e * rows + mt * kBM, pol_a);
+        }
+    };
     if (warp == 0 && lane == 0) {
         if (wg_smem) {
             ptx::mbar_arrive_expect_tx(wg_bar, wg_bytes);
@@ -240,23 +275,29 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         }
         ptx::tma_prefetch_desc(&tmA1);
         ptx::tma_prefetch_desc(&tmA2);
-        if (first_p >= 0) {
-            int g, e, mt, kp;
-            decode(first_p, g, e, mt, kp);
-            const CUtensorMap* tm = g == 0 ? &tmA1 : &tmA2;
-            const int rows = g == 0 ? a.dff : a.d;
-            for (int kb = 0; kb < npre; ++kb) {
-                ptx::mbar_arrive_expect_tx(&full[kb], S::kA);
-                ptx::tma_load_2d(smem + S::kOffA + kb * S::kA, tm, &full[kb], (kp * kbp + kb) * kBK,
-                                 e * rows + mt * kBM, pol_a);
-            }
-        }
+        // before the PDL wait: issued mid-token-phase, the 160 KB bursts of the
+        // token-owning CTAs delayed every flag poll behind them by ~4 us
+        prefetch_a();
     }
 
     // ---------------- dependent part
     ptx::pdl_wait();
     ptx::pdl_trigger();
+    mark3(1);
     if (tid == 0) tl_mark(a.tl, 1);
+    // speculative loads of each warp's first token (row + meta), in flight
+    // together with n: rows below C always exist, unused ones are dropped
+    const int t_first = (int)blockIdx.x * a.tpc + warp;
+    const bool spec = gate_cta && warp < a.tpc && t_first < a.C;
+    int4 xk[8];
+    ResMeta mk{0, -1};
+    if (spec) {
+        const __nv_bfloat16* x = a.res_x_in + (int64_t)t_first * a.d;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            if (c < (a.d >> 8)) xk[c] = *reinterpret_cast<const int4*>(x + c * 256 + lane * 8);
+        if (lane == 0) mk = a.res_meta_in[t_first];
+    }
     const uint64_t q = *a.step * (uint64_t)a.L + (uint64_t)a.layer;
     const int parity = (int)(q & 1);
     const uint64_t epoch = q + 1;
@@ -265,109 +306,119 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         if (tid == 0) atomicExch(a.err, ERR_CAPACITY);
         __trap();
     }
+    mark3(11);
     // the next layer's GEMM1 counters start from zero
     if (blockIdx.x == 0 && tid < a.E_loc) a.hdone[((parity ^ 1) * a.E_loc) + tid] = 0;
 
-    // ---------------- (1) gate, one warp per token
+    // ---------------- (1) gate: (token, expert) dot products spread over warps
     const int E = a.E;
     const int t0 = blockIdx.x * a.tpc;
     const int nt = max(0, min(a.tpc, n - t0));
-    if (tid < kMaxKeys) s_cnt[tid] = 0;
-    const int chunks = a.d >> 8;
-    const __nv_bfloat16* wgp = a.wg;
-    if (wg_smem) {
-        if (nt > 0) ptx::mbar_wait(wg_bar, 0, a.err, ERR_TIMEOUT_PIPE);
-        wgp = reinterpret_cast<const __nv_bfloat16*>(smem + S::kOffB);
+    if (tid < kMaxKeys) {
+        s_cnt[tid] = 0;
+        s_tot[tid] = 0;
+        s_before[tid] = 0;
     }
-    for (int i = warp; i < nt; i += kWarps) {
-        const int t = t0 + i;
-        const __nv_bfloat16* x = a.res_x_in + (int64_t)t * a.d;
-        int4 xv[8];
+    const int chunks = a.d >> 8;
+    if (wg_smem) {
+        // always: the copy must land before the B ring reuses this region
+        ptx::mbar_wait(wg_bar, 0, a.err, ERR_TIMEOUT_PIPE);
+    }
+    mark3(12);
+    if (spec && lane == 0) s_meta_spec[warp] = mk;
+    // Gate scratch in the (still idle) B-ring region: [Wg | token rows | logits].
+    // A warp walking one token through every expert is a serial chain of
+    // ~600 instructions (~1.5 us); instead each warp takes (token, expert)
+    // items, every dot product still in the oracle's order (lane-sliced,
+    // c-major/k-minor, xor butterfly), and one thread per token does softmax.
+    const uint32_t wg_al = wg_smem ? (wg_bytes + 1023u) & ~1023u : 0u;
+    const uint32_t lg_off = (uint32_t)(BST * S::kB) - (uint32_t)((a.tpc * E * 4 + 1023) & ~1023);
+    float* s_logit = reinterpret_cast<float*>(smem + S::kOffB + lg_off);
+    const bool x_smem = wg_al + (uint32_t)nt * a.d * 2 <= lg_off;
+    const uint32_t xs_base = ptx::smem_u32(smem + S::kOffB + wg_al);
+    if (x_smem) {  // stage the CTA's token rows (first rows still in registers)
+        for (int i = warp; i < nt; i += kWarps) {
+            const __nv_bfloat16* x = a.res_x_in + (int64_t)(t0 + i) * a.d;
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-            if (c < chunks) xv[c] = *reinterpret_cast<const int4*>(x + c * 256 + lane * 8);
-        float acc[EMAX];
-#pragma unroll
-        for (int e = 0; e < EMAX; ++e) acc[e] = 0.f;
-        // experts in groups of 8: issue all of a group's Wg loads for a chunk
-        // before the FMAs (independent L1/L2 round trips in flight); the
-        // per-expert accumulation order (c-major, k-minor) is unchanged
-#pragma unroll
-        for (int e0 = 0; e0 < EMAX; e0 += 8) {
-            if (e0 < E) {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    if (c < chunks) {
-                        int4 wv[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u)
-                            if (e0 + u < E)
-                                wv[u] = *reinterpret_cast<const int4*>(
-                                    wgp + (int64_t)(e0 + u) * a.d + c * 256 + lane * 8);
-                        float xf[8];
-                        unpack8(xv[c], xf);
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            if (e0 + u < E) {
-                                float wf[8];
-                                unpack8(wv[u], wf);
-#pragma unroll
-                                for (int k = 0; k < 8; ++k) acc[e0 + u] = fmaf(xf[k], wf[k], acc[e0 + u]);
-                            }
-                        }
-                    }
+            for (int c = 0; c < 8; ++c) {
+                if (c < chunks) {
+                    const int4 v = i == warp ? xk[c] : *reinterpret_cast<const int4*>(x + c * 256 + lane * 8);
+                    *reinterpret_cast<int4*>(smem + S::kOffB + wg_al + ((uint32_t)i * a.d + c * 256 + lane * 8) * 2) = v;
                 }
             }
         }
+        __syncthreads();
+    }
+    mark3(14);
+    for (int w = warp; w < nt * E; w += kWarps) {
+        const int i = w / E, e = w - i * E;
+        float acc = 0.f;
+        if (x_smem && wg_smem) {
+            const uint32_t xa = xs_base + ((uint32_t)i * a.d) * 2 + lane * 16;
+            const uint32_t wa = ptx::smem_u32(smem + S::kOffB) + ((uint32_t)e * a.d) * 2 + lane * 16;
+            for (int c = 0; c < chunks; ++c) {
+                float xf[8], wf[8];
+                unpack8(lds128(xa + c * 512), xf);
+                unpack8(lds128(wa + c * 512), wf);
 #pragma unroll
-        for (int e = 0; e < EMAX; ++e) {
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], off);
-        }
-        if (lane == 0) {
-            int best = 0;
-            float mx = acc[0];
-#pragma unroll
-            for (int e = 1; e < EMAX; ++e)
-                if (e < E && acc[e] > mx) {
-                    mx = acc[e];
-                    best = e;
-                }
-            float s = 0.f;
-#pragma unroll
-            for (int e = 0; e < EMAX; ++e)
-                if (e < E) s += expf(acc[e] - mx);
-            const ResMeta m = a.res_meta_in[t];
-            int sel = best;
-            float p = 1.f / s;
-            if (a.forced) {
-                sel = a.forced_routes[(int64_t)m.token * a.L + a.layer];
-                if ((unsigned)sel >= (unsigned)E) {
-                    atomicExch(a.err, ERR_BAD_EXPERT);
-                    sel = best;
-                }
-                float ls = acc[0];
-#pragma unroll
-                for (int e = 0; e < EMAX; ++e)
-                    if (e == sel) ls = acc[e];
-                p = expf(ls - mx) / s;
+                for (int k = 0; k < 8; ++k) acc = fmaf(xf[k], wf[k], acc);
             }
-            s_exp[i] = sel;
-            s_prob[i] = p;
-            if (a.hist && a.layer > 0 && m.prev_expert >= 0)
-                atomicAdd(&a.hist[((int64_t)(a.layer - 1) * E + m.prev_expert) * E + sel], 1ull);
-            if (a.trace) a.trace[(int64_t)m.token * a.L + a.layer] = sel;
+        } else {
+            const __nv_bfloat16* x = a.res_x_in + (int64_t)(t0 + i) * a.d + lane * 8;
+            const __nv_bfloat16* wr = a.wg + (int64_t)e * a.d + lane * 8;
+            for (int c = 0; c < chunks; ++c) {
+                float xf[8], wf[8];
+                unpack8(*reinterpret_cast<const int4*>(x + c * 256), xf);
+                unpack8(*reinterpret_cast<const int4*>(wr + c * 256), wf);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc = fmaf(xf[k], wf[k], acc);
+            }
         }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) s_logit[w] = acc;
     }
     __syncthreads();
+    mark3(13);
+    if (tid < nt) {  // softmax / top-1 per token, experts in index order
+        const int i = tid, t = t0 + i;
+        const float* lg = s_logit + i * E;
+        int best = 0;
+        float mx = lg[0];
+        for (int e = 1; e < E; ++e)
+            if (lg[e] > mx) {
+                mx = lg[e];
+                best = e;
+            }
+        float s = 0.f;
+        for (int e = 0; e < E; ++e) s += expf(lg[e] - mx);
+        const ResMeta m = (i < kWarps && i < a.tpc) ? s_meta_spec[i] : a.res_meta_in[t];
+        int sel = best;
+        float p = 1.f / s;
+        if (a.forced) {
+            sel = a.forced_routes[(int64_t)m.token * a.L + a.layer];
+            if ((unsigned)sel >= (unsigned)E) {
+                atomicExch(a.err, ERR_BAD_EXPERT);
+                sel = best;
+            }
+            p = expf(lg[sel] - mx) / s;
+        }
+        s_exp[i] = sel;
+        s_prob[i] = p;
+        s_tok[i] = m.token;
+        if (a.hist && a.layer > 0 && m.prev_expert >= 0)
+            atomicAdd(&a.hist[((int64_t)(a.layer - 1) * E + m.prev_expert) * E + sel], 1ull);
+        if (a.trace) a.trace[(int64_t)m.token * a.L + a.layer] = sel;
+    }
+    __syncthreads();
+    mark3(2);
     // ---------------- (2) stable ranks within the CTA slice, per-key counts
     if (warp == 0) {
         for (int b = 0; b < nt; b += 32) {
             const int i = b + lane;
             int key = -1;
             if (i < nt) {
-                const int e = s_exp[i];
-                key = a.gpu_of[e] * a.E_loc + a.slot_of[e];
+                key = s_key[s_exp[i]];
             }
             const uint32_t peers = __match_any_sync(0xffffffffu, key);
             const int rank = __popc(peers & lanemask_lt());
@@ -379,20 +430,29 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         for (int k = lane; k < E; k += 32) a.cta_cnt[blockIdx.x * E + k] = s_cnt[k];
     }
     if (tid == 0) tl_mark(a.tl, 4);
+    mark3(3);
     // launch epoch: slots [0, P) are per-CTA barrier flags, slot 256 the counter
     uint64_t* bslots = reinterpret_cast<uint64_t*>(a.gbar);
     const uint64_t bepoch = bslots[256] + 1;
     flag_barrier(bslots, bepoch, a.err);
+    mark3(4);
     if (tid == 0) tl_mark(a.tl, 5);
-    if (tid < E) {
-        int tot = 0, before = 0;
-        for (int c = 0; c < P; ++c) {
-            const int v = a.cta_cnt[c * E + tid];
-            tot += v;
-            before += (c < (int)blockIdx.x) ? v : 0;
+    // per-key totals and this CTA's offset: only the nact token-owning CTAs
+    // have counts; (key, part) threads sum strided CTA subsets in parallel
+    const int nact = max(1, (n + a.tpc - 1) / a.tpc);
+    if (nt > 0 || blockIdx.x == 0) {
+        const int parts = kThreads / E;
+        const int k = tid % E, part = tid / E;
+        if (part < parts) {
+            int tot = 0, before = 0;
+            for (int c = part; c < nact; c += parts) {
+                const int v = __ldcg(a.cta_cnt + c * E + k);
+                tot += v;
+                before += (c < (int)blockIdx.x) ? v : 0;
+            }
+            if (tot) atomicAdd(&s_tot[k], tot);
+            if (before) atomicAdd(&s_before[k], before);
         }
-        s_tot[tid] = tot;
-        s_before[tid] = before;
     }
     __syncthreads();
     if (tid == 0) {
@@ -418,17 +478,21 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             const int64_t slot_row = ((int64_t)(parity * a.G + a.rank) * a.C + local);
             int4* dst = reinterpret_cast<int4*>(pbase + a.sym.recv_x + slot_row * row_bytes);
             const int4* src = reinterpret_cast<const int4*>(a.res_x_in + (int64_t)t * a.d);
-            int4 buf[8];
+            int4 buf[8];  // d <= 2048: one row is 8 int4 per lane
+            if (i == warp) {  // the row this warp gated is still in registers
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (u * 32 + lane < vec) buf[u] = src[u * 32 + lane];
+                for (int u = 0; u < 8; ++u) buf[u] = xk[u];
+            } else {
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (u * 32 + lane < vec) buf[u] = src[u * 32 + lane];
+            }
 #pragma unroll
             for (int u = 0; u < 8; ++u)
                 if (u * 32 + lane < vec) dst[u * 32 + lane] = buf[u];
-            for (int v = 256 + lane; v < vec; v += 32) dst[v] = src[v];
             if (lane == 0) {
                 RecvMeta m;
-                m.token = a.res_meta_in[t].token;
+                m.token = s_tok[i];
                 m.expert = s_exp[i];
                 m.prob = s_prob[i];
                 m.pad = 0;
@@ -437,21 +501,11 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         }
     }
     __syncthreads();
-    // completion among the CTAs that own tokens (CTA 0 always takes part)
-    const int nact = max(1, (n + a.tpc - 1) / a.tpc);
-    if (tid == 0) {
-        if (nact == 1) {
-            s_flag = blockIdx.x == 0;
-        } else if ((int)blockIdx.x < nact) {
-            if (a.G > 1) __threadfence_system(); else __threadfence();
-            s_flag = atomicAdd(a.done_ctr, 1) == nact - 1;
-            if (s_flag) __threadfence();
-        } else {
-            s_flag = 0;
-        }
-    }
-    __syncthreads();
-    if (s_flag) {  // last CTA: per-(src = me, slot) counts, stats, release flags
+    mark3(5);
+    // completion: every CTA release-flags its own slot at every destination
+    // (no last-arriver counter: a same-address atomic chain plus a publishing
+    // CTA cost ~4 us); CTA 0 also publishes this source's per-slot counts
+    if (blockIdx.x == 0) {
         if (tid < E) {
             const int dest = tid / a.E_loc, slot = tid - dest * a.E_loc;
             int32_t* cnt = reinterpret_cast<int32_t*>(a.peers[dest] + a.sym.recv_cnt);
@@ -461,20 +515,25 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             int stay = 0;
             for (int s2 = 0; s2 < a.E_loc; ++s2) stay += s_tot[a.rank * a.E_loc + s2];
             atomicAdd(&a.crossed[a.layer], (unsigned long long)(n - stay));
-            *a.done_ctr = 0;
         }
         __syncthreads();
-        if (tid < a.G) {
-            uint64_t* f = reinterpret_cast<uint64_t*>(a.peers[tid] + a.sym.flags);
-            ptx::st_release_sys(f + parity * a.G + a.rank, epoch);
-        }
+    }
+    if (tid < a.G) {
+        if (a.G > 1) __threadfence_system();
+        uint64_t* f = reinterpret_cast<uint64_t*>(a.peers[tid] + a.sym.cflags);
+        ptx::flag_publish(f + ((int64_t)parity * a.G + a.rank) * kMaxCtas + blockIdx.x, epoch, a.G > 1);
     }
     if (tid == 0) tl_mark(a.tl, 6);
-    // ---------------- wait for every source's dispatch, build the tables
-    if (tid < a.G) {
-        const uint64_t* f = reinterpret_cast<const uint64_t*>(a.own_sym + a.sym.flags) + parity * a.G + tid;
-        ptx::SpinGuard g;
-        while (ptx::ld_acquire_sys(f) < epoch) g.step(a.err, ERR_TIMEOUT_DISPATCH);
+    mark3(6);
+    // ---------------- wait for every source CTA's dispatch, build the tables
+    {
+        const uint64_t* f = reinterpret_cast<const uint64_t*>(a.own_sym + a.sym.cflags) +
+                            (int64_t)parity * a.G * kMaxCtas;
+        for (int w = tid; w < a.G * P; w += kThreads) {
+            const uint64_t* fw = f + (int64_t)(w / P) * kMaxCtas + (w % P);
+            ptx::SpinGuard g;
+            while (ptx::flag_read(fw, a.G > 1) < epoch) g.step(a.err, ERR_TIMEOUT_DISPATCH);
+        }
     }
     __syncthreads();
     const int32_t* cnt = reinterpret_cast<const int32_t*>(a.own_sym + a.sym.recv_cnt) +
@@ -503,6 +562,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     __syncthreads();
     if (tid == 0) tl_mark(a.tl, 7);
     if (ts && tid == 0) ts[1] = ptx::globaltimer();
+    mark3(7);
 
     const RecvMeta* rmeta = reinterpret_cast<const RecvMeta*>(a.own_sym + a.sym.recv_meta);
     const __nv_bfloat16* rx = reinterpret_cast<const __nv_bfloat16*>(a.own_sym + a.sym.recv_x);
@@ -576,8 +636,10 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     const int sb = it % BST;
                     ptx::mbar_wait(&fullB[sb], (it / BST) & 1, a.err, ERR_TIMEOUT_PIPE);
                     if (ts2 && lane == 0 && it == kbp) ts2[8] = ptx::globaltimer();
+                    if (ts3 && lane == 0 && it == 0) ts3[9] = ptx::globaltimer();
                     ptx::mbar_wait(&full[st], ph, a.err, ERR_TIMEOUT_PIPE);
                     if (ts2 && lane == 0 && it == kbp) ts2[9] = ptx::globaltimer();
+                    if (ts3 && lane == 0 && it == 0) ts3[10] = ptx::globaltimer();
                     ptx::tc_fence_after();
                     ptx::fence_proxy_async_smem();  // cp.async (generic) rows -> tensor-core reads
                     if (lane == 0) {
@@ -605,6 +667,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         // (lane >> 3) + 4j into the SW128 layout the UMMA descriptor expects,
         // and arrives on fullB (count 32) when its copies land.
         const int cc = lane & 7;
+        if (ts3 && lane == 0) ts3[8] = ptx::globaltimer();
         int it = 0;
         int waited_e = -1;
         for (int p = blockIdx.x; p < NP; p += P) {
@@ -773,6 +836,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     __syncthreads();
     if (tid == 0) tl_mark(a.tl, 3);
     if (ts && tid == 0) ts[15] = ptx::globaltimer();
+    mark3(15);
     // every CTA read the launch epoch before arriving at the barrier, which
     // CTA 0 passed before getting here: safe to advance it
     if (blockIdx.x == 0 && tid == 0) bslots[256] = bepoch;
@@ -785,10 +849,10 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
 // ------------------------------------------------------------------ host side
 namespace {
 
-template <int NMAX, int STAGES, int BST, int EMAX>
+template <int NMAX, int STAGES, int BST>
 struct FusedLauncher {
     using Sm = Smem<NMAX, STAGES, BST>;
-    static constexpr auto kern = layer_fused_kernel<NMAX, STAGES, BST, EMAX>;
+    static constexpr auto kern = layer_fused_kernel<NMAX, STAGES, BST>;
     int ctas = 0;
     exf_status prepare() {
         if (ctas) return EXF_OK;
@@ -813,14 +877,8 @@ struct FusedLauncher {
 
 template <int NMAX, int STAGES, int BST>
 exf_status launch_nmax(const CUtensorMap* maps, const FusedArgs& a, cudaStream_t s) {
-    static FusedLauncher<NMAX, STAGES, BST, 8> l8;
-    static FusedLauncher<NMAX, STAGES, BST, 16> l16;
-    static FusedLauncher<NMAX, STAGES, BST, 32> l32;
-    static FusedLauncher<NMAX, STAGES, BST, 64> l64;
-    if (a.E <= 8) return l8.launch(maps, a, s);
-    if (a.E <= 16) return l16.launch(maps, a, s);
-    if (a.E <= 32) return l32.launch(maps, a, s);
-    return l64.launch(maps, a, s);
+    static FusedLauncher<NMAX, STAGES, BST> l;
+    return l.launch(maps, a, s);
 }
 
 }  // namespace
@@ -856,7 +914,7 @@ void plan_fused(int E_loc, int d, int dff, int ctas, int* kbp_out, int* S1, int*
 exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int nmax, cudaStream_t s) {
     if (a.E > kMaxKeys || a.E_loc > kMaxLocal) return invalid("at most 64 experts");
     if (a.d > 2048) return invalid("fused layer kernel supports d_model <= 2048");
-    if (a.tpc > 256) return invalid("token slice too large for the fused layer kernel");
+    if (a.tpc > 32) return invalid("token slice too large for the fused layer kernel");
     // (token tile, weight stages, token stages): ~208 KB of rings each
     if (nmax <= 32) return launch_nmax<32, 10, 12>(maps, a, s);
     if (nmax <= 64) return launch_nmax<64, 8, 10>(maps, a, s);

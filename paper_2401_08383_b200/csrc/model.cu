@@ -196,6 +196,7 @@ exf_status build_layout(exf_model* m) {
     m->sym.flags = take(2LL * G * 8);
     m->sym.gather_x = take((int64_t)C * d * 2);
     m->sym.gflags = take((int64_t)G * 8);
+    m->sym.cflags = take(2LL * G * kMaxCtas * 8);
     m->sym.total = o;
     EXF_CUDA_TRY(cudaMalloc(&m->sym_base, (size_t)o));
     EXF_CUDA_TRY(cudaMemset(m->sym_base, 0, (size_t)o));
@@ -380,6 +381,7 @@ FusedArgs fused_args(exf_model* m, int j) {
     a.w1 = m->w1 + (int64_t)j * m->E_loc * c.d_ffn * c.d_model;
     a.w2 = m->w2 + (int64_t)j * m->E_loc * c.d_ffn * c.d_model;
     a.a_probe = getenv("EXF_A_PROBE") ? 1 : 0;
+    a.l2_pre = getenv("EXF_L2_PREFETCH") ? atoi(getenv("EXF_L2_PREFETCH")) : 0;
     a.res_x_out = m->res_x[(j + 1) & 1];
     a.res_meta_out = m->res_meta[(j + 1) & 1];
     a.n_res_out = m->n_res + ((j + 1) & 1);
@@ -390,7 +392,9 @@ FusedArgs fused_args(exf_model* m, int j) {
     a.S2 = m->f_S2;
     a.kbp = m->f_kbp;
     a.max_chunks = m->f_max_chunks;
-    a.tl = m->tl ? m->tl + (int64_t)(j * 3) * 8 : nullptr;
+    // the per-CTA stamp rows replace the atomic step timeline here: 148-way
+    // atomics on one word distort the phases they measure
+    a.tl = nullptr;
     a.tstamp = m->tstamp;
     return a;
 }
@@ -503,7 +507,10 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     {  // fused layer kernel plan and scratch
         if (const char* env = std::getenv("EXF_FUSED")) m->fused = std::atoi(env) != 0;
         m->f_ctas = fused_ctas();
-        m->f_tpc = std::max(8, ((C + m->f_ctas - 1) / m->f_ctas + 7) / 8 * 8);
+        // one token per CTA while C <= #SMs: the gate's (token, expert) dot
+        // products then spread over 8 warps of many CTAs
+        m->f_tpc = std::max(1, (C + m->f_ctas - 1) / m->f_ctas);
+        if (m->f_tpc > 32 || d > 2048 || E > 64) m->fused = false;  // two-kernel path instead
         const int nmax_f = m->nmax <= 32 ? 32 : (m->nmax <= 64 ? 64 : 128);
         plan_fused(m->E_loc, d, f, m->f_ctas, &m->f_kbp, &m->f_S1, &m->f_S2);
         m->f_max_chunks = (C + nmax_f - 1) / nmax_f;
@@ -516,7 +523,7 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         EXF_M(dalloc(&m->f_cta_cnt, (size_t)m->f_ctas * E));
     }
     if (std::getenv("EXF_FFN_TIMELINE")) {
-        EXF_M(dalloc(&m->tstamp, (size_t)2 * kTimelineCtas * 16));
+        EXF_M(dalloc(&m->tstamp, (size_t)4 * kTimelineCtas * 16));
         EXF_M(dalloc(&m->tl, (size_t)L * 3 * 8));
     }
     EXF_M(dalloc(&m->d_peers, (size_t)c.world_size));
@@ -762,7 +769,8 @@ exf_status exf_model_replay(exf_model* m, exf_stream_t stream) {
 
 int32_t exf_model_launches_per_step(exf_model* m) {
     if (!m) return 0;
-    return 1 + 3 * m->cfg.num_layers + 2;  // begin, L x (gate_dispatch, GEMM1, GEMM2), gather x2
+    // begin, L x (fused layer | gate_dispatch + GEMM1 + GEMM2), gather send + wait
+    return 1 + (m->fused ? 1 : 3) * m->cfg.num_layers + 2;
 }
 
 exf_status exf_model_read_step_timeline(exf_model* m, uint64_t* h, int32_t reset) {
@@ -783,7 +791,7 @@ exf_status exf_model_read_ffn_timeline(exf_model* m, uint64_t* h, int32_t ctas) 
     if (!m || !h || ctas < 1 || ctas > kTimelineCtas) return invalid("bad argument");
     if (!m->tstamp) return invalid("timeline not enabled (set EXF_FFN_TIMELINE=1 before create)");
     EXF_CUDA_TRY(cudaDeviceSynchronize());
-    for (int g = 0; g < 2; ++g)
+    for (int g = 0; g < 4; ++g)
         EXF_CUDA_TRY(cudaMemcpy(h + (int64_t)g * ctas * 16, m->tstamp + (int64_t)g * kTimelineCtas * 16,
                                 sizeof(uint64_t) * ctas * 16, cudaMemcpyDeviceToHost));
     return EXF_OK;
@@ -791,13 +799,19 @@ exf_status exf_model_read_ffn_timeline(exf_model* m, uint64_t* h, int32_t ctas) 
 
 exf_status exf_model_describe(exf_model* m, char* buf, int32_t len) {
     if (!m || !buf || len < 1) return invalid("bad argument");
-    const std::string s = "{\"token_tile\": " + std::to_string(m->nmax) +
-                          ", \"gemm1\": {\"ksplit\": " + std::to_string(m->ks1) +
-                          ", \"clusters\": " + std::to_string(m->cl1) +
-                          "}, \"gemm2\": {\"ksplit\": " + std::to_string(m->ks2) +
-                          ", \"clusters\": " + std::to_string(m->cl2) +
-                          "}, \"experts_per_rank\": " + std::to_string(m->E_loc) +
-                          ", \"capacity_tokens\": " + std::to_string(m->C) + "}";
+    std::string s = "{\"token_tile\": " + std::to_string(m->nmax) +
+                    ", \"experts_per_rank\": " + std::to_string(m->E_loc) +
+                    ", \"capacity_tokens\": " + std::to_string(m->C);
+    if (m->fused)
+        s += ", \"path\": \"fused\", \"layer_kernel\": {\"ctas\": " + std::to_string(m->f_ctas) +
+             ", \"tokens_per_cta\": " + std::to_string(m->f_tpc) +
+             ", \"kblocks_per_piece\": " + std::to_string(m->f_kbp) +
+             ", \"gemm1_ksplit\": " + std::to_string(m->f_S1) +
+             ", \"gemm2_ksplit\": " + std::to_string(m->f_S2) + "}}";
+    else
+        s += ", \"path\": \"two-kernel\", \"gemm1\": {\"ksplit\": " + std::to_string(m->ks1) +
+             ", \"clusters\": " + std::to_string(m->cl1) + "}, \"gemm2\": {\"ksplit\": " +
+             std::to_string(m->ks2) + ", \"clusters\": " + std::to_string(m->cl2) + "}}";
     std::strncpy(buf, s.c_str(), (size_t)len - 1);
     buf[len - 1] = 0;
     return EXF_OK;

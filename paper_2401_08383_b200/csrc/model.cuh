@@ -37,8 +37,10 @@ struct ResMeta {
 };
 
 struct Symm {  // byte offsets inside the symmetric region
-    int64_t recv_x, recv_meta, recv_cnt, flags, gather_x, gflags, total;
+    int64_t recv_x, recv_meta, recv_cnt, flags, gather_x, gflags, cflags, total;
 };
+// fused layer kernel: per-(parity, src rank, src CTA) dispatch-complete flags
+constexpr int kMaxCtas = 256;
 
 // Everything a kernel needs, passed by value.
 struct LayerArgs {
@@ -132,6 +134,7 @@ struct FusedArgs {
     const __nv_bfloat16* w1;  // [E_loc][dff][d] of this layer
     const __nv_bfloat16* w2;  // [E_loc][d][dff] of this layer
     int32_t a_probe;          // diagnostics: contiguous 16 KB A loads (wrong numerics)
+    int32_t l2_pre;           // weight tiles per CTA prefetched into L2 before the PDL wait
     unsigned long long* tl;
     uint64_t* tstamp;    // optional per-CTA stamps [grid][16] (diagnostics)
 };

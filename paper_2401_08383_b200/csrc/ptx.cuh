@@ -160,6 +160,17 @@ __device__ __forceinline__ void tma_gather4(void* smem_dst, const CUtensorMap* m
         : "memory");
 }
 // 1-D bulk copy global -> shared (size multiple of 16), completion on mbarrier.
+// L2 prefetch of one tensor-map box / a contiguous byte range (no smem, no barrier)
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -274,6 +285,22 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
 }
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_gpu_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// flag publish/observe at the narrowest scope covering every peer: .gpu when
+// the whole job is one device, .sys once peers are other GPUs (NVLink)
+__device__ __forceinline__ void flag_publish(uint64_t* p, uint64_t v, bool multi_gpu) {
+    if (multi_gpu) st_release_sys(p, v); else st_release_gpu_u64(p, v);
+}
+__device__ __forceinline__ uint64_t flag_read(const uint64_t* p, bool multi_gpu) {
+    return multi_gpu ? ld_acquire_sys(p) : ld_acquire_gpu_u64(p);
 }
 __device__ __forceinline__ int ld_acquire_gpu_s32(const int* p) {
     int v;

@@ -26,7 +26,7 @@ def main():
     s.synchronize()
     m.check()
     ctas = 148
-    buf = np.zeros((2, ctas, 16), np.uint64)
+    buf = np.zeros((4, ctas, 16), np.uint64)
     _capi.call("exf_model_read_ffn_timeline", m.handle, buf.ctypes.data, ctas)
     t = buf[0].astype(np.int64)
     t0 = t[:, 0].min()
@@ -59,6 +59,26 @@ def main():
     w = rel[:, 15].argmax()
     print(f"slowest cta {w}: jobs", [(round(rel[w, 2 + 2 * j], 2), round(rel[w, 3 + 2 * j], 2)) for j in range(5)
                                     if t[w, 2 + 2 * j] > 0])
+    # token phase of the last layer (L=4 -> odd row 3) against the previous
+    # layer's exits (even row 2)
+    cur = buf[3].astype(np.int64)
+    prv = buf[2].astype(np.int64)
+    z = prv[:, 15].max()
+    names = ["entry", "pdl wait", "gate", "ranks", "barrier", "dispatch", "completion", "tables"]
+    print(f"token phase rel. previous layer's last exit (prev exit min {(prv[:, 15].min() - z) / 1e3:.2f}):")
+    for k, nm in enumerate(names):
+        v = (cur[:, k] - z) / 1e3
+        print(f"  {nm:10s} min {v.min():7.2f} mean {v.mean():7.2f} max {v.max():7.2f}")
+    print(f"  first MMA  min {(t[:, 2] - z).min() / 1e3:7.2f} mean {(t[:, 2] - z).mean() / 1e3:7.2f}")
+    print("  gate detail (n loaded / Wg ready / dot products done / rows staged):")
+    for c in range(4):
+        print(f"   cta {c}: " + " ".join(f"{(cur[c, k] - z) / 1e3:6.2f}" for k in (11, 12, 13, 14)))
+    print("  per CTA (0..9, 147):", " / ".join(names))
+    for c in list(range(10)) + [ctas - 1]:
+        print(f"   cta {c:3d}: " + " ".join(f"{(cur[c, k] - z) / 1e3:6.2f}" for k in range(8)) +
+              f" | B start {(cur[c, 8] - z) / 1e3:6.2f} fullB {(cur[c, 9] - z) / 1e3:6.2f} "
+              f"fullA {(cur[c, 10] - z) / 1e3:6.2f} mma {(t[c, 2] - z) / 1e3:6.2f}")
+    print(f"  exit       min {(cur[:, 15] - z).min() / 1e3:7.2f} max {(cur[:, 15] - z).max() / 1e3:7.2f}")
     ok = t[:, 12] > 0
     print(f"job 1 first A TMA issued {(rel[:, 12] - rel[:, 3])[ok].mean():.2f} us after job 0's last MMA; "
           f"first B gather {(rel[:, 13] - rel[:, 3])[ok].mean():.2f}; job 1 first MMA "

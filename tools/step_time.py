@@ -1,0 +1,47 @@
+"""Quick step-time probe (diagnostics): the bench model (BASELINE configs[1],
+N=1, contiguous placement) captured in a CUDA graph and replayed; prints the
+mean device time per decode step. Knobs come from the EXF_* environment.
+Usage: python tools/step_time.py [--reps N] [--batch B]"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--reps", type=int, default=50)
+    p.add_argument("--batch", type=int, default=64)
+    p.add_argument("--experts", type=int, default=8)
+    p.add_argument("--layers", type=int, default=24)
+    a = p.parse_args()
+    import torch
+    from paper_2401_08383_b200 import placement as pl
+    from paper_2401_08383_b200.affinity import Topology
+    from paper_2401_08383_b200.model import MoeModel, MoeModelConfig
+    cfg = MoeModelConfig(num_experts=a.experts, num_layers=a.layers, d_model=1024, d_ffn=4096,
+                         tokens_per_gpu=a.batch, seed=1234, gate_affinity=0.8)
+    m = MoeModel(cfg, pl.contiguous_placement(a.experts, a.layers, Topology(1, 1)))
+    x = torch.randn(a.batch, 1024).to(torch.bfloat16).cuda()
+    s = torch.cuda.Stream()
+    for _ in range(3):
+        m.step(x, s)
+    m.capture(x, s)
+    for _ in range(5):
+        m.replay(s)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.synchronize()
+    e0.record(s)
+    for _ in range(a.reps):
+        m.replay(s)
+    e1.record(s)
+    e1.synchronize()
+    m.check()
+    us = e0.elapsed_time(e1) * 1000.0 / a.reps
+    knobs = {k: v for k, v in os.environ.items() if k.startswith("EXF_")}
+    print(f"step {us:.1f} us  ({us / a.layers:.2f} us/layer, {a.batch / us * 1e6:.0f} tok/s)  {knobs}")
+
+
+if __name__ == "__main__":
+    main()
