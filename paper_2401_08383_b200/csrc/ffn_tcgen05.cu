@@ -57,9 +57,6 @@ struct FfnSmem {
     static constexpr int kBytes = kOffMisc + 64 + 1024;  // + alignment slack
 };
 
-__device__ __forceinline__ float gelu_erf(float v) {
-    return 0.5f * v * (1.0f + erff(v * 0.70710678118654752440f));
-}
 
 template <int NMAX, int STAGES, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)

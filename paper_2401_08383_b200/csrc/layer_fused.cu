@@ -87,9 +87,6 @@ __device__ __forceinline__ void red_add_release(int32_t* p, int32_t v) {
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-__device__ __forceinline__ float gelu_erf(float v) {
-    return 0.5f * v * (1.0f + erff(v * 0.70710678118654752440f));
-}
 
 // All-to-all flag barrier: every CTA release-stores its own epoch slot, then
 // P threads acquire-poll all slots in parallel. No same-address atomics (a
@@ -179,6 +176,12 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     __shared__ int32_t s_flag;
     __shared__ int64_t s_rrow[NMAX];
     __shared__ float s_rprob[NMAX];
+    __shared__ int32_t s_rtok[NMAX];
+    __shared__ int32_t s_rexp[NMAX];
+    __shared__ float s_logit_d[kMaxKeys];  // dense-mode gate logits of the CTA's token
+    // dense mode reuses s_exp / s_prob / s_pos / s_tok (resident-token indexed,
+    // n <= #CTAs <= 256) as slot / prob / canonical row, and s_tok as the
+    // canonical-row -> resident-row map
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int P = gridDim.x;
@@ -234,7 +237,8 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             ptx::mbar_init(&tmem_full[b], 1);
             ptx::mbar_init(&tmem_empty[b], 128);
         }
-        ptx::mbar_init(&tmem_empty[NBUF], 1);  // Wg staging barrier
+        ptx::mbar_init(&tmem_empty[NBUF], 1);      // Wg staging barrier
+        ptx::mbar_init(&tmem_empty[NBUF + 1], 1);  // dense-mode route tables
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc(&misc[0], NBUF * NMAX);
@@ -248,6 +252,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // the layer's gate matrix is a weight too: bulk-copy it into the B-stage
     // region (unused until the expert phase) when it fits, before the wait
     uint64_t* wg_bar = &tmem_empty[NBUF];
+    uint64_t* route_bar = &tmem_empty[NBUF + 1];  // dense mode: route tables built
     const uint32_t wg_bytes = (uint32_t)a.E * a.d * 2;
     const bool gate_cta = (int)blockIdx.x * a.tpc < a.C;  // may own tokens this layer
     // placement tables are stream-ordered host writes, never written by the
@@ -288,7 +293,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // speculative loads of each warp's first token (row + meta), in flight
     // together with n: rows below C always exist, unused ones are dropped
     const int t_first = (int)blockIdx.x * a.tpc + warp;
-    const bool spec = gate_cta && warp < a.tpc && t_first < a.C;
+    const bool spec = !a.dense && gate_cta && warp < a.tpc && t_first < a.C;
     int4 xk[8];
     ResMeta mk{0, -1};
     if (spec) {
@@ -309,7 +314,17 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     mark3(11);
     // the next layer's GEMM1 counters start from zero
     if (blockIdx.x == 0 && tid < a.E_loc) a.hdone[((parity ^ 1) * a.E_loc) + tid] = 0;
+    // launch epoch: slots [0, P) are per-CTA barrier flags, slot 256 the counter
+    uint64_t* bslots = reinterpret_cast<uint64_t*>(a.gbar);
+    const uint64_t bepoch = bslots[256] + 1;
 
+    if (a.dense) {
+        // GEMM1 runs over all n resident tokens at once; the GEMM2 tables are
+        // filled by the token warp (route_bar) while GEMM1 streams
+        if (blockIdx.x == 0 && tid == 0) *a.n_res_out = n;
+        __syncthreads();
+        if (ts && tid == 0) ts[1] = ptx::globaltimer();
+    } else {
     // ---------------- (1) gate: (token, expert) dot products spread over warps
     const int E = a.E;
     const int t0 = blockIdx.x * a.tpc;
@@ -431,9 +446,6 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     }
     if (tid == 0) tl_mark(a.tl, 4);
     mark3(3);
-    // launch epoch: slots [0, P) are per-CTA barrier flags, slot 256 the counter
-    uint64_t* bslots = reinterpret_cast<uint64_t*>(a.gbar);
-    const uint64_t bepoch = bslots[256] + 1;
     flag_barrier(bslots, bepoch, a.err);
     mark3(4);
     if (tid == 0) tl_mark(a.tl, 5);
@@ -563,6 +575,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     if (tid == 0) tl_mark(a.tl, 7);
     if (ts && tid == 0) ts[1] = ptx::globaltimer();
     mark3(7);
+    }  // !dense token phase
 
     const RecvMeta* rmeta = reinterpret_cast<const RecvMeta*>(a.own_sym + a.sym.recv_meta);
     const __nv_bfloat16* rx = reinterpret_cast<const __nv_bfloat16*>(a.own_sym + a.sym.recv_x);
@@ -572,9 +585,18 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         while (s2 + 1 < a.G && t[2 + s2 + 1] <= i) ++s2;
         return ((int64_t)parity * a.G + s2) * a.C + t[11 + s2] + (i - t[2 + s2]);
     };
+    // tokens of (gemm, expert): dense GEMM1 runs over every resident token;
+    // otherwise (and for dense GEMM2, once the routes are in) the tables
+    auto cnt = [&](int g, int e) -> int {
+        if (a.dense) {
+            if (g == 0) return n;
+            ptx::mbar_wait(route_bar, 0, a.err, ERR_TIMEOUT_DISPATCH);
+        }
+        return tab[e * S::kTabInts];
+    };
     // chunks of piece p (the CTA's first piece always runs >= 1: prefetched)
-    auto nchunks = [&](int p, int e) {
-        const int c = (tab[e * S::kTabInts] + NMAX - 1) / NMAX;
+    auto nchunks = [&](int p, int g, int e) {
+        const int c = (cnt(g, e) + NMAX - 1) / NMAX;
         return (p == first_p && c == 0) ? 1 : c;
     };
     auto slot_of_tile = [&](int g, int e, int mt, int c) -> int64_t {
@@ -590,7 +612,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             for (int p = blockIdx.x; p < NP; p += P) {
                 int g, e, mt, kp;
                 decode(p, g, e, mt, kp);
-                const int nch = nchunks(p, e);
+                const int nch = nchunks(p, g, e);
                 const CUtensorMap* tm = g == 0 ? &tmA1 : &tmA2;
                 const int rows = g == 0 ? a.dff : a.d;
                 for (int c = 0; c < nch; ++c)
@@ -601,15 +623,8 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         ptx::mbar_wait(&empty[st], ph ^ 1, a.err, ERR_TIMEOUT_PIPE);
                         if (ts && it == kbp) ts[12] = ptx::globaltimer();  // job 1's first A tile
                         ptx::mbar_arrive_expect_tx(&full[st], S::kA);
-                        if (a.a_probe) {
-                            const int kt = (g == 0 ? a.d : a.dff) / kBK;
-                            const __nv_bfloat16* wt = (g == 0 ? a.w1 : a.w2) +
-                                (((int64_t)e * (rows / kBM) + mt) * kt + kp * kbp + kb) * (kBM * kBK);
-                            ptx::bulk_load(smem + S::kOffA + st * S::kA, wt, S::kA, &full[st]);
-                        } else {
-                            ptx::tma_load_2d(smem + S::kOffA + st * S::kA, tm, &full[st],
-                                             (kp * kbp + kb) * kBK, e * rows + mt * kBM, pol_a);
-                        }
+                        ptx::tma_load_2d(smem + S::kOffA + st * S::kA, tm, &full[st],
+                                         (kp * kbp + kb) * kBK, e * rows + mt * kBM, pol_a);
                     }
             }
             if (ts2) ts2[14] = ptx::globaltimer();
@@ -620,8 +635,8 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         for (int p = blockIdx.x; p < NP; p += P) {
             int g, e, mt, kp;
             decode(p, g, e, mt, kp);
-            const int n_e = tab[e * S::kTabInts];
-            const int nch = nchunks(p, e);
+            const int n_e = cnt(g, e);
+            const int nch = nchunks(p, g, e);
             for (int c = 0; c < nch; ++c, ++job) {
                 const int nc = max(0, min(NMAX, n_e - c * NMAX));
                 const int ncol = max(16, (nc + 15) & ~15);
@@ -673,19 +688,21 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         for (int p = blockIdx.x; p < NP; p += P) {
             int g, e, mt, kp;
             decode(p, g, e, mt, kp);
-            const int n_e = tab[e * S::kTabInts];
+            const int n_e = cnt(g, e);
             const int off_e = tab[e * S::kTabInts + 1];
-            const int nch = nchunks(p, e);
+            const int nch = nchunks(p, g, e);
             if (g == 1 && nch > 0 && waited_e != e) {
                 // all GEMM1 (tile, chunk) units of expert e must be complete
-                const int target = mt1 * ((n_e + NMAX - 1) / NMAX);
+                const int target = mt1 * ((cnt(0, e) + NMAX - 1) / NMAX);
                 ptx::SpinGuard sg;
                 while (ld_acq_s32(a.hdone + parity * a.E_loc + e) < target) sg.step(a.err, ERR_TIMEOUT_PIPE);
                 waited_e = e;
             }
-            const __nv_bfloat16* src = g == 0 ? rx : a.H;
+            // GEMM1 rows: dispatched tokens (recv region) or, dense, the resident
+            // tokens themselves; GEMM2 rows: H in canonical order
+            const __nv_bfloat16* src = g == 0 ? (a.dense ? a.res_x_in : rx) : a.H;
             const int ld = g == 0 ? a.d : a.dff;
-            const int row_lim = g == 0 ? 2 * a.G * a.C : a.C;
+            const int row_lim = g == 0 ? (a.dense ? a.C : 2 * a.G * a.C) : a.C;
             for (int c = 0; c < nch; ++c) {
                 const int cb = c * NMAX;
                 const int nc = max(0, min(NMAX, n_e - cb));
@@ -695,14 +712,13 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 for (int j = 0; j < NMAX / 4; ++j) {
                     const int r = (lane >> 3) + 4 * j;
                     const int i = cb + (r < nc ? r : 0);
-                    const int64_t row = g == 0 ? recv_row(e, i) : (int64_t)(off_e + i);
+                    const int64_t row = g == 0 ? (a.dense ? (int64_t)i : recv_row(e, i)) : (int64_t)(off_e + i);
                     rows[j] = (int32_t)(row < 0 ? 0 : (row >= row_lim ? row_lim - 1 : row));
                 }
                 for (int kb = 0; kb < kbp; ++kb, ++it) {
                     const int sb = it % BST;
                     ptx::mbar_wait(&emptyB[sb], ((it / BST) & 1) ^ 1, a.err, ERR_TIMEOUT_PIPE);
                     if (ts && lane == 0 && it == kbp) ts[13] = ptx::globaltimer();  // job 1's first B rows
-                    if (ts2 && lane == 0 && it < 16 && !(it & 1)) ts2[it >> 1] = ptx::globaltimer();
                     uint8_t* sbase = smem + S::kOffB + sb * S::kB;
                     const __nv_bfloat16* kcol = src + (int64_t)(kp * kbp + kb) * kBK + cc * 8;
 #pragma unroll
@@ -716,7 +732,132 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             }
         }
         if (ts2 && lane == 0) ts2[13] = ptx::globaltimer();
-    } else if (warp >= 4) {
+    } else {
+        if (a.dense) {
+            // ====== dense mode (G == 1, token t is CTA t's): the token phase
+            // runs concurrently with GEMM1's MMAs; its result is first needed
+            // by GEMM1's epilogue (which rows of H to keep, and where).
+            const int E = a.E;
+            const int t = blockIdx.x;
+            const bool own = t < n;
+            ResMeta mo{0, -1};
+            if (own && warp == 3 && lane == 0) mo = a.res_meta_in[t];  // in flight with the gate
+            // (1) gate on warps 3..7 (idle until the first accumulator is
+            // ready): (token, expert) dot products in the oracle's order
+            const int chunks = a.d >> 8;
+            for (int e = warp - 3; own && e < E; e += kWarps - 3) {
+                const __nv_bfloat16* x = a.res_x_in + (int64_t)t * a.d + lane * 8;
+                const __nv_bfloat16* wr = a.wg + (int64_t)e * a.d + lane * 8;
+                int4 xv[8], wv[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (c < chunks) {
+                        xv[c] = *reinterpret_cast<const int4*>(x + c * 256);
+                        wv[c] = *reinterpret_cast<const int4*>(wr + c * 256);
+                    }
+                float acc = 0.f;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (c < chunks) {
+                        float xf[8], wf[8];
+                        unpack8(xv[c], xf);
+                        unpack8(wv[c], wf);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) acc = fmaf(xf[k], wf[k], acc);
+                    }
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                if (lane == 0) s_logit_d[e] = acc;
+            }
+            asm volatile("bar.sync 3, 160;" ::: "memory");  // warps 3..7
+            if (warp == 3) {
+                if (ts3 && lane == 0) ts3[12] = ptx::globaltimer();
+                // (2) top-1 + softmax; the route travels as ONE 64-bit flag
+                // {epoch:24 | slot:8 | prob:32}: no barrier, no count prefix
+                uint64_t* rf = reinterpret_cast<uint64_t*>(a.own_sym + a.sym.cflags) + (int64_t)parity * kMaxCtas;
+                const uint64_t e24 = epoch & 0xFFFFFFull;
+                int sel = 0;
+                if (own && lane == 0) {
+                    const float* lg = s_logit_d;
+                    int best = 0;
+                    float mx = lg[0];
+                    for (int e = 1; e < E; ++e)
+                        if (lg[e] > mx) {
+                            mx = lg[e];
+                            best = e;
+                        }
+                    float s = 0.f;
+                    for (int e = 0; e < E; ++e) s += expf(lg[e] - mx);
+                    sel = best;
+                    float p = 1.f / s;
+                    if (a.forced) {
+                        sel = a.forced_routes[(int64_t)mo.token * a.L + a.layer];
+                        if ((unsigned)sel >= (unsigned)E) {
+                            atomicExch(a.err, ERR_BAD_EXPERT);
+                            sel = best;
+                        }
+                        p = expf(lg[sel] - mx) / s;
+                    }
+                    const uint64_t flag = (e24 << 40) | ((uint64_t)(uint32_t)s_key[sel] << 32) | __float_as_uint(p);
+                    ptx::st_release_gpu_u64(rf + t, flag);
+                    if (a.hist && a.layer > 0 && mo.prev_expert >= 0)
+                        atomicAdd(&a.hist[((int64_t)(a.layer - 1) * E + mo.prev_expert) * E + sel], 1ull);
+                    if (a.trace) a.trace[(int64_t)mo.token * a.L + a.layer] = sel;
+                }
+                // (3) every token's route: one round trip once all are out
+                for (int k = lane; k < kMaxKeys; k += 32) {
+                    s_cnt[k] = 0;
+                    s_before[k] = 0;
+                }
+                for (int u = lane; u < n; u += 32) {
+                    ptx::SpinGuard sg;
+                    uint64_t v;
+                    while (((v = ptx::ld_acquire_gpu_u64(rf + u)) >> 40) != e24) sg.step(a.err, ERR_TIMEOUT_DISPATCH);
+                    s_exp[u] = (int)((v >> 32) & 0xFF);  // slot
+                    s_prob[u] = __uint_as_float((uint32_t)v);
+                }
+                __syncwarp();
+                if (ts3 && lane == 0) ts3[13] = ptx::globaltimer();
+                // (4) canonical positions (slot, resident order) and GEMM2 tables
+                for (int u = lane; u < n; u += 32) atomicAdd(&s_cnt[s_exp[u]], 1);
+                __syncwarp();
+                if (lane == 0) {
+                    int acc = 0;
+                    for (int e = 0; e < a.E_loc; ++e) {
+                        int32_t* tb = tab + e * S::kTabInts;
+                        tb[0] = s_cnt[e];
+                        tb[1] = acc;
+                        tb[2] = 0;
+                        tb[3] = s_cnt[e];
+                        tb[11] = 0;
+                        s_start[e] = acc;
+                        acc += s_cnt[e];
+                    }
+                }
+                __syncwarp();
+                for (int r = 0; r < n; r += 32) {
+                    const int u = r + lane;
+                    const int key = u < n ? s_exp[u] : -1;
+                    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+                    const int rk = __popc(peers & lanemask_lt());
+                    if (key >= 0) {
+                        const int pos = s_start[key] + s_before[key] + rk;
+                        s_pos[u] = pos;
+                        s_tok[pos] = u;  // canonical row -> resident row
+                    }
+                    __syncwarp();
+                    if (key >= 0 && rk == 0) s_before[key] += __popc(peers);
+                    __syncwarp();
+                }
+                if (own && lane == 0) a.res_meta_out[s_pos[t]] = ResMeta{mo.token, sel};
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive(route_bar);  // tables ready for the GEMM roles
+                    if (ts3) ts3[2] = ptx::globaltimer();
+                }
+            }
+        }
+      if (warp >= 4) {
         // ================= epilogue =================
         const int et = tid - 128;  // TMEM lane == weight row within the tile
         const int lane_base = (warp & 3) * 32;
@@ -724,9 +865,9 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         for (int p = blockIdx.x; p < NP; p += P) {
             int g, e, mt, kp;
             decode(p, g, e, mt, kp);
-            const int n_e = tab[e * S::kTabInts];
+            const int n_e = cnt(g, e);
             const int off_e = tab[e * S::kTabInts + 1];
-            const int nch = nchunks(p, e);
+            const int nch = nchunks(p, g, e);
             const int Sg = g == 0 ? a.S1 : a.S2;
             const int mrows = g == 0 ? a.dff : a.d;
             const int m_glob = mt * kBM + et;
@@ -740,30 +881,37 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 if (ts2 && et == 0 && job == 0) ts2[10] = ptx::globaltimer();
                 ptx::tc_fence_after();
                 const uint32_t t_base = tmem + buf * NMAX + ((uint32_t)lane_base << 16);
-                float accv[NMAX];
+                auto tmem16 = [&](int col, float (&v)[16]) {
+                    uint32_t r[16];
+                    ptx::tmem_ld_32x32b_x16(t_base + col, r);
+                    ptx::tmem_wait_ld();
 #pragma unroll
-                for (int col = 0; col < NMAX; col += 16) {
-                    if (col < nc) {
-                        uint32_t r[16];
-                        ptx::tmem_ld_32x32b_x16(t_base + col, r);
-                        ptx::tmem_wait_ld();
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) accv[col + i] = __uint_as_float(r[i]);
-                    }
+                    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+                };
+                auto release_tmem = [&]() {
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&tmem_empty[buf]);
+                };
+                if (nc == 0) {  // prefetched first piece of an empty expert
+                    release_tmem();
+                    continue;
                 }
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(&tmem_empty[buf]);
-                if (nc == 0) continue;  // prefetched first piece of an empty expert
-                bool finish = true;
                 const int64_t slot = slot_of_tile(g, e, mt, c);
+                const int Smax = max(a.S1, a.S2);
+                bool from_ws = false;  // finished values come from the k-ordered partial sum
                 if (Sg > 1) {
                     // park the partial; the last-arriving piece of this tile
                     // reduces all partials in k order (deterministic)
-                    const int Smax = max(a.S1, a.S2);
-                    float* wsp = a.ws + ((slot * Smax + kp) * NMAX) * kBM;
+                    float* wsp = a.ws + ((slot * Smax + kp) * NMAX) * kBM + et;
+#pragma unroll 1
+                    for (int col = 0; col < nc; col += 16) {
+                        float v[16];
+                        tmem16(col, v);
 #pragma unroll
-                    for (int i = 0; i < NMAX; ++i)
-                        if (i < nc) __stcg(wsp + i * kBM + et, accv[i]);
+                        for (int i = 0; i < 16; ++i)
+                            if (col + i < nc) __stcg(wsp + (col + i) * kBM, v[i]);
+                    }
+                    release_tmem();
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     if (et == 0) {
                         const int prev = atom_add_acq_rel(a.item_ctr + slot, 1);  // release partials
@@ -771,67 +919,146 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         if (s_flag) a.item_ctr[slot] = 0;  // next use is a later launch
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
-                    finish = s_flag;
-                    if (finish) {
-                        // k-ordered sum; one batch of independent loads per
-                        // (k, 16 tokens) instead of a dependent chain per token
-                        const float* w0 = a.ws + (slot * Smax * NMAX) * kBM;
+                    if (!s_flag) continue;
+                    from_ws = true;
+                }
+                // Final values 4 tokens at a time in a ROLLED loop. ncu showed the
+                // epilogue stalled on instruction fetch (stall_no_inst): a
+                // 16-token unrolled body (~15 KB of SASS) does not fit a
+                // sub-partition's L0 i-cache next to the co-resident producer
+                // warp's loop; fully unrolled over all tokens it was ~90 KB.
+                constexpr int kG = 4;
+                const float* w0 = a.ws + (slot * Smax * NMAX) * kBM + et;
+                auto final4 = [&](int col, float (&v)[kG]) {
+                    if (from_ws) {
 #pragma unroll
-                        for (int i = 0; i < NMAX; ++i) accv[i] = 0.f;
+                        for (int i = 0; i < kG; ++i) v[i] = 0.f;
                         for (int k = 0; k < Sg; ++k) {
-                            const float* wk = w0 + (int64_t)k * NMAX * kBM + et;
+                            const float* wk = w0 + (int64_t)k * NMAX * kBM;
+                            float pv[kG];
 #pragma unroll
-                            for (int i0 = 0; i0 < NMAX; i0 += 16) {
-                                if (i0 < nc) {
-                                    float v[16];
+                            for (int i = 0; i < kG; ++i) pv[i] = col + i < nc ? __ldcg(wk + (col + i) * kBM) : 0.f;
 #pragma unroll
-                                    for (int i = 0; i < 16; ++i) v[i] = i0 + i < nc ? __ldcg(wk + (i0 + i) * kBM) : 0.f;
+                            for (int i = 0; i < kG; ++i) v[i] += pv[i];
+                        }
+                    } else {
+                        uint32_t r[kG];
+                        ptx::tmem_ld_32x32b_x4(t_base + col, r);
+                        ptx::tmem_wait_ld();
 #pragma unroll
-                                    for (int i = 0; i < 16; ++i) accv[i0 + i] += v[i];
+                        for (int i = 0; i < kG; ++i) v[i] = __uint_as_float(r[i]);
+                    }
+                };
+                if (g == 0) {
+                    if (a.dense) {
+                        // dense GEMM1 covered every resident token: keep the
+                        // rows routed to this expert, at their canonical rows
+                        ptx::mbar_wait(route_bar, 0, a.err, ERR_TIMEOUT_DISPATCH);
+                        if (ts3 && et == 0 && job == 0) ts3[14] = ptx::globaltimer();
+                    }
+                    const long long c_in = clock64();
+                    if (a.dense) {
+                        // only this expert's routed tokens (~1/E of the dense
+                        // columns): canonical rows off1.., resident rows via s_tok,
+                        // TMEM column = resident row - cb; 8 loads in flight
+                        const int ne1 = tab[e * S::kTabInts], off1 = tab[e * S::kTabInts + 1];
+#pragma unroll 1
+                        for (int j0 = 0; j0 < ne1; j0 += 8) {
+                            uint32_t r8[8];
+                            int pos8[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                const int j = j0 + i;
+                                const int col = (j < ne1 ? s_tok[off1 + j] : cb) - cb;
+                                const bool in = j < ne1 && col >= 0 && col < nc;
+                                pos8[i] = in ? off1 + j : -1;
+                                if (from_ws) {
+                                    float s = 0.f;
+                                    for (int k = 0; k < Sg; ++k)
+                                        s += in ? __ldcg(w0 + (int64_t)k * NMAX * kBM + col * kBM) : 0.f;
+                                    r8[i] = __float_as_uint(s);
+                                } else {
+                                    r8[i] = ptx::tmem_ld_32x32b_x1(t_base + (in ? col : 0));
                                 }
                             }
+                            if (!from_ws) ptx::tmem_wait_ld_dep8(r8);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                if (pos8[i] >= 0)
+                                    a.H[(int64_t)pos8[i] * a.dff + m_glob] =
+                                        __float2bfloat16(gelu_erf(__uint_as_float(r8[i]) + bias));
                         }
                     }
-                }
-                if (!finish) continue;
-                if (g == 0) {
+#pragma unroll 1
+                    for (int col = 0; col < (a.dense ? 0 : nc); col += kG) {
+                        float v[kG];
+                        final4(col, v);
+                        // branch-free: independent GELUs and row lookups, then
+                        // predicated stores
+                        __nv_bfloat16 hv[kG];
+                        int row[kG];
 #pragma unroll
-                    for (int i = 0; i < NMAX; ++i)
-                        if (i < nc)
-                            a.H[(int64_t)(off_e + cb + i) * a.dff + m_glob] = __float2bfloat16(gelu_erf(accv[i] + bias));
+                        for (int i = 0; i < kG; ++i) {
+                            hv[i] = __float2bfloat16(gelu_erf(v[i] + bias));
+                            const int j = cb + col + i;
+                            const int slot_j = a.dense ? s_exp[j] : e;
+                            const int pos_j = a.dense ? s_pos[j] : off_e + j;
+                            row[i] = (col + i < nc && slot_j == e) ? pos_j : -1;
+                        }
+#pragma unroll
+                        for (int i = 0; i < kG; ++i)
+                            if (row[i] >= 0) a.H[(int64_t)row[i] * a.dff + m_glob] = hv[i];
+                    }
+                    if (ts2 && et == 0 && job < 4) ts2[job] = (uint64_t)(clock64() - c_in);  // diagnostics
+                    if (ts2 && (et & 31) == 0 && job == 0) ts2[4 + (et >> 5)] = (uint64_t)(clock64() - c_in);
+                    if (!from_ws) release_tmem();
+                    if (ts3 && et == 0 && job == 0) ts3[4] = ptx::globaltimer();
                     asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (ts3 && et == 0 && job == 0) ts3[5] = ptx::globaltimer();
                     if (et == 0) red_add_release(a.hdone + parity * a.E_loc + e, 1);
+                    if (ts3 && et == 0 && job == 0) ts3[6] = ptx::globaltimer();
                 } else {
-                    // per-token receive row and gate prob, resolved once per job
+                    // per token: source row of the residual, gate prob, output row
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     if (et < nc) {
-                        const int64_t rr = recv_row(e, cb + et);
-                        s_rrow[et] = rr;
-                        s_rprob[et] = rmeta[rr].prob;
-                    }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-#pragma unroll
-                    for (int i0 = 0; i0 < NMAX; i0 += 16) {
-                        if (i0 < nc) {
-                            __nv_bfloat16 xin[16];  // batch the residual loads
-#pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                if (i0 + i < nc) xin[i] = rx[s_rrow[i0 + i] * a.d + m_glob];
-#pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                if (i0 + i < nc)
-                                    a.res_x_out[(int64_t)(off_e + cb + i0 + i) * a.d + m_glob] = __float2bfloat16(
-                                        __bfloat162float(xin[i]) + s_rprob[i0 + i] * (accv[i0 + i] + bias));
+                        if (a.dense) {  // canonical row -> resident row (route tables)
+                            const int u = s_tok[off_e + cb + et];
+                            s_rrow[et] = u;
+                            s_rprob[et] = s_prob[u];
+                        } else {
+                            const int64_t rr = recv_row(e, cb + et);
+                            const RecvMeta m = rmeta[rr];
+                            s_rrow[et] = rr;
+                            s_rprob[et] = m.prob;
+                            s_rtok[et] = m.token;
+                            s_rexp[et] = m.expert;
                         }
                     }
-                    if (mt == 0 && et < nc) {
-                        const RecvMeta m = rmeta[recv_row(e, cb + et)];
-                        a.res_meta_out[off_e + cb + et] = ResMeta{m.token, m.expert};
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    const __nv_bfloat16* xres = a.dense ? a.res_x_in : rx;
+#pragma unroll 1
+                    for (int col = 0; col < nc; col += 2 * kG) {
+                        __nv_bfloat16 xin[2 * kG];  // residual loads in flight first
+#pragma unroll
+                        for (int i = 0; i < 2 * kG; ++i)
+                            if (col + i < nc) xin[i] = xres[s_rrow[col + i] * a.d + m_glob];
+                        float v[2 * kG];
+                        final4(col, *reinterpret_cast<float(*)[kG]>(&v[0]));
+                        if (col + kG < nc) final4(col + kG, *reinterpret_cast<float(*)[kG]>(&v[kG]));
+#pragma unroll
+                        for (int i = 0; i < 2 * kG; ++i)
+                            if (col + i < nc)
+                                a.res_x_out[(int64_t)(off_e + cb + col + i) * a.d + m_glob] = __float2bfloat16(
+                                    __bfloat162float(xin[i]) + s_rprob[col + i] * (v[i] + bias));
                     }
+                    if (!from_ws) release_tmem();
+                    if (!a.dense && mt == 0 && et < nc)  // dense: the token's own CTA wrote it
+                        a.res_meta_out[off_e + cb + et] = ResMeta{s_rtok[et], s_rexp[et]};
                 }
             }
         }
         if (ts2 && et == 0) ts2[12] = ptx::globaltimer();
+      }  // epilogue warps
     }
     __syncthreads();
     if (tid == 0) tl_mark(a.tl, 3);
@@ -917,7 +1144,7 @@ exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int n
     if (a.tpc > 32) return invalid("token slice too large for the fused layer kernel");
     // (token tile, weight stages, token stages): ~208 KB of rings each
     if (nmax <= 32) return launch_nmax<32, 10, 12>(maps, a, s);
-    if (nmax <= 64) return launch_nmax<64, 8, 10>(maps, a, s);
+    if (nmax <= 64) return launch_nmax<64, 10, 6>(maps, a, s);
     return launch_nmax<128, 6, 7>(maps, a, s);
 }
 

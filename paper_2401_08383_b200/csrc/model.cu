@@ -135,7 +135,8 @@ struct exf_model {
     uint32_t* gbar = nullptr;               // [2] gate_dispatch grid barrier
     // fused layer kernel (one launch per layer)
     bool fused = true;
-    int f_ctas = 148, f_tpc = 8, f_kbp = 8, f_S1 = 1, f_S2 = 1, f_max_chunks = 1;
+    bool dense = false;                     // fused, single GPU: dense over resident tokens
+    int f_ctas = 148, f_tpc = 8, f_kbp = 8, f_S1 = 1, f_S2 = 1, f_max_chunks = 1, f_nmax = 32;
     float* ws = nullptr;                    // split-K partials
     int32_t* item_ctr = nullptr;            // split-K arrivals per tile/chunk
     int32_t* hdone = nullptr;               // [2][E_loc]
@@ -378,10 +379,8 @@ FusedArgs fused_args(exf_model* m, int j) {
     a.H = m->H;
     a.b1 = m->b1 + (int64_t)j * m->E_loc * c.d_ffn;
     a.b2 = m->b2 + (int64_t)j * m->E_loc * c.d_model;
-    a.w1 = m->w1 + (int64_t)j * m->E_loc * c.d_ffn * c.d_model;
-    a.w2 = m->w2 + (int64_t)j * m->E_loc * c.d_ffn * c.d_model;
-    a.a_probe = getenv("EXF_A_PROBE") ? 1 : 0;
-    a.l2_pre = getenv("EXF_L2_PREFETCH") ? atoi(getenv("EXF_L2_PREFETCH")) : 0;
+    a.dense = m->dense ? 1 : 0;
+    a.dbg = std::getenv("EXF_DBG") ? std::atoi(std::getenv("EXF_DBG")) : 0;
     a.res_x_out = m->res_x[(j + 1) & 1];
     a.res_meta_out = m->res_meta[(j + 1) & 1];
     a.n_res_out = m->n_res + ((j + 1) & 1);
@@ -406,7 +405,7 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
         case 5: {  // fused layer kernel (gate..GEMM2 in one launch)
             if (j < 0 || j >= c.num_layers) return invalid("layer out of range");
             const CUtensorMap maps[4] = {m->tmap1[j], m->tmap2[j], m->gmap_recv, m->gmap_h};
-            return launch_layer_fused(maps, fused_args(m, j), m->nmax, s);
+            return launch_layer_fused(maps, fused_args(m, j), m->f_nmax, s);
         }
         case 0:
             if (!x_in) return invalid("null input");
@@ -490,7 +489,6 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     EXF_M(dalloc(&m->n_res, 2));
     EXF_M(dalloc(&m->expert, (size_t)C));
     EXF_M(dalloc(&m->prob, (size_t)C));
-    EXF_M(dalloc(&m->H, (size_t)C * f));
     EXF_M(dalloc(&m->hist, (size_t)(L - 1) * E * E));
     EXF_M(dalloc(&m->crossed, (size_t)L));
     EXF_M(dalloc(&m->trace, (size_t)C * L));
@@ -511,7 +509,14 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         // products then spread over 8 warps of many CTAs
         m->f_tpc = std::max(1, (C + m->f_ctas - 1) / m->f_ctas);
         if (m->f_tpc > 32 || d > 2048 || E > 64) m->fused = false;  // two-kernel path instead
-        const int nmax_f = m->nmax <= 32 ? 32 : (m->nmax <= 64 ? 64 : 128);
+        // single GPU: every expert is local, so the layer runs dense over all
+        // resident tokens and the token phase leaves the GEMMs' critical path
+        m->dense = m->fused && c.world_size == 1 && m->f_tpc == 1;
+        if (const char* env = std::getenv("EXF_DENSE")) m->dense = m->dense && std::atoi(env) != 0;
+        const int tok = m->dense ? C : m->nmax;
+        const int nmax_f = tok <= 32 ? 32 : (tok <= 64 ? 64 : 128);
+        m->f_nmax = nmax_f;
+        EXF_M(dalloc(&m->H, (size_t)C * f));
         plan_fused(m->E_loc, d, f, m->f_ctas, &m->f_kbp, &m->f_S1, &m->f_S2);
         m->f_max_chunks = (C + nmax_f - 1) / nmax_f;
         const int64_t slots = (int64_t)m->E_loc * (f / 128 + d / 128) * m->f_max_chunks;

@@ -131,15 +131,35 @@ struct FusedArgs {
     int32_t* item_ctr;   // arrivals per (gemm, expert, tile, chunk)
     int32_t* hdone;      // [2 parity][E_loc] completed GEMM1 (tile, chunk) units
     int32_t S1, S2, kbp, max_chunks;
-    const __nv_bfloat16* w1;  // [E_loc][dff][d] of this layer
-    const __nv_bfloat16* w2;  // [E_loc][d][dff] of this layer
-    int32_t a_probe;          // diagnostics: contiguous 16 KB A loads (wrong numerics)
-    int32_t l2_pre;           // weight tiles per CTA prefetched into L2 before the PDL wait
+    // dense single-GPU mode (G == 1, one token per CTA): GEMM1's MMAs run over
+    // every resident token from the PDL wait on, while each token's CTA gates
+    // it and publishes {epoch, slot, prob} in one 64-bit route flag; GEMM1's
+    // epilogue keeps routed rows only, GEMM2 runs on the compact H
+    int32_t dense;
+    int32_t dbg;  // diagnostics knob (EXF_DBG), 0 in production
     unsigned long long* tl;
     uint64_t* tstamp;    // optional per-CTA stamps [grid][16] (diagnostics)
 };
 
 __host__ __device__ inline int64_t bytes_bf16(int64_t n) { return n * 2; }
+
+// GELU(v) = v/2 (1 + erf(v/sqrt2)) with erf from Abramowitz-Stegun 7.1.26
+// (|error| <= 1.5e-7, far below the bf16 rounding of H; the oracle uses exact
+// erf, oracle/exflow_model_oracle.c): one reciprocal, one exp2, five FMAs.
+// libdevice erff's branchy polynomial cost ~190 cycles per value on the one
+// epilogue warp of each SM sub-partition (~3000 cycles per 16-token group),
+// which made the expert epilogues the critical path.
+__device__ __forceinline__ float gelu_erf(float v) {
+    const float z = fabsf(v) * 0.70710678118654752440f;
+    const float t = __fdividef(1.0f, fmaf(0.3275911f, z, 1.0f));
+    float p = fmaf(1.061405429f, t, -1.453152027f);
+    p = fmaf(p, t, 1.421413741f);
+    p = fmaf(p, t, -0.284496736f);
+    p = fmaf(p, t, 0.254829592f);
+    const float e = exp2f(-z * z * 1.44269504088896341f);
+    const float erf_abs = fmaf(-p * t, e, 1.0f);
+    return 0.5f * v * (1.0f + copysignf(erf_abs, v));
+}
 
 // error codes written to the device error word before a trap
 enum : int {

@@ -48,8 +48,9 @@ def main():
     t2 = buf[1].astype(np.int64)
     r2 = (t2 - t0) / 1000.0
     j0 = rel[:, 2]
-    print("B producer pass at it=0,2,..,14 rel. job-0 first MMA:",
-          " ".join(f"{(r2[:, k] - j0).mean():.2f}" for k in range(8)))
+    print("GEMM1 epilogue store-loop cycles per job (median over CTAs, job 0..3):",
+          [int(np.median(t2[:, k])) for k in range(4)], "; job 0 by epilogue warp 4..7:",
+          [int(np.median(t2[:, 4 + k])) for k in range(4)])
     print(f"job 1 MMA: fullB ready {(r2[:, 8] - rel[:, 3]).mean():.2f}, A ready {(r2[:, 9] - rel[:, 3]).mean():.2f} "
           f"after job 0 last MMA")
     print(f"job 0 epilogue: tmem_full at {(r2[:, 10] - rel[:, 3]).mean():.2f} after last MMA, "
@@ -70,6 +71,13 @@ def main():
         v = (cur[:, k] - z) / 1e3
         print(f"  {nm:10s} min {v.min():7.2f} mean {v.mean():7.2f} max {v.max():7.2f}")
     print(f"  first MMA  min {(t[:, 2] - z).min() / 1e3:7.2f} mean {(t[:, 2] - z).mean() / 1e3:7.2f}")
+    print("  dense token warp (rel. prev exit; median/max): gate %s ranks %s barrier %s prefix %s flag %s" % tuple(
+        "%.2f/%.2f" % (np.median((cur[:, k] - z) / 1e3), ((cur[:, k] - z) / 1e3).max()) for k in (12, 13, 14, 7, 2)))
+    r10 = buf[1][:, 10].astype(np.int64)
+    print("  dense GEMM1 epilogue of job 0 (us after tmem_full): tmem-ld %.2f route-wait %.2f stores %.2f bar %.2f "
+          "red %.2f" % tuple(np.median((cur[:, k] - r10) / 1e3) for k in (3, 14, 4, 5, 6)))
+    print("  tmem_full of job 0 rel. prev exit: median %.2f; route tables ready median %.2f" % (
+        np.median((r10 - z) / 1e3), np.median((cur[:, 2] - z) / 1e3)))
     print("  gate detail (n loaded / Wg ready / dot products done / rows staged):")
     for c in range(4):
         print(f"   cta {c}: " + " ".join(f"{(cur[c, k] - z) / 1e3:6.2f}" for k in (11, 12, 13, 14)))
