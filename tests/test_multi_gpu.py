@@ -1,0 +1,32 @@
+"""Real multi-GPU parity (needs >= 2 visible B200s; skipped otherwise): launches
+tests/mgpu_worker.py under torchrun, one process per GPU, for the fused
+one-launch-per-layer path and the two-kernel path. Each rank's kernels
+exchange tokens with the others over NVLink P2P; rank 0 checks every layer
+against the CPU oracle (see the worker's docstring)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _gpus():
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("phased", [False, True])
+def test_two_gpu_parity(phased):
+    n = _gpus()
+    if n < 2:
+        pytest.skip("needs two GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29631" if phased else "29633",
+           os.path.join(HERE, "mgpu_worker.py")] + (["--phased"] if phased else [])
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "path OK" in r.stdout
