@@ -32,6 +32,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <vector>
 
 namespace exf {
 
@@ -186,9 +187,12 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int P = gridDim.x;
     const int mt1 = a.dff / kBM, mt2 = a.d / kBM;
-    const int NP1 = a.E_loc * mt1 * a.S1;
-    const int NP = NP1 + a.E_loc * mt2 * a.S2;
-    const int kbp = a.kbp;
+    // this CTA's pieces of the static stream-K schedule (host-built, fixed
+    // per model: safe to read before the PDL wait)
+    __shared__ Piece s_pc[kMaxPieces];
+    const int pc0 = a.piece_off[blockIdx.x];
+    const int npc = a.piece_off[blockIdx.x + 1] - pc0;
+    if (tid < npc) s_pc[tid] = a.pieces[pc0 + tid];
     if (tid == 0) tl_mark(a.tl, 0);
     uint64_t* ts = a.tstamp ? a.tstamp + (int64_t)blockIdx.x * 16 : nullptr;
     if (ts && tid == 0) ts[0] = ptx::globaltimer();
@@ -204,24 +208,6 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         if (ts3 && threadIdx.x == 0) ts3[k] = ptx::globaltimer();
     };
     mark3(0);
-
-    // piece p -> (gemm, expert, tile, k-part)
-    auto decode = [&](int p, int& g, int& e, int& mt, int& kp) {
-        if (p < NP1) {
-            g = 0;
-            kp = p % a.S1;
-            const int it = p / a.S1;
-            e = it / mt1;
-            mt = it - e * mt1;
-        } else {
-            g = 1;
-            const int q2 = p - NP1;
-            kp = q2 % a.S2;
-            const int it = q2 / a.S2;
-            e = it / mt2;
-            mt = it - e * mt2;
-        }
-    };
 
     // ---------------- independent prologue (overlaps the previous kernel)
     if (tid == 0) {
@@ -246,8 +232,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = misc[0];
-    const int first_p = blockIdx.x < NP ? (int)blockIdx.x : -1;
-    const int npre = first_p >= 0 ? min(kbp, STAGES) : 0;
+    const int npre = npc > 0 ? min((int)s_pc[0].nkb, STAGES) : 0;
     const uint64_t pol_a = ptx::policy_evict_first();
     // the layer's gate matrix is a weight too: bulk-copy it into the B-stage
     // region (unused until the expert phase) when it fits, before the wait
@@ -260,15 +245,14 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     if (tid < a.E) s_key[tid] = a.gpu_of[tid] * a.E_loc + a.slot_of[tid];
     const bool wg_smem = wg_bytes <= (uint32_t)(BST * S::kB) && gate_cta;
     auto prefetch_a = [&]() {  // first weight stages of the CTA's first piece
-        if (first_p < 0) return;
-        int g, e, mt, kp;
-        decode(first_p, g, e, mt, kp);
-        const CUtensorMap* tm = g == 0 ? &tmA1 : &tmA2;
-        const int rows = g == 0 ? a.dff : a.d;
+        if (npc == 0) return;
+        const Piece pc = s_pc[0];
+        const CUtensorMap* tm = pc.g == 0 ? &tmA1 : &tmA2;
+        const int rows = pc.g == 0 ? a.dff : a.d;
         for (int kb = 0; kb < npre; ++kb) {
             ptx::mbar_arrive_expect_tx(&full[kb], S::kA);
-            ptx::tma_load_2d(smem + S::kOffA + kb * S::kA, tm, &full[kb], (kp * kbp + kb) * kBK,
-                             e * rows + mt * kBM, pol_a);
+            ptx::tma_load_2d(smem + S::kOffA + kb * S::kA, tm, &full[kb], (pc.kb0 + kb) * kBK,
+                             pc.e * rows + pc.mt * kBM, pol_a);
         }
     };
     if (warp == 0 && lane == 0) {
@@ -597,7 +581,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // chunks of piece p (the CTA's first piece always runs >= 1: prefetched)
     auto nchunks = [&](int p, int g, int e) {
         const int c = (cnt(g, e) + NMAX - 1) / NMAX;
-        return (p == first_p && c == 0) ? 1 : c;
+        return (p == 0 && c == 0) ? 1 : c;
     };
     auto slot_of_tile = [&](int g, int e, int mt, int c) -> int64_t {
         const int64_t base = g == 0 ? 0 : (int64_t)a.E_loc * mt1 * a.max_chunks;
@@ -609,9 +593,9 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         // ================= A producer: weight tiles via TMA =================
         if (lane == 0) {
             int it = 0;
-            for (int p = blockIdx.x; p < NP; p += P) {
-                int g, e, mt, kp;
-                decode(p, g, e, mt, kp);
+            for (int p = 0; p < npc; ++p) {
+                const Piece pc = s_pc[p];
+                const int g = pc.g, e = pc.e, mt = pc.mt, kbp = pc.nkb;
                 const int nch = nchunks(p, g, e);
                 const CUtensorMap* tm = g == 0 ? &tmA1 : &tmA2;
                 const int rows = g == 0 ? a.dff : a.d;
@@ -621,10 +605,10 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         const int st = it % STAGES;
                         const uint32_t ph = (it / STAGES) & 1;
                         ptx::mbar_wait(&empty[st], ph ^ 1, a.err, ERR_TIMEOUT_PIPE);
-                        if (ts && it == kbp) ts[12] = ptx::globaltimer();  // job 1's first A tile
+                        if (ts && p == 1 && c == 0 && kb == 0) ts[12] = ptx::globaltimer();  // job 1's first A tile
                         ptx::mbar_arrive_expect_tx(&full[st], S::kA);
                         ptx::tma_load_2d(smem + S::kOffA + st * S::kA, tm, &full[st],
-                                         (kp * kbp + kb) * kBK, e * rows + mt * kBM, pol_a);
+                                         (pc.kb0 + kb) * kBK, e * rows + mt * kBM, pol_a);
                     }
             }
             if (ts2) ts2[14] = ptx::globaltimer();
@@ -632,9 +616,9 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     } else if (warp == 1) {
         // ================= MMA issuer =================
         int it = 0, job = 0;
-        for (int p = blockIdx.x; p < NP; p += P) {
-            int g, e, mt, kp;
-            decode(p, g, e, mt, kp);
+        for (int p = 0; p < npc; ++p) {
+            const Piece pc = s_pc[p];
+            const int g = pc.g, e = pc.e, kbp = pc.nkb;
             const int n_e = cnt(g, e);
             const int nch = nchunks(p, g, e);
             for (int c = 0; c < nch; ++c, ++job) {
@@ -650,10 +634,10 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     const uint32_t ph = (it / STAGES) & 1;
                     const int sb = it % BST;
                     ptx::mbar_wait(&fullB[sb], (it / BST) & 1, a.err, ERR_TIMEOUT_PIPE);
-                    if (ts2 && lane == 0 && it == kbp) ts2[8] = ptx::globaltimer();
+                    if (ts2 && lane == 0 && job == 1 && kb == 0) ts2[8] = ptx::globaltimer();
                     if (ts3 && lane == 0 && it == 0) ts3[9] = ptx::globaltimer();
                     ptx::mbar_wait(&full[st], ph, a.err, ERR_TIMEOUT_PIPE);
-                    if (ts2 && lane == 0 && it == kbp) ts2[9] = ptx::globaltimer();
+                    if (ts2 && lane == 0 && job == 1 && kb == 0) ts2[9] = ptx::globaltimer();
                     if (ts3 && lane == 0 && it == 0) ts3[10] = ptx::globaltimer();
                     ptx::tc_fence_after();
                     ptx::fence_proxy_async_smem();  // cp.async (generic) rows -> tensor-core reads
@@ -685,9 +669,9 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         if (ts3 && lane == 0) ts3[8] = ptx::globaltimer();
         int it = 0;
         int waited_e = -1;
-        for (int p = blockIdx.x; p < NP; p += P) {
-            int g, e, mt, kp;
-            decode(p, g, e, mt, kp);
+        for (int p = 0; p < npc; ++p) {
+            const Piece pc = s_pc[p];
+            const int g = pc.g, e = pc.e, kbp = pc.nkb;
             const int n_e = cnt(g, e);
             const int off_e = tab[e * S::kTabInts + 1];
             const int nch = nchunks(p, g, e);
@@ -718,9 +702,9 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 for (int kb = 0; kb < kbp; ++kb, ++it) {
                     const int sb = it % BST;
                     ptx::mbar_wait(&emptyB[sb], ((it / BST) & 1) ^ 1, a.err, ERR_TIMEOUT_PIPE);
-                    if (ts && lane == 0 && it == kbp) ts[13] = ptx::globaltimer();  // job 1's first B rows
+                    if (ts && lane == 0 && p == 1 && c == 0 && kb == 0) ts[13] = ptx::globaltimer();  // job 1's first B rows
                     uint8_t* sbase = smem + S::kOffB + sb * S::kB;
-                    const __nv_bfloat16* kcol = src + (int64_t)(kp * kbp + kb) * kBK + cc * 8;
+                    const __nv_bfloat16* kcol = src + (int64_t)(pc.kb0 + kb) * kBK + cc * 8;
 #pragma unroll
                     for (int j = 0; j < NMAX / 4; ++j) {
                         const int r = (lane >> 3) + 4 * j;
@@ -862,13 +846,13 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         const int et = tid - 128;  // TMEM lane == weight row within the tile
         const int lane_base = (warp & 3) * 32;
         int job = 0;
-        for (int p = blockIdx.x; p < NP; p += P) {
-            int g, e, mt, kp;
-            decode(p, g, e, mt, kp);
+        for (int p = 0; p < npc; ++p) {
+            const Piece pc = s_pc[p];
+            const int g = pc.g, e = pc.e, mt = pc.mt, kp = pc.kidx;
             const int n_e = cnt(g, e);
             const int off_e = tab[e * S::kTabInts + 1];
             const int nch = nchunks(p, g, e);
-            const int Sg = g == 0 ? a.S1 : a.S2;
+            const int Sg = pc.S;  // contributors to this tile
             const int mrows = g == 0 ? a.dff : a.d;
             const int m_glob = mt * kBM + et;
             const float bias = __bfloat162float((g == 0 ? a.b1 : a.b2)[(int64_t)e * mrows + m_glob]);
@@ -897,7 +881,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     continue;
                 }
                 const int64_t slot = slot_of_tile(g, e, mt, c);
-                const int Smax = max(a.S1, a.S2);
+                const int Smax = a.max_contrib;
                 bool from_ws = false;  // finished values come from the k-ordered partial sum
                 if (Sg > 1) {
                     // park the partial; the last-arriving piece of this tile
@@ -1117,25 +1101,72 @@ int fused_ctas() {
     return sms;
 }
 
-// Uniform split-K piece size: the largest kbp (64-wide k-blocks per piece)
-// dividing both K's that minimises rounds(pieces / CTAs) * kbp.
-void plan_fused(int E_loc, int d, int dff, int ctas, int* kbp_out, int* S1, int* S2) {
-    const int k1 = d / kBK, k2 = dff / kBK;
-    long best = -1;
-    int best_kbp = 1;
-    for (int kbp = 32; kbp >= 1; kbp /= 2) {
-        if (k1 % kbp || k2 % kbp) continue;
-        const long np = (long)E_loc * (dff / kBM) * (k1 / kbp) + (long)E_loc * (d / kBM) * (k2 / kbp);
-        // each piece also pays a pipeline/epilogue overhead worth ~4 k-blocks
-        const long cost = ((np + ctas - 1) / ctas) * (kbp + 4);
-        if (best < 0 || cost < best) {
-            best = cost;
-            best_kbp = kbp;
-        }
+// Static per-CTA piece lists from a time-aware greedy list scheduler (host,
+// once per model). GEMM1 tiles are cut into pieces of <= 16 k-blocks (whole
+// tiles at d <= 1024: no partials), GEMM2 tiles into pieces of <= 8 k-blocks.
+// Pieces are placed expert-major, GEMM1 first, each on the CTA that can start
+// it earliest; a GEMM2 piece of expert e is ready only once e's GEMM1 pieces
+// are modelled complete plus the epilogue/flag latency, so GEMM2 of early
+// experts overlaps GEMM1 of later ones while every CTA streams about the same
+// number of k-blocks (uniform round-robin pieces left the last of 4 rounds on
+// < half the SMs; equal stream-K shares made every CTA wait for every GEMM1).
+// A CTA's GEMM2 pieces always follow its GEMM1 pieces (deadlock freedom of the
+// hdone waits). Returns false if a CTA would need more than kMaxPieces.
+bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece>& pieces,
+                          std::vector<int32_t>& off, int* max_contrib, int* max_pieces) {
+    const int k1 = d / kBK, k2 = dff / kBK, mt1 = dff / kBM, mt2 = d / kBM;
+    // measured at configs[1]: (16, 16) 45.9 us/layer; (16, 8) 53.2, (16, 12) 49.8,
+    // (16, 32) 50.9, (8, 8) 65.2: per-piece costs exceed the model's estimate
+    int psz[2] = {16, 16};
+    if (const char* s = std::getenv("EXF_PIECE1")) psz[0] = std::max(1, std::atoi(s));
+    if (const char* s = std::getenv("EXF_PIECE2")) psz[1] = std::max(1, std::atoi(s));
+    const int kk[2] = {k1, k2}, mts[2] = {mt1, mt2};
+    constexpr double kSwitch = 1.0;   // per-piece pipeline cost, in k-blocks
+    constexpr double kReady = 6.0;    // GEMM1 epilogue + hdone + token-row load latency
+    std::vector<double> free_at(ctas, 0.0), done1(E_loc, 0.0);
+    std::vector<std::vector<Piece>> per(ctas);
+    for (int g = 0; g < 2; ++g) {
+        const int S = (kk[g] + psz[g] - 1) / psz[g];
+        for (int e = 0; e < E_loc; ++e)
+            for (int mt = 0; mt < mts[g]; ++mt)
+                for (int s = 0; s < S; ++s) {
+                    Piece p{};
+                    p.g = (int16_t)g;
+                    p.e = (int16_t)e;
+                    p.mt = (int16_t)mt;
+                    p.kb0 = (int16_t)(s * psz[g]);
+                    p.nkb = (int16_t)std::min(psz[g], kk[g] - s * psz[g]);
+                    p.kidx = (int16_t)s;
+                    p.S = (int16_t)S;
+                    const double ready = g == 0 ? 0.0 : done1[e] + kReady;
+                    int best = 0;
+                    double best_start = 1e300;
+                    for (int c = 0; c < ctas; ++c) {
+                        const double st = std::max(free_at[c], ready);
+                        if (st < best_start - 1e-9) {
+                            best_start = st;
+                            best = c;
+                        }
+                    }
+                    free_at[best] = best_start + p.nkb + kSwitch;
+                    if (g == 0) done1[e] = std::max(done1[e], free_at[best]);
+                    per[best].push_back(p);
+                }
     }
-    *kbp_out = best_kbp;
-    *S1 = k1 / best_kbp;
-    *S2 = k2 / best_kbp;
+    pieces.clear();
+    off.assign(ctas + 1, 0);
+    *max_pieces = 0;
+    *max_contrib = 1;
+    for (int c = 0; c < ctas; ++c) {
+        off[c] = (int32_t)pieces.size();
+        for (const Piece& p : per[c]) {
+            pieces.push_back(p);
+            *max_contrib = std::max(*max_contrib, (int)p.S);
+        }
+        *max_pieces = std::max(*max_pieces, (int)per[c].size());
+    }
+    off[ctas] = (int32_t)pieces.size();
+    return *max_pieces <= kMaxPieces;
 }
 
 exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int nmax, cudaStream_t s) {

@@ -38,7 +38,8 @@ exf_status launch_ffn_gemm(const CUtensorMap& map, const CUtensorMap& mapB, cons
 exf_status make_gather_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols);
 exf_status plan_ffn_gemm(int nmax, int mode, int items, int K, int* ksplit, int* clusters);
 exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int nmax, cudaStream_t s);
-void plan_fused(int E_loc, int d, int dff, int ctas, int* kbp, int* S1, int* S2);
+bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece>& pieces,
+                          std::vector<int32_t>& off, int* max_contrib, int* max_pieces);
 int fused_ctas();
 
 namespace {
@@ -136,7 +137,9 @@ struct exf_model {
     // fused layer kernel (one launch per layer)
     bool fused = true;
     bool dense = false;                     // fused, single GPU: dense over resident tokens
-    int f_ctas = 148, f_tpc = 8, f_kbp = 8, f_S1 = 1, f_S2 = 1, f_max_chunks = 1, f_nmax = 32;
+    int f_ctas = 148, f_tpc = 8, f_max_chunks = 1, f_nmax = 32, f_max_contrib = 1, f_max_pieces = 0;
+    Piece* f_pieces = nullptr;              // stream-K schedule of the fused kernel
+    int32_t* f_piece_off = nullptr;         // [ctas + 1]
     float* ws = nullptr;                    // split-K partials
     int32_t* item_ctr = nullptr;            // split-K arrivals per tile/chunk
     int32_t* hdone = nullptr;               // [2][E_loc]
@@ -387,9 +390,9 @@ FusedArgs fused_args(exf_model* m, int j) {
     a.ws = m->ws;
     a.item_ctr = m->item_ctr;
     a.hdone = m->hdone;
-    a.S1 = m->f_S1;
-    a.S2 = m->f_S2;
-    a.kbp = m->f_kbp;
+    a.pieces = m->f_pieces;
+    a.piece_off = m->f_piece_off;
+    a.max_contrib = m->f_max_contrib;
     a.max_chunks = m->f_max_chunks;
     // the per-CTA stamp rows replace the atomic step timeline here: 148-way
     // atomics on one word distort the phases they measure
@@ -517,10 +520,20 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         const int nmax_f = tok <= 32 ? 32 : (tok <= 64 ? 64 : 128);
         m->f_nmax = nmax_f;
         EXF_M(dalloc(&m->H, (size_t)C * f));
-        plan_fused(m->E_loc, d, f, m->f_ctas, &m->f_kbp, &m->f_S1, &m->f_S2);
+        std::vector<Piece> pieces;
+        std::vector<int32_t> off;
+        if (!build_fused_schedule(m->E_loc, d, f, m->f_ctas, pieces, off, &m->f_max_contrib,
+                                  &m->f_max_pieces))
+            m->fused = m->dense = false;  // too many pieces per CTA: two-kernel path
+        EXF_M(dalloc(&m->f_pieces, pieces.size()));
+        EXF_M(dalloc(&m->f_piece_off, off.size()));
+        EXF_CUDA_TRY(cudaMemcpy(m->f_pieces, pieces.data(), pieces.size() * sizeof(Piece),
+                                cudaMemcpyHostToDevice));
+        EXF_CUDA_TRY(cudaMemcpy(m->f_piece_off, off.data(), off.size() * sizeof(int32_t),
+                                cudaMemcpyHostToDevice));
         m->f_max_chunks = (C + nmax_f - 1) / nmax_f;
         const int64_t slots = (int64_t)m->E_loc * (f / 128 + d / 128) * m->f_max_chunks;
-        const int smax = std::max(m->f_S1, m->f_S2);
+        const int smax = m->f_max_contrib;
         EXF_M(dalloc(&m->ws, smax > 1 ? (size_t)(slots * smax * nmax_f * 128) : 1));
         EXF_M(dalloc(&m->item_ctr, (size_t)slots));
         EXF_M(dalloc(&m->hdone, (size_t)2 * m->E_loc));
@@ -558,7 +571,7 @@ exf_status exf_model_destroy(exf_model* m) {
                     m->res_x[1], m->res_meta[0], m->res_meta[1], m->n_res, m->expert, m->prob, m->H,
                     m->hist, m->crossed, m->trace, m->forced, m->step, m->err, m->done_ctr,
                     m->cta_cnt, m->gbar, m->tl, m->ws, m->item_ctr, m->hdone, m->fbar,
-                    m->f_cta_cnt,
+                    m->f_cta_cnt, m->f_pieces, m->f_piece_off,
                     m->d_peers, m->sym_base, m->tstamp};
     for (void* p : bufs)
         if (p) cudaFree(p);
@@ -810,9 +823,9 @@ exf_status exf_model_describe(exf_model* m, char* buf, int32_t len) {
     if (m->fused)
         s += ", \"path\": \"fused\", \"layer_kernel\": {\"ctas\": " + std::to_string(m->f_ctas) +
              ", \"tokens_per_cta\": " + std::to_string(m->f_tpc) +
-             ", \"kblocks_per_piece\": " + std::to_string(m->f_kbp) +
-             ", \"gemm1_ksplit\": " + std::to_string(m->f_S1) +
-             ", \"gemm2_ksplit\": " + std::to_string(m->f_S2) + "}}";
+             ", \"dense\": " + std::string(m->dense ? "true" : "false") +
+             ", \"schedule\": \"stream-k\", \"max_pieces_per_cta\": " + std::to_string(m->f_max_pieces) +
+             ", \"max_tile_contributors\": " + std::to_string(m->f_max_contrib) + "}}";
     else
         s += ", \"path\": \"two-kernel\", \"gemm1\": {\"ksplit\": " + std::to_string(m->ks1) +
              ", \"clusters\": " + std::to_string(m->cl1) + "}, \"gemm2\": {\"ksplit\": " +

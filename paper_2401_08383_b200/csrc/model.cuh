@@ -98,6 +98,17 @@ struct FfnArgs {
     unsigned long long* tl;      // optional step timeline [4] (diagnostics)
 };
 
+// One piece of the fused kernel's static stream-K schedule: a contiguous run
+// of 64-wide k-blocks of one (gemm, local expert, 128-row tile). Every CTA
+// owns an equal share of GEMM1's and of GEMM2's k-blocks, cut at tile edges;
+// a tile's contributors (S, in k order kidx) park fp32 partials and the last
+// to arrive sums them in k order.
+struct Piece {
+    int16_t g, e, mt, kb0;
+    int16_t nkb, kidx, S, pad;
+};
+constexpr int kMaxPieces = 16;  // per CTA
+
 // Arguments of the fused per-layer kernel (layer_fused.cu).
 struct FusedArgs {
     // token side
@@ -130,7 +141,9 @@ struct FusedArgs {
     float* ws;           // split-K partials
     int32_t* item_ctr;   // arrivals per (gemm, expert, tile, chunk)
     int32_t* hdone;      // [2 parity][E_loc] completed GEMM1 (tile, chunk) units
-    int32_t S1, S2, kbp, max_chunks;
+    const Piece* pieces;       // stream-K schedule, CTA c owns [piece_off[c], piece_off[c+1])
+    const int32_t* piece_off;  // [grid + 1]
+    int32_t max_contrib, max_chunks;
     // dense single-GPU mode (G == 1, one token per CTA): GEMM1's MMAs run over
     // every resident token from the PDL wait on, while each token's CTA gates
     // it and publishes {epoch, slot, prob} in one 64-bit route flag; GEMM1's
