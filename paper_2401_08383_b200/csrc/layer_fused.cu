@@ -1102,8 +1102,9 @@ int fused_ctas() {
 }
 
 // Static per-CTA piece lists from a time-aware greedy list scheduler (host,
-// once per model). GEMM1 tiles are cut into pieces of <= 16 k-blocks (whole
-// tiles at d <= 1024: no partials), GEMM2 tiles into pieces of <= 8 k-blocks.
+// once per model). GEMM1 and GEMM2 tiles are cut into pieces of <= 16
+// k-blocks (whole GEMM1 tiles at d <= 1024: no partials; EXF_PIECE1 /
+// EXF_PIECE2 override).
 // Pieces are placed expert-major, GEMM1 first, each on the CTA that can start
 // it earliest; a GEMM2 piece of expert e is ready only once e's GEMM1 pieces
 // are modelled complete plus the epilogue/flag latency, so GEMM2 of early
@@ -1125,7 +1126,10 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
     constexpr double kReady = 6.0;    // GEMM1 epilogue + hdone + token-row load latency
     std::vector<double> free_at(ctas, 0.0), done1(E_loc, 0.0);
     std::vector<std::vector<Piece>> per(ctas);
-    for (int g = 0; g < 2; ++g) {
+    // EXF_FILL2=1: GEMM2 as a stream-K fill (below); measured slower at
+    // configs[1] (48.3 vs 45.8 us/layer): long GEMM2 runs stall on hdone
+    const bool fill2 = std::getenv("EXF_FILL2") != nullptr;
+    for (int g = 0; g < (fill2 ? 1 : 2); ++g) {
         const int S = (kk[g] + psz[g] - 1) / psz[g];
         for (int e = 0; e < E_loc; ++e)
             for (int mt = 0; mt < mts[g]; ++mt)
@@ -1152,6 +1156,58 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
                     if (g == 0) done1[e] = std::max(done1[e], free_at[best]);
                     per[best].push_back(p);
                 }
+    }
+    if (fill2) {
+        // GEMM2 as a stream-K fill: CTAs in order of the time they finish
+        // their GEMM1 tiles receive contiguous runs of GEMM2's expert-major
+        // (tile, k-block) sequence, sized so that every CTA ends together;
+        // early-free CTAs get the early experts, whose GEMM1 ended first.
+        const int64_t U2 = (int64_t)E_loc * mt2 * k2;
+        std::vector<int> order(ctas);
+        for (int c = 0; c < ctas; ++c) order[c] = c;
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return free_at[x] < free_at[y]; });
+        // finish time T: sum_c max(0, T - free_c - switch) = U2
+        double lo = 0, hi = 1e9;
+        for (int it = 0; it < 200; ++it) {
+            const double T = 0.5 * (lo + hi);
+            double s = 0;
+            for (int c = 0; c < ctas; ++c) s += std::max(0.0, T - free_at[c] - 2 * kSwitch);
+            (s >= (double)U2 ? hi : lo) = T;
+        }
+        std::vector<int64_t> share(ctas, 0);
+        int64_t given = 0;
+        double acc = 0;
+        for (int i = 0; i < ctas; ++i) {  // integer shares by cumulative rounding
+            const int c = order[i];
+            acc += std::max(0.0, hi - free_at[c] - 2 * kSwitch);
+            const int64_t upto = std::min<int64_t>(U2, (int64_t)std::llround(acc));
+            share[c] = std::max<int64_t>(0, upto - given);
+            given += share[c];
+        }
+        share[order[ctas - 1]] += U2 - given;
+        std::vector<int16_t> cnt(E_loc * mt2, 0);
+        int64_t u = 0;
+        for (int i = 0; i < ctas; ++i) {
+            const int c = order[i];
+            const int64_t end = u + share[c];
+            while (u < end) {
+                const int64_t tile = u / k2;
+                const int kb0 = (int)(u - tile * k2);
+                const int n = (int)(std::min<int64_t>(end, (tile + 1) * k2) - u);
+                Piece p{};
+                p.g = 1;
+                p.e = (int16_t)(tile / mt2);
+                p.mt = (int16_t)(tile % mt2);
+                p.kb0 = (int16_t)kb0;
+                p.nkb = (int16_t)n;
+                p.kidx = cnt[tile]++;
+                per[c].push_back(p);
+                u += n;
+            }
+        }
+        for (auto& v : per)
+            for (auto& p : v)
+                if (p.g == 1) p.S = cnt[p.e * mt2 + p.mt];
     }
     pieces.clear();
     off.assign(ctas + 1, 0);
