@@ -329,6 +329,13 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    # DRAM bytes per launch of the dominant kernel from the committed
+    # `ncu --set full` capture (profiles/), when it matches this kernel
+    traffic, traffic_src = None, None
+    ncu_path = os.path.join(ROOT, "profiles", "r01_fused_ncu_summary.json")
+    if fused and n == 1 and os.path.exists(ncu_path):
+        summ = json.load(open(ncu_path))
+        traffic, traffic_src = summ.get("traffic_bytes_per_launch"), "profiles/r01_fused_ncu_summary.json"
     launches = model.launches_per_step()
 
     # ---- CPU baseline (rank 0, N=1 only)
@@ -357,7 +364,7 @@ def main():
         "roofline": {"kernel": ("layer_fused_kernel (gate+dispatch+GEMM1+GEMM2 per layer, tcgen05)"
                                 if fused else "ffn_gemm_kernel (GEMM1+GEMM2 per layer, tcgen05)"),
                      "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
+                     "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
                      "bytes_per_launch": ffn_bytes, "ms_per_launch": ffn_avg_ms,
                      "bytes_model": "active local experts x (W1+W2+b1+b2) + tokens x (2d in, 4f H rw, 4d out)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
