@@ -265,6 +265,12 @@ exf_status exf_model_describe(exf_model* model, char* buf, int32_t len);
  * of the fused kernel, rows 2/3 = fused token-phase stamps of even/odd layers;
  * requires EXF_FFN_TIMELINE=1 at create time). */
 exf_status exf_model_read_ffn_timeline(exf_model* model, uint64_t* h_stamps, int32_t ctas);
+/* Diagnostics: the last spin timeout of the fused layer kernel, read from
+ * host-mapped memory (valid even after the CUDA context is lost):
+ * out12 = {timed out?, site code (101..112, see csrc/layer_fused.cu), block,
+ * thread, then 8 progress words of that CTA's roles}. Returns 0 if the
+ * channel is not set up (no fused launch yet). */
+int32_t exf_debug_last_timeout(int32_t* out12);
 /* Diagnostics: per (layer, kernel in {gate_dispatch, GEMM1, GEMM2}) globaltimer
  * [first CTA entry, first wait-return, last wait-return, last CTA exit,
  * phase marks 4..7] ([L][3][8] u64); reset != 0 re-arms the timeline. */

@@ -112,6 +112,7 @@ SIGNATURES = {
     "exf_model_launches_per_step": (_I32, [_VP]),
     "exf_model_describe": (C.c_int, [_VP, _VP, _I32]),
     "exf_model_read_ffn_timeline": (C.c_int, [_VP, _VP, _I32]),
+    "exf_debug_last_timeout": (C.c_int32, [_VP]),
     "exf_model_read_step_timeline": (C.c_int, [_VP, _VP, _I32]),
 }
 

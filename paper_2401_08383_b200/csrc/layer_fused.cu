@@ -32,6 +32,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 namespace exf {
@@ -128,12 +129,17 @@ __device__ void grid_barrier(uint32_t* gbar, int32_t* err) {
     __syncthreads();
 }
 
-// A (weights) and B (token rows) run in separate rings: the tiny token tiles
-// get a deeper ring so their gathers run ahead of the weight stream.
+// A (weights) and B (token rows) run in separate rings. A pipeline stage
+// carries kKPS 64-wide k-blocks: the MMA warp's per-stage control work (two
+// barrier waits, a proxy fence, commits) capped the weight stream at ~32 GB/s
+// per SM with one k-block (16 KB) per stage; the TMA ceiling is ~46 GB/s.
+constexpr int kKPS = 2;
 template <int NMAX, int STAGES, int BST>
 struct Smem {
-    static constexpr int kA = kBM * kBK * 2;
-    static constexpr int kB = NMAX * kBK * 2;
+    static constexpr int kA1 = kBM * kBK * 2;    // one k-block of weights (16 KB)
+    static constexpr int kB1 = NMAX * kBK * 2;   // one k-block of token rows
+    static constexpr int kA = kA1 * kKPS;
+    static constexpr int kB = kB1 * kKPS;
     static constexpr int kOffA = 0;
     static constexpr int kOffB = STAGES * kA;
     static constexpr int kOffTab = kOffB + BST * kB;
@@ -190,6 +196,10 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // this CTA's pieces of the static stream-K schedule (host-built, fixed
     // per model: safe to read before the PDL wait)
     __shared__ Piece s_pc[kMaxPieces];
+    __shared__ uint64_t s_iss[STAGES];  // diagnostics: MMA issue time per weight stage
+    __shared__ int s_prog[8];  // diagnostics: A it, MMA it, MMA job, B it, B piece, epi job, epi piece, token
+    if (tid < 8) s_prog[tid] = 0;
+    if (tid == 0 && blockIdx.x == 0) ptx::g_dbg_prog = s_prog;
     const int pc0 = a.piece_off[blockIdx.x];
     const int npc = a.piece_off[blockIdx.x + 1] - pc0;
     if (tid < npc) s_pc[tid] = a.pieces[pc0 + tid];
@@ -232,7 +242,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = misc[0];
-    const int npre = npc > 0 ? min((int)s_pc[0].nkb, STAGES) : 0;
+    const int npre = npc > 0 ? min((int)s_pc[0].nkb / kKPS, STAGES) : 0;  // prefetched stages
     const uint64_t pol_a = ptx::policy_evict_first();
     // the layer's gate matrix is a weight too: bulk-copy it into the B-stage
     // region (unused until the expert phase) when it fits, before the wait
@@ -243,16 +253,18 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // placement tables are stream-ordered host writes, never written by the
     // previous kernel: safe to read before the PDL wait
     if (tid < a.E) s_key[tid] = a.gpu_of[tid] * a.E_loc + a.slot_of[tid];
-    const bool wg_smem = wg_bytes <= (uint32_t)(BST * S::kB) && gate_cta;
+    // (never in dense mode: there the token-row ring is live from the start)
+    const bool wg_smem = !a.dense && wg_bytes <= (uint32_t)(BST * S::kB) && gate_cta;
     auto prefetch_a = [&]() {  // first weight stages of the CTA's first piece
         if (npc == 0) return;
         const Piece pc = s_pc[0];
         const CUtensorMap* tm = pc.g == 0 ? &tmA1 : &tmA2;
         const int rows = pc.g == 0 ? a.dff : a.d;
-        for (int kb = 0; kb < npre; ++kb) {
-            ptx::mbar_arrive_expect_tx(&full[kb], S::kA);
-            ptx::tma_load_2d(smem + S::kOffA + kb * S::kA, tm, &full[kb], (pc.kb0 + kb) * kBK,
-                             pc.e * rows + pc.mt * kBM, pol_a);
+        for (int s = 0; s < npre; ++s) {
+            ptx::mbar_arrive_expect_tx(&full[s], S::kA);
+            for (int j = 0; j < kKPS; ++j)
+                ptx::tma_load_2d(smem + S::kOffA + s * S::kA + j * S::kA1, tm, &full[s],
+                                 (pc.kb0 + s * kKPS + j) * kBK, pc.e * rows + pc.mt * kBM, pol_a);
         }
     };
     if (warp == 0 && lane == 0) {
@@ -321,7 +333,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     const int chunks = a.d >> 8;
     if (wg_smem) {
         // always: the copy must land before the B ring reuses this region
-        ptx::mbar_wait(wg_bar, 0, a.err, ERR_TIMEOUT_PIPE);
+        ptx::mbar_wait(wg_bar, 0, a.err, 101);
     }
     mark3(12);
     if (spec && lane == 0) s_meta_spec[warp] = mk;
@@ -528,7 +540,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         for (int w = tid; w < a.G * P; w += kThreads) {
             const uint64_t* fw = f + (int64_t)(w / P) * kMaxCtas + (w % P);
             ptx::SpinGuard g;
-            while (ptx::flag_read(fw, a.G > 1) < epoch) g.step(a.err, ERR_TIMEOUT_DISPATCH);
+            while (ptx::flag_read(fw, a.G > 1) < epoch) g.step(a.err, 112);
         }
     }
     __syncthreads();
@@ -574,7 +586,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     auto cnt = [&](int g, int e) -> int {
         if (a.dense) {
             if (g == 0) return n;
-            ptx::mbar_wait(route_bar, 0, a.err, ERR_TIMEOUT_DISPATCH);
+            ptx::mbar_wait(route_bar, 0, a.err, 102);
         }
         return tab[e * S::kTabInts];
     };
@@ -593,6 +605,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         // ================= A producer: weight tiles via TMA =================
         if (lane == 0) {
             int it = 0;
+            uint64_t hold_ns = 0, hold_n = 0;
             for (int p = 0; p < npc; ++p) {
                 const Piece pc = s_pc[p];
                 const int g = pc.g, e = pc.e, mt = pc.mt, kbp = pc.nkb;
@@ -600,22 +613,33 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 const CUtensorMap* tm = g == 0 ? &tmA1 : &tmA2;
                 const int rows = g == 0 ? a.dff : a.d;
                 for (int c = 0; c < nch; ++c)
-                    for (int kb = 0; kb < kbp; ++kb, ++it) {
+                    for (int kb = 0; kb < kbp; kb += kKPS, ++it) {
                         if (it < npre) continue;
                         const int st = it % STAGES;
                         const uint32_t ph = (it / STAGES) & 1;
-                        ptx::mbar_wait(&empty[st], ph ^ 1, a.err, ERR_TIMEOUT_PIPE);
+                        ptx::mbar_wait(&empty[st], ph ^ 1, a.err, 103, 8000000000ull);  // longest: the producer waits behind everything
+                        if (ts2 && it >= STAGES) {  // diagnostics: MMA issue -> stage freed
+                            hold_ns += ptx::globaltimer() - s_iss[st];
+                            ++hold_n;
+                        }
                         if (ts && p == 1 && c == 0 && kb == 0) ts[12] = ptx::globaltimer();  // job 1's first A tile
+                        s_prog[0] = it;
                         ptx::mbar_arrive_expect_tx(&full[st], S::kA);
-                        ptx::tma_load_2d(smem + S::kOffA + st * S::kA, tm, &full[st],
-                                         (pc.kb0 + kb) * kBK, e * rows + mt * kBM, pol_a);
+#pragma unroll
+                        for (int j = 0; j < kKPS; ++j)
+                            ptx::tma_load_2d(smem + S::kOffA + st * S::kA + j * S::kA1, tm, &full[st],
+                                             (pc.kb0 + kb + j) * kBK, e * rows + mt * kBM, pol_a);
                     }
             }
-            if (ts2) ts2[14] = ptx::globaltimer();
+            if (ts2) {
+                ts2[14] = ptx::globaltimer();
+                ts2[4] = hold_n ? hold_ns / hold_n : 0;
+            }
         }
     } else if (warp == 1) {
         // ================= MMA issuer =================
         int it = 0, job = 0;
+        uint64_t wA = 0, wB = 0;
         for (int p = 0; p < npc; ++p) {
             const Piece pc = s_pc[p];
             const int g = pc.g, e = pc.e, kbp = pc.nkb;
@@ -626,38 +650,58 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 const int ncol = max(16, (nc + 15) & ~15);
                 const uint32_t idesc = ptx::umma_idesc_bf16(kBM, ncol);
                 const int buf = job % NBUF;
-                if (job >= NBUF) ptx::mbar_wait(&tmem_empty[buf], ((job / NBUF) - 1) & 1, a.err, ERR_TIMEOUT_PIPE);
+                s_prog[2] = job;
+                if (job >= NBUF) ptx::mbar_wait(&tmem_empty[buf], ((job / NBUF) - 1) & 1, a.err, 104);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem + buf * NMAX;
-                for (int kb = 0; kb < kbp; ++kb, ++it) {
+                for (int kb = 0; kb < kbp; kb += kKPS, ++it) {
                     const int st = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
                     const int sb = it % BST;
-                    ptx::mbar_wait(&fullB[sb], (it / BST) & 1, a.err, ERR_TIMEOUT_PIPE);
+                    s_prog[1] = it;
+                    const uint64_t w0t = ts2 ? ptx::globaltimer() : 0;
+                    ptx::mbar_wait(&fullB[sb], (it / BST) & 1, a.err, 105);
+                    const uint64_t w1t = ts2 ? ptx::globaltimer() : 0;
                     if (ts2 && lane == 0 && job == 1 && kb == 0) ts2[8] = ptx::globaltimer();
                     if (ts3 && lane == 0 && it == 0) ts3[9] = ptx::globaltimer();
-                    ptx::mbar_wait(&full[st], ph, a.err, ERR_TIMEOUT_PIPE);
+                    ptx::mbar_wait(&full[st], ph, a.err, 106);
+                    if (ts2 && it > 0) {  // diagnostics: MMA warp blocked on rows / weights
+                        wB += w1t - w0t;
+                        wA += ptx::globaltimer() - w1t;
+                    }
                     if (ts2 && lane == 0 && job == 1 && kb == 0) ts2[9] = ptx::globaltimer();
                     if (ts3 && lane == 0 && it == 0) ts3[10] = ptx::globaltimer();
                     ptx::tc_fence_after();
                     ptx::fence_proxy_async_smem();  // cp.async (generic) rows -> tensor-core reads
                     if (lane == 0) {
-                        const uint64_t da = ptx::umma_desc_sw128(ptx::smem_u32(smem + S::kOffA + st * S::kA));
-                        const uint64_t db = ptx::umma_desc_sw128(ptx::smem_u32(smem + S::kOffB + sb * S::kB));
 #pragma unroll
-                        for (int kk = 0; kk < kBK / 16; ++kk)
-                            ptx::umma_bf16(d_tmem, da + 2 * kk, db + 2 * kk, idesc, (kb | kk) ? 1u : 0u);
+                        for (int j = 0; j < kKPS; ++j) {
+                            const uint64_t da =
+                                ptx::umma_desc_sw128(ptx::smem_u32(smem + S::kOffA + st * S::kA + j * S::kA1));
+                            const uint64_t db =
+                                ptx::umma_desc_sw128(ptx::smem_u32(smem + S::kOffB + sb * S::kB + j * S::kB1));
+#pragma unroll
+                            for (int kk = 0; kk < kBK / 16; ++kk)
+                                if (a.dbg != 2)  // diagnostics: EXF_DBG=2 streams without MMAs
+                                    ptx::umma_bf16(d_tmem, da + 2 * kk, db + 2 * kk, idesc, (kb | j | kk) ? 1u : 0u);
+                        }
                         ptx::umma_commit(&empty[st]);
                         ptx::umma_commit(&emptyB[sb]);
-                        if (kb == kbp - 1) ptx::umma_commit(&tmem_full[buf]);
+                        if (kb + kKPS >= kbp) ptx::umma_commit(&tmem_full[buf]);
+                        if (ts2) s_iss[st] = ptx::globaltimer();
                         if (ts && kb == 0 && job < 6) ts[2 + 2 * job] = ptx::globaltimer();
-                        if (ts && kb == kbp - 1 && job < 6) ts[3 + 2 * job] = ptx::globaltimer();
+                        if (ts && kb + kKPS >= kbp && job < 6) ts[3 + 2 * job] = ptx::globaltimer();
                     }
                     __syncwarp();
                 }
             }
         }
-        if (ts2 && lane == 0) ts2[15] = ptx::globaltimer();
+        if (ts2 && lane == 0) {
+            ts2[15] = ptx::globaltimer();
+            ts2[5] = wB;
+            ts2[6] = wA;
+            ts2[7] = (uint64_t)it;
+        }
     } else if (warp == 2) {
         // ====== B producer: the expert's token rows via cp.async (LSU path) ======
         // Token tiles are tiny (NMAX rows x 128 B per k-block); as TMA gathers
@@ -679,7 +723,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 // all GEMM1 (tile, chunk) units of expert e must be complete
                 const int target = mt1 * ((cnt(0, e) + NMAX - 1) / NMAX);
                 ptx::SpinGuard sg;
-                while (ld_acq_s32(a.hdone + parity * a.E_loc + e) < target) sg.step(a.err, ERR_TIMEOUT_PIPE);
+                while (ld_acq_s32(a.hdone + parity * a.E_loc + e) < target) sg.step(a.err, 107);
                 waited_e = e;
             }
             // GEMM1 rows: dispatched tokens (recv region) or, dense, the resident
@@ -699,17 +743,22 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     const int64_t row = g == 0 ? (a.dense ? (int64_t)i : recv_row(e, i)) : (int64_t)(off_e + i);
                     rows[j] = (int32_t)(row < 0 ? 0 : (row >= row_lim ? row_lim - 1 : row));
                 }
-                for (int kb = 0; kb < kbp; ++kb, ++it) {
+                for (int kb = 0; kb < kbp; kb += kKPS, ++it) {
                     const int sb = it % BST;
-                    ptx::mbar_wait(&emptyB[sb], ((it / BST) & 1) ^ 1, a.err, ERR_TIMEOUT_PIPE);
+                    s_prog[3] = it;
+                    s_prog[4] = p;
+                    ptx::mbar_wait(&emptyB[sb], ((it / BST) & 1) ^ 1, a.err, 108);
                     if (ts && lane == 0 && p == 1 && c == 0 && kb == 0) ts[13] = ptx::globaltimer();  // job 1's first B rows
-                    uint8_t* sbase = smem + S::kOffB + sb * S::kB;
-                    const __nv_bfloat16* kcol = src + (int64_t)(pc.kb0 + kb) * kBK + cc * 8;
 #pragma unroll
-                    for (int j = 0; j < NMAX / 4; ++j) {
-                        const int r = (lane >> 3) + 4 * j;
-                        if (4 * j < ncol)
-                            ptx::cp_async16(sbase + r * 128 + ((cc ^ (r & 7)) << 4), kcol + (int64_t)rows[j] * ld);
+                    for (int h = 0; h < kKPS; ++h) {
+                        uint8_t* sbase = smem + S::kOffB + sb * S::kB + h * S::kB1;
+                        const __nv_bfloat16* kcol = src + (int64_t)(pc.kb0 + kb + h) * kBK + cc * 8;
+#pragma unroll
+                        for (int j = 0; j < NMAX / 4; ++j) {
+                            const int r = (lane >> 3) + 4 * j;
+                            if (4 * j < ncol)
+                                ptx::cp_async16(sbase + r * 128 + ((cc ^ (r & 7)) << 4), kcol + (int64_t)rows[j] * ld);
+                        }
                     }
                     ptx::cp_async_arrive_noinc(&fullB[sb]);
                 }
@@ -796,7 +845,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 for (int u = lane; u < n; u += 32) {
                     ptx::SpinGuard sg;
                     uint64_t v;
-                    while (((v = ptx::ld_acquire_gpu_u64(rf + u)) >> 40) != e24) sg.step(a.err, ERR_TIMEOUT_DISPATCH);
+                    while (((v = ptx::ld_acquire_gpu_u64(rf + u)) >> 40) != e24) sg.step(a.err, 109);
                     s_exp[u] = (int)((v >> 32) & 0xFF);  // slot
                     s_prob[u] = __uint_as_float((uint32_t)v);
                 }
@@ -860,8 +909,12 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 const int cb = c * NMAX;
                 const int nc = max(0, min(NMAX, n_e - cb));
                 const int buf = job % NBUF;
+                if (et == 0) {
+                    s_prog[5] = job;
+                    s_prog[6] = p;
+                }
                 if (ts2 && et == 0 && job == 1) ts2[11] = ptx::globaltimer();
-                ptx::mbar_wait(&tmem_full[buf], (job / NBUF) & 1, a.err, ERR_TIMEOUT_PIPE);
+                ptx::mbar_wait(&tmem_full[buf], (job / NBUF) & 1, a.err, 110);
                 if (ts2 && et == 0 && job == 0) ts2[10] = ptx::globaltimer();
                 ptx::tc_fence_after();
                 const uint32_t t_base = tmem + buf * NMAX + ((uint32_t)lane_base << 16);
@@ -937,7 +990,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     if (a.dense) {
                         // dense GEMM1 covered every resident token: keep the
                         // rows routed to this expert, at their canonical rows
-                        ptx::mbar_wait(route_bar, 0, a.err, ERR_TIMEOUT_DISPATCH);
+                        ptx::mbar_wait(route_bar, 0, a.err, 111);
                         if (ts3 && et == 0 && job == 0) ts3[14] = ptx::globaltimer();
                     }
                     const long long c_in = clock64();
@@ -994,7 +1047,6 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                             if (row[i] >= 0) a.H[(int64_t)row[i] * a.dff + m_glob] = hv[i];
                     }
                     if (ts2 && et == 0 && job < 4) ts2[job] = (uint64_t)(clock64() - c_in);  // diagnostics
-                    if (ts2 && (et & 31) == 0 && job == 0) ts2[4 + (et >> 5)] = (uint64_t)(clock64() - c_in);
                     if (!from_ws) release_tmem();
                     if (ts3 && et == 0 && job == 0) ts3[4] = ptx::globaltimer();
                     asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -1119,8 +1171,9 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
     // measured at configs[1]: (16, 16) 45.9 us/layer; (16, 8) 53.2, (16, 12) 49.8,
     // (16, 32) 50.9, (8, 8) 65.2: per-piece costs exceed the model's estimate
     int psz[2] = {16, 16};
-    if (const char* s = std::getenv("EXF_PIECE1")) psz[0] = std::max(1, std::atoi(s));
-    if (const char* s = std::getenv("EXF_PIECE2")) psz[1] = std::max(1, std::atoi(s));
+    if (const char* s = std::getenv("EXF_PIECE1")) psz[0] = std::atoi(s);
+    if (const char* s = std::getenv("EXF_PIECE2")) psz[1] = std::atoi(s);
+    for (int g = 0; g < 2; ++g) psz[g] = std::max(kKPS, psz[g] / kKPS * kKPS);  // whole stages
     const int kk[2] = {k1, k2}, mts[2] = {mt1, mt2};
     constexpr double kSwitch = 1.0;   // per-piece pipeline cost, in k-blocks
     constexpr double kReady = 6.0;    // GEMM1 epilogue + hdone + token-row load latency
@@ -1162,16 +1215,17 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
         // their GEMM1 tiles receive contiguous runs of GEMM2's expert-major
         // (tile, k-block) sequence, sized so that every CTA ends together;
         // early-free CTAs get the early experts, whose GEMM1 ended first.
-        const int64_t U2 = (int64_t)E_loc * mt2 * k2;
+        const int k2s = k2 / kKPS;  // units: pipeline stages of kKPS k-blocks
+        const int64_t U2 = (int64_t)E_loc * mt2 * k2s;
         std::vector<int> order(ctas);
         for (int c = 0; c < ctas; ++c) order[c] = c;
         std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return free_at[x] < free_at[y]; });
-        // finish time T: sum_c max(0, T - free_c - switch) = U2
+        // finish time T: sum_c max(0, T - free_c - switch) = U2 (times in k-blocks)
         double lo = 0, hi = 1e9;
         for (int it = 0; it < 200; ++it) {
             const double T = 0.5 * (lo + hi);
             double s = 0;
-            for (int c = 0; c < ctas; ++c) s += std::max(0.0, T - free_at[c] - 2 * kSwitch);
+            for (int c = 0; c < ctas; ++c) s += std::max(0.0, T - free_at[c] - 2 * kSwitch) / kKPS;
             (s >= (double)U2 ? hi : lo) = T;
         }
         std::vector<int64_t> share(ctas, 0);
@@ -1179,7 +1233,7 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
         double acc = 0;
         for (int i = 0; i < ctas; ++i) {  // integer shares by cumulative rounding
             const int c = order[i];
-            acc += std::max(0.0, hi - free_at[c] - 2 * kSwitch);
+            acc += std::max(0.0, hi - free_at[c] - 2 * kSwitch) / kKPS;
             const int64_t upto = std::min<int64_t>(U2, (int64_t)std::llround(acc));
             share[c] = std::max<int64_t>(0, upto - given);
             given += share[c];
@@ -1191,15 +1245,15 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
             const int c = order[i];
             const int64_t end = u + share[c];
             while (u < end) {
-                const int64_t tile = u / k2;
-                const int kb0 = (int)(u - tile * k2);
-                const int n = (int)(std::min<int64_t>(end, (tile + 1) * k2) - u);
+                const int64_t tile = u / k2s;
+                const int s0 = (int)(u - tile * k2s);
+                const int n = (int)(std::min<int64_t>(end, (tile + 1) * k2s) - u);
                 Piece p{};
                 p.g = 1;
                 p.e = (int16_t)(tile / mt2);
                 p.mt = (int16_t)(tile % mt2);
-                p.kb0 = (int16_t)kb0;
-                p.nkb = (int16_t)n;
+                p.kb0 = (int16_t)(s0 * kKPS);
+                p.nkb = (int16_t)(n * kKPS);
                 p.kidx = cnt[tile]++;
                 per[c].push_back(p);
                 u += n;
@@ -1225,14 +1279,39 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
     return *max_pieces <= kMaxPieces;
 }
 
+namespace {
+int* g_dbg_host_words = nullptr;  // host view of this unit's g_dbg_host
+}
+
 exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int nmax, cudaStream_t s) {
+    if (!g_dbg_host_words) {  // diagnostics channel for timed-out spins (survives a trap)
+        void* h = nullptr;
+        void* dptr = nullptr;
+        if (cudaHostAlloc(&h, 64, cudaHostAllocMapped) == cudaSuccess &&
+            cudaHostGetDevicePointer(&dptr, h, 0) == cudaSuccess) {
+            std::memset(h, 0, 64);
+            volatile int* dv = static_cast<volatile int*>(dptr);
+            if (cudaMemcpyToSymbol(ptx::g_dbg_host, &dv, sizeof(dv)) == cudaSuccess)
+                g_dbg_host_words = static_cast<int*>(h);
+        }
+        cudaGetLastError();
+    }
     if (a.E > kMaxKeys || a.E_loc > kMaxLocal) return invalid("at most 64 experts");
     if (a.d > 2048) return invalid("fused layer kernel supports d_model <= 2048");
     if (a.tpc > 32) return invalid("token slice too large for the fused layer kernel");
     // (token tile, weight stages, token stages): ~208 KB of rings each
-    if (nmax <= 32) return launch_nmax<32, 10, 12>(maps, a, s);
-    if (nmax <= 64) return launch_nmax<64, 10, 6>(maps, a, s);
-    return launch_nmax<128, 6, 7>(maps, a, s);
+    if ((a.d / kBK) % kKPS || (a.dff / kBK) % kKPS) return invalid("d_model and d_ffn must be multiples of 128");
+    // (token tile, weight stages, token stages) with kKPS k-blocks per stage
+    if (nmax <= 32) return launch_nmax<32, 5, 6>(maps, a, s);
+    if (nmax <= 64) return launch_nmax<64, 5, 3>(maps, a, s);
+    return launch_nmax<128, 3, 3>(maps, a, s);
 }
 
 }  // namespace exf
+
+extern "C" int32_t exf_debug_last_timeout(int32_t* out12) {
+    if (!out12) return 0;
+    const int* w = exf::g_dbg_host_words;
+    for (int i = 0; i < 12; ++i) out12[i] = w ? ((volatile const int*)w)[i] : 0;
+    return w ? 1 : 0;
+}

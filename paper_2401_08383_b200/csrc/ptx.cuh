@@ -25,6 +25,15 @@ __device__ __forceinline__ uint64_t globaltimer() {
 
 // Bounded spin: after `ns` nanoseconds record `code` in *err and trap, so a
 // lost peer or a protocol bug becomes a kernel fault instead of a GPU hang.
+// Diagnostics: host-mapped pinned words {flag, code, block, thread} written by
+// a timed-out spin before it traps, readable on the host after the context is
+// lost (exf_debug_last_timeout). One pointer per translation unit; set by that
+// unit's host code (the fused-kernel launcher sets its own).
+static __device__ volatile int* g_dbg_host = nullptr;
+// optional per-CTA progress words (generic smem address, same in every CTA)
+// copied into g_dbg_host[4..11] on a timeout
+static __device__ volatile int* g_dbg_prog = nullptr;
+
 struct SpinGuard {
     uint64_t start = 0;
     uint32_t iters = 0;
@@ -35,6 +44,15 @@ struct SpinGuard {
                 start = now;
             } else if (now - start > ns) {
                 if (err) atomicExch(err, code);
+                if (g_dbg_host) {
+                    g_dbg_host[1] = code;
+                    g_dbg_host[2] = (int)blockIdx.x;
+                    g_dbg_host[3] = (int)threadIdx.x;
+                    if (g_dbg_prog)
+                        for (int i = 0; i < 8; ++i) g_dbg_host[4 + i] = g_dbg_prog[i];
+                    __threadfence_system();
+                    g_dbg_host[0] = 1;
+                }
                 __threadfence_system();
                 __trap();
             }
@@ -79,9 +97,10 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t pa
         : "memory");
     return ok != 0;
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int* err, int code) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int* err, int code,
+                                          uint64_t timeout_ns = 4000000000ull) {
     SpinGuard g;
-    while (!mbar_try_wait(bar, parity)) g.step(err, code);
+    while (!mbar_try_wait(bar, parity)) g.step(err, code, timeout_ns);
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity, int* err,
                                                   int code) {

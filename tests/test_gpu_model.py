@@ -165,16 +165,33 @@ def test_tiny_config_single_device(torch_cuda, orc):
     run_checked(torch_cuda, models, xs, assign)
 
 
-@pytest.mark.parametrize("E,L,d,dff,B", [(8, 4, 512, 2048, 256), (8, 4, 1024, 4096, 64),
-                                         (16, 3, 256, 512, 8), (64, 3, 1024, 1024, 96),
-                                         (32, 2, 2048, 2048, 48)])
+FUSED_CONFIGS = [(8, 4, 512, 2048, 256), (8, 4, 1024, 4096, 64), (16, 3, 256, 512, 8),
+                 (64, 3, 1024, 1024, 96), (32, 2, 2048, 2048, 48),
+                 # > 4 jobs per CTA: TMEM accumulator buffers wrap around
+                 (8, 2, 1024, 8192, 64), (16, 2, 1024, 4096, 64)]
+
+
+@pytest.mark.parametrize("E,L,d,dff,B", FUSED_CONFIGS)
 def test_fused_layer_kernel_single_device(torch_cuda, orc, E, L, d, dff, B):
-    # the one-launch-per-layer kernel: gate, bucketing, dispatch, split-K
-    # GEMM1 -> GEMM2 with in-kernel dependencies; same oracle checks per layer
+    # the one-launch-per-layer kernel (dense single-GPU mode where C <= #SMs):
+    # gate, routing, GEMM1 -> GEMM2 with in-kernel dependencies; oracle per layer
     assign = orc.contiguous_placement(E, L, 1)
     models = _models(1, assign, num_experts=E, num_layers=L, d_model=d, d_ffn=dff,
                      tokens_per_gpu=B, seed=42 + E, gate_affinity=0.5)
     xs = _inputs(torch_cuda, models, 1)
+    run_checked(torch_cuda, models, xs, assign, ffn_samples=24, fused=True)
+
+
+@pytest.mark.parametrize("E,L,d,dff,B", FUSED_CONFIGS[:2] + FUSED_CONFIGS[5:])
+def test_fused_layer_kernel_dispatch_path(torch_cuda, orc, monkeypatch, E, L, d, dff, B):
+    # the same kernel with the single-GPU dense mode off: gate, bucketing,
+    # dispatch exchange, split-K pieces over the dispatched rows
+    monkeypatch.setenv("EXF_DENSE", "0")
+    assign = orc.contiguous_placement(E, L, 1)
+    models = _models(1, assign, num_experts=E, num_layers=L, d_model=d, d_ffn=dff,
+                     tokens_per_gpu=B, seed=7 + E, gate_affinity=0.5)
+    assert models[0].describe()["layer_kernel"]["dense"] is False
+    xs = _inputs(torch_cuda, models, 2)
     run_checked(torch_cuda, models, xs, assign, ffn_samples=24, fused=True)
 
 

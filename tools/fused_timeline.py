@@ -49,8 +49,11 @@ def main():
     r2 = (t2 - t0) / 1000.0
     j0 = rel[:, 2]
     print("GEMM1 epilogue store-loop cycles per job (median over CTAs, job 0..3):",
-          [int(np.median(t2[:, k])) for k in range(4)], "; job 0 by epilogue warp 4..7:",
-          [int(np.median(t2[:, 4 + k])) for k in range(4)])
+          [int(np.median(t2[:, k])) for k in range(4)])
+    its = np.maximum(t2[:, 7], 1)
+    print(f"weight stage hold (MMA issue -> stage freed): median {np.median(t2[:, 4]):.0f} ns; "
+          f"MMA warp blocked per stage on token rows {np.median(t2[:, 5] / its):.0f} ns, "
+          f"on weights {np.median(t2[:, 6] / its):.0f} ns (stages/CTA {int(np.median(t2[:, 7]))})")
     print(f"job 1 MMA: fullB ready {(r2[:, 8] - rel[:, 3]).mean():.2f}, A ready {(r2[:, 9] - rel[:, 3]).mean():.2f} "
           f"after job 0 last MMA")
     print(f"job 0 epilogue: tmem_full at {(r2[:, 10] - rel[:, 3]).mean():.2f} after last MMA, "
