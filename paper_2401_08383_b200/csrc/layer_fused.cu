@@ -197,6 +197,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // per model: safe to read before the PDL wait)
     __shared__ Piece s_pc[kMaxPieces];
     __shared__ uint64_t s_iss[STAGES];  // diagnostics: MMA issue time per weight stage
+    __shared__ int32_t s_brow[NMAX];  // token-row producer: source row per token column
     __shared__ int s_prog[8];  // diagnostics: A it, MMA it, MMA job, B it, B piece, epi job, epi piece, token
     if (tid < 8) s_prog[tid] = 0;
     if (tid == 0 && blockIdx.x == 0) ptx::g_dbg_prog = s_prog;
@@ -214,6 +215,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // [2] gate done, [3] ranks done, [4] barrier passed, [5] dispatch stored,
     // [6] completion done, [7] flags seen / tables built, [15] exit
     uint64_t* ts3 = ts ? ts + (int64_t)(2 + (a.layer & 1)) * 4096 * 16 : nullptr;
+    uint64_t* ts4 = ts ? ts + (int64_t)4 * 4096 * 16 : nullptr;  // [2p], [2p+1]: B piece p setup start / rows ready
     auto mark3 = [&](int k) {
         if (ts3 && threadIdx.x == 0) ts3[k] = ptx::globaltimer();
     };
@@ -243,6 +245,15 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     ptx::tc_fence_after();
     const uint32_t tmem = misc[0];
     const int npre = npc > 0 ? min((int)s_pc[0].nkb / kKPS, STAGES) : 0;  // prefetched stages
+    // k-block offset of pipeline step kb within a piece of nkb k-blocks: each
+    // CTA starts at its own stage and wraps around, so the CTAs' concurrent
+    // token-row loads spread over the activation matrix (in dense mode every
+    // CTA's first GEMM1 piece reads the same rows: the first stage took ~4 us
+    // from 148-way same-line L2 traffic); the order is fixed per CTA
+    auto kbr = [&](int nkb, int kb) {
+        const int nst = nkb / kKPS;
+        return ((kb / kKPS + (int)blockIdx.x) % nst) * kKPS;
+    };
     const uint64_t pol_a = ptx::policy_evict_first();
     // the layer's gate matrix is a weight too: bulk-copy it into the B-stage
     // region (unused until the expert phase) when it fits, before the wait
@@ -264,7 +275,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             ptx::mbar_arrive_expect_tx(&full[s], S::kA);
             for (int j = 0; j < kKPS; ++j)
                 ptx::tma_load_2d(smem + S::kOffA + s * S::kA + j * S::kA1, tm, &full[s],
-                                 (pc.kb0 + s * kKPS + j) * kBK, pc.e * rows + pc.mt * kBM, pol_a);
+                                 (pc.kb0 + kbr(pc.nkb, s * kKPS) + j) * kBK, pc.e * rows + pc.mt * kBM, pol_a);
         }
     };
     if (warp == 0 && lane == 0) {
@@ -628,7 +639,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
 #pragma unroll
                         for (int j = 0; j < kKPS; ++j)
                             ptx::tma_load_2d(smem + S::kOffA + st * S::kA + j * S::kA1, tm, &full[st],
-                                             (pc.kb0 + kb + j) * kBK, e * rows + mt * kBM, pol_a);
+                                             (pc.kb0 + kbr(kbp, kb) + j) * kBK, e * rows + mt * kBM, pol_a);
                     }
             }
             if (ts2) {
@@ -640,6 +651,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         // ================= MMA issuer =================
         int it = 0, job = 0;
         uint64_t wA = 0, wB = 0;
+        if (ts2 && lane == 0) ts2[3] = ptx::globaltimer();  // diagnostics: MMA role entry
         for (int p = 0; p < npc; ++p) {
             const Piece pc = s_pc[p];
             const int g = pc.g, e = pc.e, kbp = pc.nkb;
@@ -669,7 +681,6 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         wB += w1t - w0t;
                         wA += ptx::globaltimer() - w1t;
                     }
-                    if (ts2 && lane == 0 && job == 1 && kb == 0) ts2[9] = ptx::globaltimer();
                     if (ts3 && lane == 0 && it == 0) ts3[10] = ptx::globaltimer();
                     ptx::tc_fence_after();
                     ptx::fence_proxy_async_smem();  // cp.async (generic) rows -> tensor-core reads
@@ -714,6 +725,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         int it = 0;
         int waited_e = -1;
         for (int p = 0; p < npc; ++p) {
+            if (ts4 && lane == 0 && p < 8) ts4[2 * p] = ptx::globaltimer();
             const Piece pc = s_pc[p];
             const int g = pc.g, e = pc.e, kbp = pc.nkb;
             const int n_e = cnt(g, e);
@@ -735,14 +747,31 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 const int cb = c * NMAX;
                 const int nc = max(0, min(NMAX, n_e - cb));
                 const int ncol = max(16, (nc + 15) & ~15);
-                int32_t rows[NMAX / 4];
+                // source row of every token column, once per chunk, into a
+                // small shared table (a rolled loop: the unrolled per-lane
+                // version with recv_row inlined NMAX/4 times cost ~1.5 us per
+                // piece, stalling the MMA at every job boundary)
+                int32_t rows[NMAX / 4];  // this lane's rows, in registers for the copy loop
+                if (g == 0 && !a.dense) {  // dispatched rows: per-source segments
+                    __syncwarp();  // previous chunk's copies have read the table
+#pragma unroll 1
+                    for (int r = lane; r < NMAX; r += 32) {
+                        const int64_t row = recv_row(e, cb + (r < nc ? r : 0));
+                        s_brow[r] = (int32_t)(row < 0 ? 0 : (row >= row_lim ? row_lim - 1 : row));
+                    }
+                    __syncwarp();
 #pragma unroll
-                for (int j = 0; j < NMAX / 4; ++j) {
-                    const int r = (lane >> 3) + 4 * j;
-                    const int i = cb + (r < nc ? r : 0);
-                    const int64_t row = g == 0 ? (a.dense ? (int64_t)i : recv_row(e, i)) : (int64_t)(off_e + i);
-                    rows[j] = (int32_t)(row < 0 ? 0 : (row >= row_lim ? row_lim - 1 : row));
+                    for (int j = 0; j < NMAX / 4; ++j) rows[j] = s_brow[(lane >> 3) + 4 * j];
+                } else {  // resident rows (dense GEMM1) or H rows (GEMM2): arithmetic
+                    const int base = g == 0 ? 0 : off_e;
+#pragma unroll
+                    for (int j = 0; j < NMAX / 4; ++j) {
+                        const int r = (lane >> 3) + 4 * j;
+                        rows[j] = min(base + cb + (r < nc ? r : 0), row_lim - 1);
+                    }
                 }
+                if (ts2 && it == 0 && lane == 0) ts2[9] = ptx::globaltimer();  // diagnostics: rows ready
+                if (ts4 && lane == 0 && p < 8 && c == 0) ts4[2 * p + 1] = ptx::globaltimer();
                 for (int kb = 0; kb < kbp; kb += kKPS, ++it) {
                     const int sb = it % BST;
                     s_prog[3] = it;
@@ -752,7 +781,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
 #pragma unroll
                     for (int h = 0; h < kKPS; ++h) {
                         uint8_t* sbase = smem + S::kOffB + sb * S::kB + h * S::kB1;
-                        const __nv_bfloat16* kcol = src + (int64_t)(pc.kb0 + kb + h) * kBK + cc * 8;
+                        const __nv_bfloat16* kcol = src + (int64_t)(pc.kb0 + kbr(kbp, kb) + h) * kBK + cc * 8;
 #pragma unroll
                         for (int j = 0; j < NMAX / 4; ++j) {
                             const int r = (lane >> 3) + 4 * j;
@@ -761,6 +790,11 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         }
                     }
                     ptx::cp_async_arrive_noinc(&fullB[sb]);
+                    if (ts2 && it == 0 && lane == 0) {  // diagnostics: first stage issue -> landed
+                        ts2[1] = ptx::globaltimer();
+                        asm volatile("cp.async.wait_all;" ::: "memory");
+                        ts2[2] = ptx::globaltimer();
+                    }
                 }
             }
         }
@@ -1046,7 +1080,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         for (int i = 0; i < kG; ++i)
                             if (row[i] >= 0) a.H[(int64_t)row[i] * a.dff + m_glob] = hv[i];
                     }
-                    if (ts2 && et == 0 && job < 4) ts2[job] = (uint64_t)(clock64() - c_in);  // diagnostics
+                    if (ts2 && et == 0 && job == 0) ts2[job] = (uint64_t)(clock64() - c_in);  // diagnostics
                     if (!from_ws) release_tmem();
                     if (ts3 && et == 0 && job == 0) ts3[4] = ptx::globaltimer();
                     asm volatile("bar.sync 1, 128;" ::: "memory");

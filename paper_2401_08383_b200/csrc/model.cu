@@ -541,7 +541,7 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         EXF_M(dalloc(&m->f_cta_cnt, (size_t)m->f_ctas * E));
     }
     if (std::getenv("EXF_FFN_TIMELINE")) {
-        EXF_M(dalloc(&m->tstamp, (size_t)4 * kTimelineCtas * 16));
+        EXF_M(dalloc(&m->tstamp, (size_t)5 * kTimelineCtas * 16));
         EXF_M(dalloc(&m->tl, (size_t)L * 3 * 8));
     }
     EXF_M(dalloc(&m->d_peers, (size_t)c.world_size));
@@ -809,7 +809,7 @@ exf_status exf_model_read_ffn_timeline(exf_model* m, uint64_t* h, int32_t ctas) 
     if (!m || !h || ctas < 1 || ctas > kTimelineCtas) return invalid("bad argument");
     if (!m->tstamp) return invalid("timeline not enabled (set EXF_FFN_TIMELINE=1 before create)");
     EXF_CUDA_TRY(cudaDeviceSynchronize());
-    for (int g = 0; g < 4; ++g)
+    for (int g = 0; g < 5; ++g)
         EXF_CUDA_TRY(cudaMemcpy(h + (int64_t)g * ctas * 16, m->tstamp + (int64_t)g * kTimelineCtas * 16,
                                 sizeof(uint64_t) * ctas * 16, cudaMemcpyDeviceToHost));
     return EXF_OK;

@@ -26,7 +26,7 @@ def main():
     s.synchronize()
     m.check()
     ctas = 148
-    buf = np.zeros((4, ctas, 16), np.uint64)
+    buf = np.zeros((5, ctas, 16), np.uint64)
     _capi.call("exf_model_read_ffn_timeline", m.handle, buf.ctypes.data, ctas)
     t = buf[0].astype(np.int64)
     t0 = t[:, 0].min()
@@ -48,8 +48,17 @@ def main():
     t2 = buf[1].astype(np.int64)
     r2 = (t2 - t0) / 1000.0
     j0 = rel[:, 2]
-    print("GEMM1 epilogue store-loop cycles per job (median over CTAs, job 0..3):",
-          [int(np.median(t2[:, k])) for k in range(4)])
+    print("GEMM1 epilogue store-loop cycles, job 0 (median over CTAs):", int(np.median(t2[:, 0])),
+          "; first token-row stage: issue -> landed %.2f us (issued %.2f us after layer entry stamp)" % (
+              np.median((t2[:, 2] - t2[:, 1]) / 1e3), np.median((t2[:, 1] - t[:, 0]) / 1e3)))
+    b_start = buf[3][:, 8].astype(np.int64)
+    mma_full_b = buf[3][:, 9].astype(np.int64)
+    print("  rel. token-row producer start: rows ready %.2f, first stage issued %.2f, landed %.2f, MMA role entry "
+          "%.2f, MMA saw it %.2f us" % tuple(np.median((v - b_start) / 1e3)
+                                            for v in (t2[:, 9], t2[:, 1], t2[:, 2], t2[:, 3], mma_full_b)))
+    t4 = buf[4].astype(np.int64)
+    print("  token-row producer per-piece setup (start -> rows ready), median us, pieces 0..3:",
+          [round(float(np.median((t4[:, 2 * p + 1] - t4[:, 2 * p]) / 1e3)), 2) for p in range(4)])
     its = np.maximum(t2[:, 7], 1)
     print(f"weight stage hold (MMA issue -> stage freed): median {np.median(t2[:, 4]):.0f} ns; "
           f"MMA warp blocked per stage on token rows {np.median(t2[:, 5] / its):.0f} ns, "
