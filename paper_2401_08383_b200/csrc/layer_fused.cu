@@ -153,7 +153,11 @@ struct Smem {
 
 }  // namespace
 
-template <int NMAX, int STAGES, int BST, int NBUF = (NMAX <= 64 ? 4 : 2)>
+// DENSE: single-GPU dense mode (else the dispatch path); DIAG: timeline
+// stamps compiled in. Specialised at compile time so each variant carries
+// only its own code: ncu showed the epilogue and per-piece setup stalled on
+// instruction fetch (stall_no_inst) in the ~170 KB all-paths kernel.
+template <int NMAX, int STAGES, int BST, bool DENSE, bool DIAG, int NBUF = (NMAX <= 64 ? 4 : 2)>
 __global__ void __launch_bounds__(kThreads, 1)
 layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
                    const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
@@ -205,7 +209,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     const int npc = a.piece_off[blockIdx.x + 1] - pc0;
     if (tid < npc) s_pc[tid] = a.pieces[pc0 + tid];
     if (tid == 0) tl_mark(a.tl, 0);
-    uint64_t* ts = a.tstamp ? a.tstamp + (int64_t)blockIdx.x * 16 : nullptr;
+    uint64_t* ts = (DIAG && a.tstamp) ? a.tstamp + (int64_t)blockIdx.x * 16 : nullptr;
     if (ts && tid == 0) ts[0] = ptx::globaltimer();
     // second stamp row (diagnostics): [0..7] B producer at it = 0,2,..,14,
     // [9]/[10] job-0 epilogue start/done, [11] job-1 epilogue start,
@@ -265,7 +269,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // previous kernel: safe to read before the PDL wait
     if (tid < a.E) s_key[tid] = a.gpu_of[tid] * a.E_loc + a.slot_of[tid];
     // (never in dense mode: there the token-row ring is live from the start)
-    const bool wg_smem = !a.dense && wg_bytes <= (uint32_t)(BST * S::kB) && gate_cta;
+    const bool wg_smem = !DENSE && wg_bytes <= (uint32_t)(BST * S::kB) && gate_cta;
     auto prefetch_a = [&]() {  // first weight stages of the CTA's first piece
         if (npc == 0) return;
         const Piece pc = s_pc[0];
@@ -300,7 +304,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // speculative loads of each warp's first token (row + meta), in flight
     // together with n: rows below C always exist, unused ones are dropped
     const int t_first = (int)blockIdx.x * a.tpc + warp;
-    const bool spec = !a.dense && gate_cta && warp < a.tpc && t_first < a.C;
+    const bool spec = !DENSE && gate_cta && warp < a.tpc && t_first < a.C;
     int4 xk[8];
     ResMeta mk{0, -1};
     if (spec) {
@@ -325,7 +329,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     uint64_t* bslots = reinterpret_cast<uint64_t*>(a.gbar);
     const uint64_t bepoch = bslots[256] + 1;
 
-    if (a.dense) {
+    if (DENSE) {
         // GEMM1 runs over all n resident tokens at once; the GEMM2 tables are
         // filled by the token warp (route_bar) while GEMM1 streams
         if (blockIdx.x == 0 && tid == 0) *a.n_res_out = n;
@@ -595,7 +599,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // tokens of (gemm, expert): dense GEMM1 runs over every resident token;
     // otherwise (and for dense GEMM2, once the routes are in) the tables
     auto cnt = [&](int g, int e) -> int {
-        if (a.dense) {
+        if (DENSE) {
             if (g == 0) return n;
             ptx::mbar_wait(route_bar, 0, a.err, 102);
         }
@@ -693,7 +697,6 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                                 ptx::umma_desc_sw128(ptx::smem_u32(smem + S::kOffB + sb * S::kB + j * S::kB1));
 #pragma unroll
                             for (int kk = 0; kk < kBK / 16; ++kk)
-                                if (a.dbg != 2)  // diagnostics: EXF_DBG=2 streams without MMAs
                                     ptx::umma_bf16(d_tmem, da + 2 * kk, db + 2 * kk, idesc, (kb | j | kk) ? 1u : 0u);
                         }
                         ptx::umma_commit(&empty[st]);
@@ -740,9 +743,9 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             }
             // GEMM1 rows: dispatched tokens (recv region) or, dense, the resident
             // tokens themselves; GEMM2 rows: H in canonical order
-            const __nv_bfloat16* src = g == 0 ? (a.dense ? a.res_x_in : rx) : a.H;
+            const __nv_bfloat16* src = g == 0 ? (DENSE ? a.res_x_in : rx) : a.H;
             const int ld = g == 0 ? a.d : a.dff;
-            const int row_lim = g == 0 ? (a.dense ? a.C : 2 * a.G * a.C) : a.C;
+            const int row_lim = g == 0 ? (DENSE ? a.C : 2 * a.G * a.C) : a.C;
             for (int c = 0; c < nch; ++c) {
                 const int cb = c * NMAX;
                 const int nc = max(0, min(NMAX, n_e - cb));
@@ -752,7 +755,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 // version with recv_row inlined NMAX/4 times cost ~1.5 us per
                 // piece, stalling the MMA at every job boundary)
                 int32_t rows[NMAX / 4];  // this lane's rows, in registers for the copy loop
-                if (g == 0 && !a.dense) {  // dispatched rows: per-source segments
+                if (g == 0 && !DENSE) {  // dispatched rows: per-source segments
                     __syncwarp();  // previous chunk's copies have read the table
 #pragma unroll 1
                     for (int r = lane; r < NMAX; r += 32) {
@@ -800,7 +803,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         }
         if (ts2 && lane == 0) ts2[13] = ptx::globaltimer();
     } else {
-        if (a.dense) {
+        if (DENSE) {
             // ====== dense mode (G == 1, token t is CTA t's): the token phase
             // runs concurrently with GEMM1's MMAs; its result is first needed
             // by GEMM1's epilogue (which rows of H to keep, and where).
@@ -1021,14 +1024,14 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     }
                 };
                 if (g == 0) {
-                    if (a.dense) {
+                    if (DENSE) {
                         // dense GEMM1 covered every resident token: keep the
                         // rows routed to this expert, at their canonical rows
                         ptx::mbar_wait(route_bar, 0, a.err, 111);
                         if (ts3 && et == 0 && job == 0) ts3[14] = ptx::globaltimer();
                     }
                     const long long c_in = clock64();
-                    if (a.dense) {
+                    if (DENSE) {
                         // only this expert's routed tokens (~1/E of the dense
                         // columns): canonical rows off1.., resident rows via s_tok,
                         // TMEM column = resident row - cb; 8 loads in flight
@@ -1061,7 +1064,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         }
                     }
 #pragma unroll 1
-                    for (int col = 0; col < (a.dense ? 0 : nc); col += kG) {
+                    for (int col = 0; col < (DENSE ? 0 : nc); col += kG) {
                         float v[kG];
                         final4(col, v);
                         // branch-free: independent GELUs and row lookups, then
@@ -1072,8 +1075,8 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         for (int i = 0; i < kG; ++i) {
                             hv[i] = __float2bfloat16(gelu_erf(v[i] + bias));
                             const int j = cb + col + i;
-                            const int slot_j = a.dense ? s_exp[j] : e;
-                            const int pos_j = a.dense ? s_pos[j] : off_e + j;
+                            const int slot_j = DENSE ? s_exp[j] : e;
+                            const int pos_j = DENSE ? s_pos[j] : off_e + j;
                             row[i] = (col + i < nc && slot_j == e) ? pos_j : -1;
                         }
 #pragma unroll
@@ -1091,7 +1094,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     // per token: source row of the residual, gate prob, output row
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     if (et < nc) {
-                        if (a.dense) {  // canonical row -> resident row (route tables)
+                        if (DENSE) {  // canonical row -> resident row (route tables)
                             const int u = s_tok[off_e + cb + et];
                             s_rrow[et] = u;
                             s_rprob[et] = s_prob[u];
@@ -1105,7 +1108,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         }
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
-                    const __nv_bfloat16* xres = a.dense ? a.res_x_in : rx;
+                    const __nv_bfloat16* xres = DENSE ? a.res_x_in : rx;
 #pragma unroll 1
                     for (int col = 0; col < nc; col += 2 * kG) {
                         __nv_bfloat16 xin[2 * kG];  // residual loads in flight first
@@ -1122,7 +1125,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                                     __bfloat162float(xin[i]) + s_rprob[col + i] * (v[i] + bias));
                     }
                     if (!from_ws) release_tmem();
-                    if (!a.dense && mt == 0 && et < nc)  // dense: the token's own CTA wrote it
+                    if (!DENSE && mt == 0 && et < nc)  // dense: the token's own CTA wrote it
                         a.res_meta_out[off_e + cb + et] = ResMeta{s_rtok[et], s_rexp[et]};
                 }
             }
@@ -1146,10 +1149,10 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
 // ------------------------------------------------------------------ host side
 namespace {
 
-template <int NMAX, int STAGES, int BST>
+template <int NMAX, int STAGES, int BST, bool DENSE, bool DIAG>
 struct FusedLauncher {
     using Sm = Smem<NMAX, STAGES, BST>;
-    static constexpr auto kern = layer_fused_kernel<NMAX, STAGES, BST>;
+    static constexpr auto kern = layer_fused_kernel<NMAX, STAGES, BST, DENSE, DIAG>;
     int ctas = 0;
     exf_status prepare() {
         if (ctas) return EXF_OK;
@@ -1174,8 +1177,12 @@ struct FusedLauncher {
 
 template <int NMAX, int STAGES, int BST>
 exf_status launch_nmax(const CUtensorMap* maps, const FusedArgs& a, cudaStream_t s) {
-    static FusedLauncher<NMAX, STAGES, BST> l;
-    return l.launch(maps, a, s);
+    static FusedLauncher<NMAX, STAGES, BST, true, false> dense;
+    static FusedLauncher<NMAX, STAGES, BST, false, false> dispatch;
+    static FusedLauncher<NMAX, STAGES, BST, true, true> dense_diag;
+    static FusedLauncher<NMAX, STAGES, BST, false, true> dispatch_diag;
+    if (a.tstamp) return a.dense ? dense_diag.launch(maps, a, s) : dispatch_diag.launch(maps, a, s);
+    return a.dense ? dense.launch(maps, a, s) : dispatch.launch(maps, a, s);
 }
 
 }  // namespace
@@ -1336,8 +1343,11 @@ exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int n
     // (token tile, weight stages, token stages): ~208 KB of rings each
     if ((a.d / kBK) % kKPS || (a.dff / kBK) % kKPS) return invalid("d_model and d_ffn must be multiples of 128");
     // (token tile, weight stages, token stages) with kKPS k-blocks per stage
-    if (nmax <= 32) return launch_nmax<32, 5, 6>(maps, a, s);
-    if (nmax <= 64) return launch_nmax<64, 5, 3>(maps, a, s);
+    // 128 KB of weights in flight streams as fast as 160 KB (profiles/
+    // r01_tma_stream_bench.txt); the deeper token-row ring hides per-piece
+    // setup and row-load latency at job boundaries
+    if (nmax <= 32) return launch_nmax<32, 4, 10>(maps, a, s);
+    if (nmax <= 64) return launch_nmax<64, 4, 5>(maps, a, s);
     return launch_nmax<128, 3, 3>(maps, a, s);
 }
 

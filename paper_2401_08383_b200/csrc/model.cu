@@ -383,7 +383,6 @@ FusedArgs fused_args(exf_model* m, int j) {
     a.b1 = m->b1 + (int64_t)j * m->E_loc * c.d_ffn;
     a.b2 = m->b2 + (int64_t)j * m->E_loc * c.d_model;
     a.dense = m->dense ? 1 : 0;
-    a.dbg = std::getenv("EXF_DBG") ? std::atoi(std::getenv("EXF_DBG")) : 0;
     a.res_x_out = m->res_x[(j + 1) & 1];
     a.res_meta_out = m->res_meta[(j + 1) & 1];
     a.n_res_out = m->n_res + ((j + 1) & 1);

@@ -149,7 +149,6 @@ struct FusedArgs {
     // it and publishes {epoch, slot, prob} in one 64-bit route flag; GEMM1's
     // epilogue keeps routed rows only, GEMM2 runs on the compact H
     int32_t dense;
-    int32_t dbg;  // diagnostics knob (EXF_DBG), 0 in production
     unsigned long long* tl;
     uint64_t* tstamp;    // optional per-CTA stamps [grid][16] (diagnostics)
 };
