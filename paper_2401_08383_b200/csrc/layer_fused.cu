@@ -1031,7 +1031,8 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         if (ts3 && et == 0 && job == 0) ts3[14] = ptx::globaltimer();
                     }
                     const long long c_in = clock64();
-                    if (DENSE) {
+                    const bool routed_only = DENSE && !from_ws;
+                    if (routed_only) {
                         // only this expert's routed tokens (~1/E of the dense
                         // columns): canonical rows off1.., resident rows via s_tok,
                         // TMEM column = resident row - cb; 8 loads in flight
@@ -1046,16 +1047,9 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                                 const int col = (j < ne1 ? s_tok[off1 + j] : cb) - cb;
                                 const bool in = j < ne1 && col >= 0 && col < nc;
                                 pos8[i] = in ? off1 + j : -1;
-                                if (from_ws) {
-                                    float s = 0.f;
-                                    for (int k = 0; k < Sg; ++k)
-                                        s += in ? __ldcg(w0 + (int64_t)k * NMAX * kBM + col * kBM) : 0.f;
-                                    r8[i] = __float_as_uint(s);
-                                } else {
-                                    r8[i] = ptx::tmem_ld_32x32b_x1(t_base + (in ? col : 0));
-                                }
+                                r8[i] = ptx::tmem_ld_32x32b_x1(t_base + (in ? col : 0));
                             }
-                            if (!from_ws) ptx::tmem_wait_ld_dep8(r8);
+                            ptx::tmem_wait_ld_dep8(r8);
 #pragma unroll
                             for (int i = 0; i < 8; ++i)
                                 if (pos8[i] >= 0)
@@ -1063,8 +1057,10 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                                         __float2bfloat16(gelu_erf(__uint_as_float(r8[i]) + bias));
                         }
                     }
+                    // dispatch path, or a split-K finisher: every column (dense
+                    // keeps the routed ones), values from TMEM or the partials
 #pragma unroll 1
-                    for (int col = 0; col < (DENSE ? 0 : nc); col += kG) {
+                    for (int col = 0; col < (routed_only ? 0 : nc); col += kG) {
                         float v[kG];
                         final4(col, v);
                         // branch-free: independent GELUs and row lookups, then
@@ -1110,16 +1106,15 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     const __nv_bfloat16* xres = DENSE ? a.res_x_in : rx;
 #pragma unroll 1
-                    for (int col = 0; col < nc; col += 2 * kG) {
-                        __nv_bfloat16 xin[2 * kG];  // residual loads in flight first
+                    for (int col = 0; col < nc; col += kG) {
+                        __nv_bfloat16 xin[kG];  // residual loads in flight first
 #pragma unroll
-                        for (int i = 0; i < 2 * kG; ++i)
+                        for (int i = 0; i < kG; ++i)
                             if (col + i < nc) xin[i] = xres[s_rrow[col + i] * a.d + m_glob];
-                        float v[2 * kG];
-                        final4(col, *reinterpret_cast<float(*)[kG]>(&v[0]));
-                        if (col + kG < nc) final4(col + kG, *reinterpret_cast<float(*)[kG]>(&v[kG]));
+                        float v[kG];
+                        final4(col, v);
 #pragma unroll
-                        for (int i = 0; i < 2 * kG; ++i)
+                        for (int i = 0; i < kG; ++i)
                             if (col + i < nc)
                                 a.res_x_out[(int64_t)(off_e + cb + col + i) * a.d + m_glob] = __float2bfloat16(
                                     __bfloat162float(xin[i]) + s_rprob[col + i] * (v[i] + bias));

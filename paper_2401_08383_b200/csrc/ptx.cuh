@@ -34,28 +34,34 @@ static __device__ volatile int* g_dbg_host = nullptr;
 // copied into g_dbg_host[4..11] on a timeout
 static __device__ volatile int* g_dbg_prog = nullptr;
 
+// Cold path of a timed-out spin: error word, host-mapped dump, trap. Kept out
+// of line so every wait site carries only its poll loop (instruction-cache
+// footprint of the persistent kernels).
+static __device__ __noinline__ void spin_timeout(int* err, int code) {
+    if (err) atomicExch(err, code);
+    if (g_dbg_host) {
+        g_dbg_host[1] = code;
+        g_dbg_host[2] = (int)blockIdx.x;
+        g_dbg_host[3] = (int)threadIdx.x;
+        if (g_dbg_prog)
+            for (int i = 0; i < 8; ++i) g_dbg_host[4 + i] = g_dbg_prog[i];
+        __threadfence_system();
+        g_dbg_host[0] = 1;
+    }
+    __threadfence_system();
+    __trap();
+}
+
 struct SpinGuard {
     uint64_t start = 0;
     uint32_t iters = 0;
     __device__ __forceinline__ void step(int* err, int code, uint64_t ns = 4000000000ull) {
         if ((++iters & 1023u) == 0) {
             const uint64_t now = globaltimer();
-            if (start == 0) {
+            if (start == 0)
                 start = now;
-            } else if (now - start > ns) {
-                if (err) atomicExch(err, code);
-                if (g_dbg_host) {
-                    g_dbg_host[1] = code;
-                    g_dbg_host[2] = (int)blockIdx.x;
-                    g_dbg_host[3] = (int)threadIdx.x;
-                    if (g_dbg_prog)
-                        for (int i = 0; i < 8; ++i) g_dbg_host[4 + i] = g_dbg_prog[i];
-                    __threadfence_system();
-                    g_dbg_host[0] = 1;
-                }
-                __threadfence_system();
-                __trap();
-            }
+            else if (now - start > ns)
+                spin_timeout(err, code);
         }
     }
 };
