@@ -95,17 +95,15 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 // 148-way atomic counter serialises for ~8 us at one L2 slice).
 __device__ void flag_barrier(uint64_t* slots, uint64_t epoch, int32_t* err) {
     __syncthreads();
-    if (threadIdx.x == 0) {
+    // published by the last thread: thread 0 issued the CTA's weight-prefetch
+    // TMA loads, and a release by it may wait for those to land
+    if (threadIdx.x == blockDim.x - 1) {
         asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(slots + blockIdx.x), "l"(epoch) : "memory");
     }
     if (threadIdx.x < gridDim.x) {
         ptx::SpinGuard g;
-        for (;;) {
-            uint64_t v;
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(slots + threadIdx.x) : "memory");
-            if (v >= epoch) break;
-            g.step(err, ERR_TIMEOUT_PIPE);
-        }
+        while (ptx::ld_relaxed_u64(slots + threadIdx.x, false) < epoch) g.step(err, ERR_TIMEOUT_PIPE);
+        ptx::fence_acquire(false);
     }
     __syncthreads();
 }
@@ -541,9 +539,11 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         }
         __syncthreads();
     }
-    if (tid < a.G) {
-        if (a.G > 1) __threadfence_system();
-        uint64_t* f = reinterpret_cast<uint64_t*>(a.peers[tid] + a.sym.cflags);
+    if (tid >= kThreads - a.G) {  // last threads: no prefetch TMA outstanding
+        const int dest = kThreads - 1 - tid;
+        // st.release.sys alone orders this CTA's row stores (bar.sync above);
+        // an extra fence.sc.sys before it only added latency
+        uint64_t* f = reinterpret_cast<uint64_t*>(a.peers[dest] + a.sym.cflags);
         ptx::flag_publish(f + ((int64_t)parity * a.G + a.rank) * kMaxCtas + blockIdx.x, epoch, a.G > 1);
     }
     if (tid == 0) tl_mark(a.tl, 6);
@@ -552,10 +552,20 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     {
         const uint64_t* f = reinterpret_cast<const uint64_t*>(a.own_sym + a.sym.cflags) +
                             (int64_t)parity * a.G * kMaxCtas;
+        if (ts4 && tid < 8) s_prog[tid] = 0;  // diagnostics: per-source last flag seen (low bits of the timer)
+        if (ts4) __syncthreads();
         for (int w = tid; w < a.G * P; w += kThreads) {
             const uint64_t* fw = f + (int64_t)(w / P) * kMaxCtas + (w % P);
             ptx::SpinGuard g;
-            while (ptx::flag_read(fw, a.G > 1) < epoch) g.step(a.err, 112);
+            while (ptx::ld_relaxed_u64(fw, a.G > 1) < epoch) g.step(a.err, 112);
+            // acquire once, on the flag itself (a full fence.acq_rel.sys after
+            // the loop cost ~5 us at G=4); bar.sync below extends it to the CTA
+            (void)ptx::flag_read(fw, a.G > 1);
+            if (ts4 && w / P < 8) atomicMax(&s_prog[w / P], (int)(ptx::globaltimer() & 0x7fffffff));
+        }
+        if (ts4) {
+            __syncthreads();
+            if (tid < a.G && tid < 8) ts4[8 + tid] = (ptx::globaltimer() & ~0x7fffffffull) | (uint32_t)s_prog[tid];
         }
     }
     __syncthreads();
@@ -738,7 +748,8 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 // all GEMM1 (tile, chunk) units of expert e must be complete
                 const int target = mt1 * ((cnt(0, e) + NMAX - 1) / NMAX);
                 ptx::SpinGuard sg;
-                while (ld_acq_s32(a.hdone + parity * a.E_loc + e) < target) sg.step(a.err, 107);
+                while (ptx::ld_relaxed_s32(a.hdone + parity * a.E_loc + e) < target) sg.step(a.err, 107);
+                ptx::fence_acquire(false);
                 waited_e = e;
             }
             // GEMM1 rows: dispatched tokens (recv region) or, dense, the resident
@@ -882,7 +893,8 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 for (int u = lane; u < n; u += 32) {
                     ptx::SpinGuard sg;
                     uint64_t v;
-                    while (((v = ptx::ld_acquire_gpu_u64(rf + u)) >> 40) != e24) sg.step(a.err, 109);
+                    // the flag carries the route itself: a relaxed read suffices
+                    while (((v = ptx::ld_relaxed_u64(rf + u, false)) >> 40) != e24) sg.step(a.err, 109);
                     s_exp[u] = (int)((v >> 32) & 0xFF);  // slot
                     s_prob[u] = __uint_as_float((uint32_t)v);
                 }
@@ -1081,11 +1093,11 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     }
                     if (ts2 && et == 0 && job == 0) ts2[job] = (uint64_t)(clock64() - c_in);  // diagnostics
                     if (!from_ws) release_tmem();
-                    if (ts3 && et == 0 && job == 0) ts3[4] = ptx::globaltimer();
+                    if (DENSE && ts3 && et == 0 && job == 0) ts3[4] = ptx::globaltimer();
                     asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (ts3 && et == 0 && job == 0) ts3[5] = ptx::globaltimer();
+                    if (DENSE && ts3 && et == 0 && job == 0) ts3[5] = ptx::globaltimer();
                     if (et == 0) red_add_release(a.hdone + parity * a.E_loc + e, 1);
-                    if (ts3 && et == 0 && job == 0) ts3[6] = ptx::globaltimer();
+                    if (DENSE && ts3 && et == 0 && job == 0) ts3[6] = ptx::globaltimer();
                 } else {
                     // per token: source row of the residual, gate prob, output row
                     asm volatile("bar.sync 1, 128;" ::: "memory");

@@ -338,6 +338,29 @@ __device__ __forceinline__ uint64_t ld_acquire_gpu_u64(const uint64_t* p) {
 __device__ __forceinline__ void st_release_gpu_u64(uint64_t* p, uint64_t v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Spin-polls read flags RELAXED and issue one acquire fence once the value is
+// seen: an acquire load at >= cluster scope invalidates L1 (CCTL.IVALL), and
+// issuing it on every poll iteration of 148+ spinning threads stretched each
+// flag observation to ~3 us.
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p, bool sys) {
+    uint64_t v;
+    if (sys)
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int32_t ld_relaxed_s32(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acquire(bool sys) {
+    if (sys)
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 // flag publish/observe at the narrowest scope covering every peer: .gpu when
 // the whole job is one device, .sys once peers are other GPUs (NVLink)
 __device__ __forceinline__ void flag_publish(uint64_t* p, uint64_t v, bool multi_gpu) {

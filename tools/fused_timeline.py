@@ -16,15 +16,28 @@ def main():
     from paper_2401_08383_b200.model import MoeModel, MoeModelConfig
     E = int(os.environ.get("E", "8"))
     B = int(os.environ.get("B", "64"))
+    G = int(os.environ.get("WORLD_SIZE", "1"))  # under torchrun: one process per GPU
+    rank = int(os.environ.get("RANK", "0"))
+    if G > 1:
+        import torch.distributed as dist
+        from paper_2401_08383_b200 import dist as xd
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+        dist.init_process_group("gloo")
     cfg = MoeModelConfig(num_experts=E, num_layers=4, d_model=1024, d_ffn=4096, tokens_per_gpu=B,
-                         seed=1234, gate_affinity=0.8)
-    m = MoeModel(cfg, pl.contiguous_placement(E, 4, Topology(1, 1)))
+                         seed=1234, gate_affinity=0.8, world_size=G, rank=rank)
+    m = MoeModel(cfg, pl.contiguous_placement(E, 4, Topology(1, G)))
+    if G > 1:
+        m.connect(xd.exchange_handles(m.ipc_handle()))
     x = torch.randn(B, 1024).to(torch.bfloat16).cuda()
     s = torch.cuda.Stream()
     for _ in range(3):
         m.step(x, s)
     s.synchronize()
     m.check()
+    if G > 1:
+        dist.barrier()
+        if rank != 0:
+            return
     ctas = 148
     buf = np.zeros((5, ctas, 16), np.uint64)
     _capi.call("exf_model_read_ffn_timeline", m.handle, buf.ctypes.data, ctas)
@@ -99,6 +112,11 @@ def main():
               f" | B start {(cur[c, 8] - z) / 1e3:6.2f} fullB {(cur[c, 9] - z) / 1e3:6.2f} "
               f"fullA {(cur[c, 10] - z) / 1e3:6.2f} mma {(t[c, 2] - z) / 1e3:6.2f}")
     print(f"  exit       min {(cur[:, 15] - z).min() / 1e3:7.2f} max {(cur[:, 15] - z).max() / 1e3:7.2f}")
+    if G > 1:
+        t4b = buf[4].astype(np.int64)
+        print("  dispatch flags of source rank g all seen (median over CTAs, rel. prev exit):",
+              [round(float(np.median((t4b[:, 8 + g] - z) / 1e3)), 2) for g in range(min(G, 8))],
+              "; own completion median %.2f" % np.median((cur[:, 6] - z) / 1e3))
     ok = t[:, 12] > 0
     print(f"job 1 first A TMA issued {(rel[:, 12] - rel[:, 3])[ok].mean():.2f} us after job 0's last MMA; "
           f"first B gather {(rel[:, 13] - rel[:, 3])[ok].mean():.2f}; job 1 first MMA "
