@@ -45,6 +45,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxLocal = 64;
 constexpr int kMaxKeys = 64;
+constexpr int kMaxList = 4096;  // G * C slots the dispatch path can route per layer
 
 __device__ __forceinline__ void unpack8(const int4& v, float (&f)[8]) {
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
@@ -90,23 +91,6 @@ __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// All-to-all flag barrier: every CTA release-stores its own epoch slot, then
-// P threads acquire-poll all slots in parallel. No same-address atomics (a
-// 148-way atomic counter serialises for ~8 us at one L2 slice).
-__device__ void flag_barrier(uint64_t* slots, uint64_t epoch, int32_t* err) {
-    __syncthreads();
-    // published by the last thread: thread 0 issued the CTA's weight-prefetch
-    // TMA loads, and a release by it may wait for those to land
-    if (threadIdx.x == blockDim.x - 1) {
-        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(slots + blockIdx.x), "l"(epoch) : "memory");
-    }
-    if (threadIdx.x < gridDim.x) {
-        ptx::SpinGuard g;
-        while (ptx::ld_relaxed_u64(slots + threadIdx.x, false) < epoch) g.step(err, ERR_TIMEOUT_PIPE);
-        ptx::fence_acquire(false);
-    }
-    __syncthreads();
-}
 
 __device__ void grid_barrier(uint32_t* gbar, int32_t* err) {
     __syncthreads();
@@ -141,8 +125,11 @@ struct Smem {
     static constexpr int kOffA = 0;
     static constexpr int kOffB = STAGES * kA;
     static constexpr int kOffTab = kOffB + BST * kB;
-    static constexpr int kTabInts = 20;  // n, off, seg_prefix[9], seg_start[8]
-    static constexpr int kOffBar = kOffTab + kMaxLocal * kTabInts * 4;
+    static constexpr int kTabInts = 2;  // per local expert: tokens, first canonical row
+    // dispatch path: canonical (slot, source, order) list of received slots,
+    // entry = source * C + t (t = the token's resident index at its source)
+    static constexpr int kOffList = kOffTab + kMaxLocal * kTabInts * 4;
+    static constexpr int kOffBar = kOffList + kMaxList * 2;
     // fullA[S], emptyA[S], fullB[BST], emptyB[BST], tmem_full[NBUF<=4],
     // tmem_empty[NBUF<=4], wg_bar
     static constexpr int kOffMisc = kOffBar + (2 * STAGES + 2 * BST + 10) * 8;
@@ -323,9 +310,6 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     mark3(11);
     // the next layer's GEMM1 counters start from zero
     if (blockIdx.x == 0 && tid < a.E_loc) a.hdone[((parity ^ 1) * a.E_loc) + tid] = 0;
-    // launch epoch: slots [0, P) are per-CTA barrier flags, slot 256 the counter
-    uint64_t* bslots = reinterpret_cast<uint64_t*>(a.gbar);
-    const uint64_t bepoch = bslots[256] + 1;
 
     if (DENSE) {
         // GEMM1 runs over all n resident tokens at once; the GEMM2 tables are
@@ -436,67 +420,24 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     }
     __syncthreads();
     mark3(2);
-    // ---------------- (2) stable ranks within the CTA slice, per-key counts
-    if (warp == 0) {
-        for (int b = 0; b < nt; b += 32) {
-            const int i = b + lane;
-            int key = -1;
-            if (i < nt) {
-                key = s_key[s_exp[i]];
-            }
-            const uint32_t peers = __match_any_sync(0xffffffffu, key);
-            const int rank = __popc(peers & lanemask_lt());
-            if (key >= 0) s_pos[i] = (s_cnt[key] + rank) | (key << 20);
-            __syncwarp();
-            if (key >= 0 && rank == 0) s_cnt[key] += __popc(peers);
-            __syncwarp();
-        }
-        for (int k = lane; k < E; k += 32) a.cta_cnt[blockIdx.x * E + k] = s_cnt[k];
-    }
-    if (tid == 0) tl_mark(a.tl, 4);
-    mark3(3);
-    flag_barrier(bslots, bepoch, a.err);
-    mark3(4);
-    if (tid == 0) tl_mark(a.tl, 5);
-    // per-key totals and this CTA's offset: only the nact token-owning CTAs
-    // have counts; (key, part) threads sum strided CTA subsets in parallel
-    const int nact = max(1, (n + a.tpc - 1) / a.tpc);
-    if (nt > 0 || blockIdx.x == 0) {
-        const int parts = kThreads / E;
-        const int k = tid % E, part = tid / E;
-        if (part < parts) {
-            int tot = 0, before = 0;
-            for (int c = part; c < nact; c += parts) {
-                const int v = __ldcg(a.cta_cnt + c * E + k);
-                tot += v;
-                before += (c < (int)blockIdx.x) ? v : 0;
-            }
-            if (tot) atomicAdd(&s_tot[k], tot);
-            if (before) atomicAdd(&s_before[k], before);
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
-        int acc = 0;
-        for (int k = 0; k < E; ++k) {
-            s_start[k] = acc;
-            acc += s_tot[k];
-        }
-        s_start[E] = acc;
-    }
-    __syncthreads();
-    // ---------------- (3) dispatch: rows straight into the destination region
+    // ---------------- (2) dispatch at fixed slots, per-slot route flags
+    // Token t of this rank goes to slot (rank, t) of its destination's receive
+    // region; every slot of the CTA's range (also the empty ones, t >= n) gets
+    // a route flag {epoch:24 | local slot or 0xFF:8} at EVERY destination. The
+    // destinations derive the canonical (slot, source, order) lists from the
+    // G*C flags: no intra-GPU barrier, no count prefix (each grid-wide hand-off
+    // costs ~3 us on this GPU), a single exchange round.
+    const uint64_t e24 = epoch & 0xFFFFFFull;
+    const bool sys = a.G > 1;
     {
         const int64_t row_bytes = (int64_t)a.d * 2;
         const int vec = a.d >> 3;
         for (int i = warp; i < nt; i += kWarps) {
             const int t = t0 + i;
-            const int key = s_pos[i] >> 20;
+            const int key = s_key[s_exp[i]];
             const int dest = key / a.E_loc;
-            const int pos = s_start[key] + s_before[key] + (s_pos[i] & 0xFFFFF);
-            const int local = pos - s_start[dest * a.E_loc];
             uint8_t* pbase = a.peers[dest];
-            const int64_t slot_row = ((int64_t)(parity * a.G + a.rank) * a.C + local);
+            const int64_t slot_row = (int64_t)(parity * a.G + a.rank) * a.C + t;
             int4* dst = reinterpret_cast<int4*>(pbase + a.sym.recv_x + slot_row * row_bytes);
             const int4* src = reinterpret_cast<const int4*>(a.res_x_in + (int64_t)t * a.d);
             int4 buf[8];  // d <= 2048: one row is 8 int4 per lane
@@ -518,81 +459,86 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 m.prob = s_prob[i];
                 m.pad = 0;
                 reinterpret_cast<RecvMeta*>(pbase + a.sym.recv_meta)[slot_row] = m;
+                if (dest != a.rank) atomicAdd(&a.crossed[a.layer], 1ull);
             }
         }
     }
-    __syncthreads();
+    __syncthreads();  // rows and metas stored before any flag (release below)
     mark3(5);
-    // completion: every CTA release-flags its own slot at every destination
-    // (no last-arriver counter: a same-address atomic chain plus a publishing
-    // CTA cost ~4 us); CTA 0 also publishes this source's per-slot counts
-    if (blockIdx.x == 0) {
-        if (tid < E) {
-            const int dest = tid / a.E_loc, slot = tid - dest * a.E_loc;
-            int32_t* cnt = reinterpret_cast<int32_t*>(a.peers[dest] + a.sym.recv_cnt);
-            cnt[((int64_t)parity * a.G + a.rank) * a.E_loc + slot] = s_tot[tid];
-        }
-        if (tid == 0) {
-            int stay = 0;
-            for (int s2 = 0; s2 < a.E_loc; ++s2) stay += s_tot[a.rank * a.E_loc + s2];
-            atomicAdd(&a.crossed[a.layer], (unsigned long long)(n - stay));
-        }
-        __syncthreads();
-    }
-    if (tid >= kThreads - a.G) {  // last threads: no prefetch TMA outstanding
-        const int dest = kThreads - 1 - tid;
-        // st.release.sys alone orders this CTA's row stores (bar.sync above);
-        // an extra fence.sc.sys before it only added latency
-        uint64_t* f = reinterpret_cast<uint64_t*>(a.peers[dest] + a.sym.cflags);
-        ptx::flag_publish(f + ((int64_t)parity * a.G + a.rank) * kMaxCtas + blockIdx.x, epoch, a.G > 1);
+    // flags published by the last threads: thread 0 issued the weight-prefetch
+    // TMA loads, and a release by it may wait for those to land
+    for (int q = kThreads - 1 - tid; q < a.tpc * a.G; q += kThreads) {
+        const int i = q / a.G, g = q - i * a.G;
+        const int t = t0 + i;
+        if (t >= a.C) continue;
+        const int key = i < nt ? s_key[s_exp[i]] : -1;
+        const uint64_t slotv = (key >= 0 && key / a.E_loc == g) ? (uint64_t)(key - g * a.E_loc) : 0xFFull;
+        uint64_t* f = reinterpret_cast<uint64_t*>(a.peers[g] + a.sym.cflags);
+        ptx::flag_publish(f + ((int64_t)parity * a.G + a.rank) * a.C + t, (e24 << 40) | (slotv << 32), sys);
     }
     if (tid == 0) tl_mark(a.tl, 6);
     mark3(6);
-    // ---------------- wait for every source CTA's dispatch, build the tables
+    // ---------------- (3) every CTA reads the G*C route flags destined here
+    // (scratch in the idle token-row ring: slot per entry, per-warp counts)
+    const int K = a.G * a.C;
+    uint8_t* s_kslot = smem + S::kOffB;
+    int32_t* s_wcnt = reinterpret_cast<int32_t*>(smem + S::kOffB + kMaxList);  // [kWarps][kMaxKeys]
+    int16_t* s_list = reinterpret_cast<int16_t*>(smem + S::kOffList);
+    if (tid < kMaxKeys) {
+        s_cnt[tid] = 0;
+        s_before[tid] = 0;
+    }
     {
-        const uint64_t* f = reinterpret_cast<const uint64_t*>(a.own_sym + a.sym.cflags) +
-                            (int64_t)parity * a.G * kMaxCtas;
-        if (ts4 && tid < 8) s_prog[tid] = 0;  // diagnostics: per-source last flag seen (low bits of the timer)
-        if (ts4) __syncthreads();
-        for (int w = tid; w < a.G * P; w += kThreads) {
-            const uint64_t* fw = f + (int64_t)(w / P) * kMaxCtas + (w % P);
+        const uint64_t* f = reinterpret_cast<const uint64_t*>(a.own_sym + a.sym.cflags) + (int64_t)parity * K;
+        for (int k = tid; k < K; k += kThreads) {
             ptx::SpinGuard g;
-            while (ptx::ld_relaxed_u64(fw, a.G > 1) < epoch) g.step(a.err, 112);
-            // acquire once, on the flag itself (a full fence.acq_rel.sys after
-            // the loop cost ~5 us at G=4); bar.sync below extends it to the CTA
-            (void)ptx::flag_read(fw, a.G > 1);
-            if (ts4 && w / P < 8) atomicMax(&s_prog[w / P], (int)(ptx::globaltimer() & 0x7fffffff));
-        }
-        if (ts4) {
-            __syncthreads();
-            if (tid < a.G && tid < 8) ts4[8 + tid] = (ptx::globaltimer() & ~0x7fffffffull) | (uint32_t)s_prog[tid];
+            uint64_t v;
+            while (((v = ptx::ld_relaxed_u64(f + k, sys)) >> 40) != e24) g.step(a.err, 112);
+            // acquire once, on the flag itself (orders this slot's row + meta;
+            // bar.sync below extends it to the CTA)
+            (void)ptx::flag_read(f + k, sys);
+            s_kslot[k] = (uint8_t)((v >> 32) & 0xFF);
         }
     }
     __syncthreads();
-    const int32_t* cnt = reinterpret_cast<const int32_t*>(a.own_sym + a.sym.recv_cnt) +
-                         (int64_t)parity * a.G * a.E_loc;
-    if (tid < a.E_loc) {
-        const int e = tid;
-        int32_t* t = tab + e * S::kTabInts;
-        int nn = 0, off = 0;
-        for (int s2 = 0; s2 < a.G; ++s2) {
-            int st = 0;
-            for (int x = 0; x < e; ++x) st += cnt[s2 * a.E_loc + x];
-            off += st;
-            t[2 + s2] = nn;
-            t[11 + s2] = st;
-            nn += cnt[s2 * a.E_loc + e];
+    for (int k = tid; k < K; k += kThreads)
+        if (s_kslot[k] != 0xFF) atomicAdd(&s_cnt[s_kslot[k]], 1);
+    __syncthreads();
+    if (tid == 0) {
+        int acc = 0;
+        for (int e = 0; e < a.E_loc; ++e) {
+            tab[e * S::kTabInts] = s_cnt[e];
+            tab[e * S::kTabInts + 1] = acc;
+            s_start[e] = acc;
+            acc += s_cnt[e];
         }
-        t[2 + a.G] = nn;
-        t[0] = nn;
-        t[1] = off;
-    }
-    if (blockIdx.x == 0 && tid == 0) {
-        int total = 0;
-        for (int i = 0; i < a.G * a.E_loc; ++i) total += cnt[i];
-        *a.n_res_out = total;
+        if (blockIdx.x == 0) *a.n_res_out = acc;
     }
     __syncthreads();
+    // stable placement in (source, t) order, 256 entries per round: warp ranks
+    // by match_any, cross-warp prefix through s_wcnt
+    for (int k0 = 0; k0 < K; k0 += kThreads) {
+        const int k = k0 + tid;
+        const int key = (k < K && s_kslot[k] != 0xFF) ? s_kslot[k] : -1;
+        const uint32_t peers = __match_any_sync(0xffffffffu, key);
+        const int rk = __popc(peers & lanemask_lt());
+        for (int x = tid; x < kWarps * kMaxKeys; x += kThreads) s_wcnt[x] = 0;
+        __syncthreads();
+        if (key >= 0 && rk == 0) s_wcnt[warp * kMaxKeys + key] = __popc(peers);
+        __syncthreads();
+        if (key >= 0) {
+            int before = s_start[key] + s_before[key] + rk;
+            for (int w = 0; w < warp; ++w) before += s_wcnt[w * kMaxKeys + key];
+            s_list[before] = (int16_t)k;
+        }
+        __syncthreads();
+        if (tid < a.E_loc) {
+            int tot = 0;
+            for (int w = 0; w < kWarps; ++w) tot += s_wcnt[w * kMaxKeys + tid];
+            s_before[tid] += tot;
+        }
+        __syncthreads();
+    }
     if (tid == 0) tl_mark(a.tl, 7);
     if (ts && tid == 0) ts[1] = ptx::globaltimer();
     mark3(7);
@@ -600,11 +546,10 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
 
     const RecvMeta* rmeta = reinterpret_cast<const RecvMeta*>(a.own_sym + a.sym.recv_meta);
     const __nv_bfloat16* rx = reinterpret_cast<const __nv_bfloat16*>(a.own_sym + a.sym.recv_x);
+    // receive row of the i-th token of local expert e (canonical order)
+    const int16_t* s_list_r = reinterpret_cast<const int16_t*>(smem + S::kOffList);
     auto recv_row = [&](int e, int i) -> int64_t {
-        const int32_t* t = tab + e * S::kTabInts;
-        int s2 = 0;
-        while (s2 + 1 < a.G && t[2 + s2 + 1] <= i) ++s2;
-        return ((int64_t)parity * a.G + s2) * a.C + t[11 + s2] + (i - t[2 + s2]);
+        return (int64_t)parity * a.G * a.C + s_list_r[tab[e * S::kTabInts + 1] + i];
     };
     // tokens of (gemm, expert): dense GEMM1 runs over every resident token;
     // otherwise (and for dense GEMM2, once the routes are in) the tables
@@ -909,9 +854,6 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         int32_t* tb = tab + e * S::kTabInts;
                         tb[0] = s_cnt[e];
                         tb[1] = acc;
-                        tb[2] = 0;
-                        tb[3] = s_cnt[e];
-                        tb[11] = 0;
                         s_start[e] = acc;
                         acc += s_cnt[e];
                     }
@@ -1144,9 +1086,6 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     if (tid == 0) tl_mark(a.tl, 3);
     if (ts && tid == 0) ts[15] = ptx::globaltimer();
     mark3(15);
-    // every CTA read the launch epoch before arriving at the barrier, which
-    // CTA 0 passed before getting here: safe to advance it
-    if (blockIdx.x == 0 && tid == 0) bslots[256] = bepoch;
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, NBUF * NMAX);

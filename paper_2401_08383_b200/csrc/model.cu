@@ -200,7 +200,7 @@ exf_status build_layout(exf_model* m) {
     m->sym.flags = take(2LL * G * 8);
     m->sym.gather_x = take((int64_t)C * d * 2);
     m->sym.gflags = take((int64_t)G * 8);
-    m->sym.cflags = take(2LL * G * kMaxCtas * 8);
+    m->sym.cflags = take(2LL * G * std::max<int64_t>(C, kMaxCtas) * 8);  // route flags [2][G][max(C, 256)]
     m->sym.total = o;
     EXF_CUDA_TRY(cudaMalloc(&m->sym_base, (size_t)o));
     EXF_CUDA_TRY(cudaMemset(m->sym_base, 0, (size_t)o));
@@ -510,7 +510,9 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         // one token per CTA while C <= #SMs: the gate's (token, expert) dot
         // products then spread over 8 warps of many CTAs
         m->f_tpc = std::max(1, (C + m->f_ctas - 1) / m->f_ctas);
-        if (m->f_tpc > 32 || d > 2048 || E > 64) m->fused = false;  // two-kernel path instead
+        // two-kernel path instead when the fused kernel's limits are exceeded
+        // (G*C <= 4096 routed slots per layer: layer_fused.cu kMaxList)
+        if (m->f_tpc > 32 || d > 2048 || E > 64 || (int64_t)c.world_size * C > 4096) m->fused = false;
         // single GPU: every expert is local, so the layer runs dense over all
         // resident tokens and the token phase leaves the GEMMs' critical path
         m->dense = m->fused && c.world_size == 1 && m->f_tpc == 1;

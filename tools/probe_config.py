@@ -1,3 +1,6 @@
+"""Diagnostics: build a model of the given shape (E L d d_ffn B), run two steps and
+report the fused kernel's timeout channel (exf_debug_last_timeout) on failure.
+Usage: python tools/probe_config.py E L d dff B"""
 import os, sys, ctypes as C, numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
