@@ -694,7 +694,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 const int target = mt1 * ((cnt(0, e) + NMAX - 1) / NMAX);
                 ptx::SpinGuard sg;
                 while (ptx::ld_relaxed_s32(a.hdone + parity * a.E_loc + e) < target) sg.step(a.err, 107);
-                ptx::fence_acquire(false);
+                (void)ld_acq_s32(a.hdone + parity * a.E_loc + e);  // acquire on the counter itself
                 waited_e = e;
             }
             // GEMM1 rows: dispatched tokens (recv region) or, dense, the resident
