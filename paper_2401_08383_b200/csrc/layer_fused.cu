@@ -266,6 +266,15 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 ptx::tma_load_2d(smem + S::kOffA + s * S::kA + j * S::kA1, tm, &full[s],
                                  (pc.kb0 + kbr(pc.nkb, s * kKPS) + j) * kBK, pc.e * rows + pc.mt * kBM, pol_a);
         }
+        // dense: the rest of the first pieces into L2 while the previous layer
+        // drains (its tail leaves HBM bandwidth idle)
+        for (int p = 0; DENSE && p < min(npc, a.xpre); ++p) {
+            const Piece q = s_pc[p];
+            const CUtensorMap* tq = q.g == 0 ? &tmA1 : &tmA2;
+            const int rq = q.g == 0 ? a.dff : a.d;
+            for (int kb = p == 0 ? npre * kKPS : 0; kb < q.nkb; ++kb)
+                ptx::tma_prefetch_l2_2d(tq, (q.kb0 + kbr(q.nkb, kb - kb % kKPS) + kb % kKPS) * kBK, q.e * rq + q.mt * kBM);
+        }
     };
     if (warp == 0 && lane == 0) {
         if (wg_smem) {
@@ -282,7 +291,12 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     }
 
     // ---------------- dependent part
-    ptx::pdl_wait();
+    // Dense mode waits for the previous kernel per warp, where each role first
+    // touches its output: the weight producer and the MMA warp never do, the
+    // token-row producer just before its first copy (its setup code, cold in
+    // the i-cache, runs while the previous layer drains), the token/epilogue
+    // warps at entry.
+    if (!DENSE) ptx::pdl_wait();
     ptx::pdl_trigger();
     mark3(1);
     if (tid == 0) tl_mark(a.tl, 1);
@@ -299,23 +313,24 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             if (c < (a.d >> 8)) xk[c] = *reinterpret_cast<const int4*>(x + c * 256 + lane * 8);
         if (lane == 0) mk = a.res_meta_in[t_first];
     }
-    const uint64_t q = *a.step * (uint64_t)a.L + (uint64_t)a.layer;
+    // the step counter is written by the previous step's last kernel, complete
+    // before this step's first kernel started (an L2 read: no wait needed)
+    const uint64_t q = ptx::ld_relaxed_u64(a.step, false) * (uint64_t)a.L + (uint64_t)a.layer;
     const int parity = (int)(q & 1);
     const uint64_t epoch = q + 1;
-    const int n = *a.n_res_in;
+    // dense (one GPU): every token stays resident, n == C (checked below)
+    const int n = DENSE ? a.C : *a.n_res_in;
     if (n > a.C) {  // uniform: every CTA reads the same n
         if (tid == 0) atomicExch(a.err, ERR_CAPACITY);
         __trap();
     }
     mark3(11);
-    // the next layer's GEMM1 counters start from zero
-    if (blockIdx.x == 0 && tid < a.E_loc) a.hdone[((parity ^ 1) * a.E_loc) + tid] = 0;
+    // the next layer's GEMM1 counters start from zero (dense: after the wait)
+    if (!DENSE && blockIdx.x == 0 && tid < a.E_loc) a.hdone[((parity ^ 1) * a.E_loc) + tid] = 0;
 
     if (DENSE) {
         // GEMM1 runs over all n resident tokens at once; the GEMM2 tables are
         // filled by the token warp (route_bar) while GEMM1 streams
-        if (blockIdx.x == 0 && tid == 0) *a.n_res_out = n;
-        __syncthreads();
         if (ts && tid == 0) ts[1] = ptx::globaltimer();
     } else {
     // ---------------- (1) gate: (token, expert) dot products spread over warps
@@ -729,6 +744,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         rows[j] = min(base + cb + (r < nc ? r : 0), row_lim - 1);
                     }
                 }
+                if (DENSE && it == 0) ptx::pdl_wait();  // first read of the previous layer's output
                 if (ts2 && it == 0 && lane == 0) ts2[9] = ptx::globaltimer();  // diagnostics: rows ready
                 if (ts4 && lane == 0 && p < 8 && c == 0) ts4[2 * p + 1] = ptx::globaltimer();
                 for (int kb = 0; kb < kbp; kb += kKPS, ++it) {
@@ -766,6 +782,16 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             const int E = a.E;
             const int t = blockIdx.x;
             const bool own = t < n;
+            ptx::pdl_wait();
+            if (blockIdx.x == 0 && warp == 3) {
+                if (lane == 0) {
+                    if (*a.n_res_in != n) atomicExch(a.err, ERR_CAPACITY);  // dense invariant n == C
+                    *a.n_res_out = n;
+                }
+                // the next layer's GEMM1 counters start from zero (the previous
+                // layer, their last user, is complete)
+                for (int k = lane; k < a.E_loc; k += 32) a.hdone[((parity ^ 1) * a.E_loc) + k] = 0;
+            }
             ResMeta mo{0, -1};
             if (own && warp == 3 && lane == 0) mo = a.res_meta_in[t];  // in flight with the gate
             // (1) gate on warps 3..7 (idle until the first accumulator is
@@ -825,7 +851,8 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         p = expf(lg[sel] - mx) / s;
                     }
                     const uint64_t flag = (e24 << 40) | ((uint64_t)(uint32_t)s_key[sel] << 32) | __float_as_uint(p);
-                    ptx::st_release_gpu_u64(rf + t, flag);
+                    ptx::st_relaxed_gpu_u64(rf + t, flag);  // the flag is the payload
+                    if (ts3) ts3[7] = ptx::globaltimer();
                     if (a.hist && a.layer > 0 && mo.prev_expert >= 0)
                         atomicAdd(&a.hist[((int64_t)(a.layer - 1) * E + mo.prev_expert) * E + sel], 1ull);
                     if (a.trace) a.trace[(int64_t)mo.token * a.L + a.layer] = sel;
@@ -835,6 +862,8 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     s_cnt[k] = 0;
                     s_before[k] = 0;
                 }
+                // (every CTA polls the same few L2 lines: polling a lane's flags
+                // in parallel only added contention, measured slower)
                 for (int u = lane; u < n; u += 32) {
                     ptx::SpinGuard sg;
                     uint64_t v;

@@ -149,6 +149,7 @@ struct FusedArgs {
     // it and publishes {epoch, slot, prob} in one 64-bit route flag; GEMM1's
     // epilogue keeps routed rows only, GEMM2 runs on the compact H
     int32_t dense;
+    int32_t xpre;  // dense: pieces whose weights are L2-prefetched before the PDL wait
     unsigned long long* tl;
     uint64_t* tstamp;    // optional per-CTA stamps [grid][16] (diagnostics)
 };

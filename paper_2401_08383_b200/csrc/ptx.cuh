@@ -338,6 +338,10 @@ __device__ __forceinline__ uint64_t ld_acquire_gpu_u64(const uint64_t* p) {
 __device__ __forceinline__ void st_release_gpu_u64(uint64_t* p, uint64_t v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// for a flag whose value IS the payload (nothing else to order behind it)
+__device__ __forceinline__ void st_relaxed_gpu_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 // Spin-polls read flags RELAXED and issue one acquire fence once the value is
 // seen: an acquire load at >= cluster scope invalidates L1 (CCTL.IVALL), and
 // issuing it on every poll iteration of 148+ spinning threads stretched each

@@ -96,7 +96,7 @@ def main():
         v = (cur[:, k] - z) / 1e3
         print(f"  {nm:10s} min {v.min():7.2f} mean {v.mean():7.2f} max {v.max():7.2f}")
     print(f"  first MMA  min {(t[:, 2] - z).min() / 1e3:7.2f} mean {(t[:, 2] - z).mean() / 1e3:7.2f}")
-    print("  dense token warp (rel. prev exit; median/max): gate %s ranks %s barrier %s prefix %s flag %s" % tuple(
+    print("  dense token warp (rel. prev exit; median/max): gate %s ranks %s barrier %s published %s flag %s" % tuple(
         "%.2f/%.2f" % (np.median((cur[:, k] - z) / 1e3), ((cur[:, k] - z) / 1e3).max()) for k in (12, 13, 14, 7, 2)))
     r10 = buf[1][:, 10].astype(np.int64)
     print("  dense GEMM1 epilogue of job 0 (us after tmem_full): tmem-ld %.2f route-wait %.2f stores %.2f bar %.2f "
