@@ -260,7 +260,7 @@ int32_t exf_model_launches_per_step(exf_model* model);
 /* JSON description of the launch plan (token tile, split-K, persistent
  * clusters per GEMM) into buf (NUL-terminated, truncated to len). */
 exf_status exf_model_describe(exf_model* model, char* buf, int32_t len);
-/* Diagnostics: per-CTA globaltimer stamps of the last launches ([4][ctas][16]
+/* Diagnostics: per-CTA globaltimer stamps of the last launches ([6][ctas][16]
  * u64; rows 0/1 = GEMM1/GEMM2 of the two-kernel path or expert-phase stamps
  * of the fused kernel, rows 2/3 = fused token-phase stamps of even/odd layers;
  * requires EXF_FFN_TIMELINE=1 at create time). */

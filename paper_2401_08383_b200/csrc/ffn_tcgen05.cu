@@ -484,6 +484,24 @@ exf_status make_weight_tmap(CUtensorMap* map, const void* base, int64_t rows, in
     return EXF_OK;
 }
 
+// Row-major [rows][cols] bf16 token matrix as UMMA B tiles: box = box_rows
+// rows x 64 cols, SWIZZLE_128B (the K-major layout of one k-block), rows past
+// the end zero-filled. Used where a tile's rows are contiguous (dense fused mode).
+exf_status make_tile_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return runtime_err("cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return runtime_err("cuTensorMapEncodeTiled (tile) failed: " + std::to_string((int)r));
+    return EXF_OK;
+}
+
 // Row-major [rows][cols] bf16 token matrix for TMA gather4: box = 1 row x 64
 // cols (128 B), SWIZZLE_128B, so four gathered rows land as one swizzled
 // 4-row slab of the UMMA K-major B tile.

@@ -204,7 +204,10 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // [2] gate done, [3] ranks done, [4] barrier passed, [5] dispatch stored,
     // [6] completion done, [7] flags seen / tables built, [15] exit
     uint64_t* ts3 = ts ? ts + (int64_t)(2 + (a.layer & 1)) * 4096 * 16 : nullptr;
-    uint64_t* ts4 = ts ? ts + (int64_t)4 * 4096 * 16 : nullptr;  // [2p], [2p+1]: B piece p setup start / rows ready
+    // dense: [2j], [2j+1] epilogue job j got its accumulator / finished (j < 8);
+    // dispatch path: [8 + g] flags of source g all seen
+    uint64_t* ts4 = ts ? ts + (int64_t)4 * 4096 * 16 : nullptr;
+    uint64_t* ts5 = ts ? ts + (int64_t)5 * 4096 * 16 : nullptr;  // B stage it < 16 issued (emptyB passed)
     auto mark3 = [&](int k) {
         if (ts3 && threadIdx.x == 0) ts3[k] = ptx::globaltimer();
     };
@@ -217,7 +220,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             ptx::mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < BST; ++s) {
-            ptx::mbar_init(&fullB[s], 32);  // one cp.async arrival per B-producer lane
+            ptx::mbar_init(&fullB[s], DENSE ? 1 : 32);  // TMA expect_tx / one cp.async arrival per lane
             ptx::mbar_init(&emptyB[s], 1);
         }
         for (int b = 0; b < NBUF; ++b) {
@@ -697,8 +700,51 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         if (ts3 && lane == 0) ts3[8] = ptx::globaltimer();
         int it = 0;
         int waited_e = -1;
+        if (DENSE) {
+            // Dense mode: every B tile is a contiguous row range (all resident
+            // tokens for GEMM1, expert e's canonical H rows for GEMM2), one TMA
+            // box per k-block. As cp.async (32 x 16 B per lane per stage) a
+            // stage took ~0.55 us to issue under the weight stream, so the
+            // ring never ran ahead and every job boundary stalled the MMA.
+            if (lane == 0) {
+                const uint64_t pol_b = ptx::policy_evict_last();  // re-read by every CTA
+                ptx::tma_prefetch_desc(&tmB1);
+                ptx::tma_prefetch_desc(&tmB2);
+                for (int p = 0; p < npc; ++p) {
+                    const Piece pc = s_pc[p];
+                    const int g = pc.g, e = pc.e, kbp = pc.nkb;
+                    const int nch = nchunks(p, g, e);
+                    if (g == 1 && nch > 0 && waited_e != e) {
+                        const int target = mt1 * ((cnt(0, e) + NMAX - 1) / NMAX);
+                        ptx::SpinGuard sg;
+                        while (ptx::ld_relaxed_s32(a.hdone + parity * a.E_loc + e) < target) sg.step(a.err, 107);
+                        (void)ld_acq_s32(a.hdone + parity * a.E_loc + e);
+                        // H was written through the generic proxy by other CTAs
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        waited_e = e;
+                    }
+                    const CUtensorMap* tb = g == 0 ? &tmB1 : &tmB2;
+                    const int row0 = g == 0 ? 0 : tab[e * S::kTabInts + 1];
+                    for (int c = 0; c < nch; ++c) {
+                        if (it == 0) ptx::pdl_wait();  // first read of the previous layer's output
+                        for (int kb = 0; kb < kbp; kb += kKPS, ++it) {
+                            const int sb = it % BST;
+                            s_prog[3] = it;
+                            s_prog[4] = p;
+                            ptx::mbar_wait(&emptyB[sb], ((it / BST) & 1) ^ 1, a.err, 108);
+                            if (ts && p == 1 && c == 0 && kb == 0) ts[13] = ptx::globaltimer();
+                            if (ts5 && it < 16) ts5[it] = ptx::globaltimer();
+                            ptx::mbar_arrive_expect_tx(&fullB[sb], S::kB);
+#pragma unroll
+                            for (int h = 0; h < kKPS; ++h)
+                                ptx::tma_load_2d(smem + S::kOffB + sb * S::kB + h * S::kB1, tb, &fullB[sb],
+                                                 (pc.kb0 + kbr(kbp, kb) + h) * kBK, row0 + c * NMAX, pol_b);
+                        }
+                    }
+                }
+            }
+        } else
         for (int p = 0; p < npc; ++p) {
-            if (ts4 && lane == 0 && p < 8) ts4[2 * p] = ptx::globaltimer();
             const Piece pc = s_pc[p];
             const int g = pc.g, e = pc.e, kbp = pc.nkb;
             const int n_e = cnt(g, e);
@@ -746,13 +792,13 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 }
                 if (DENSE && it == 0) ptx::pdl_wait();  // first read of the previous layer's output
                 if (ts2 && it == 0 && lane == 0) ts2[9] = ptx::globaltimer();  // diagnostics: rows ready
-                if (ts4 && lane == 0 && p < 8 && c == 0) ts4[2 * p + 1] = ptx::globaltimer();
                 for (int kb = 0; kb < kbp; kb += kKPS, ++it) {
                     const int sb = it % BST;
                     s_prog[3] = it;
                     s_prog[4] = p;
                     ptx::mbar_wait(&emptyB[sb], ((it / BST) & 1) ^ 1, a.err, 108);
                     if (ts && lane == 0 && p == 1 && c == 0 && kb == 0) ts[13] = ptx::globaltimer();  // job 1's first B rows
+                    if (ts5 && lane == 0 && it < 16) ts5[it] = ptx::globaltimer();
 #pragma unroll
                     for (int h = 0; h < kKPS; ++h) {
                         uint8_t* sbase = smem + S::kOffB + sb * S::kB + h * S::kB1;
@@ -868,23 +914,48 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     ptx::SpinGuard sg;
                     uint64_t v;
                     // the flag carries the route itself: a relaxed read suffices
-                    while (((v = ptx::ld_relaxed_u64(rf + u, false)) >> 40) != e24) sg.step(a.err, 109);
+                    while (((v = ptx::ld_relaxed_u64(rf + u, false)) >> 40) != e24) {
+                        // back off: 148 CTAs polling the same few L2 lines
+                        // delayed the late publishers' stores (measured)
+                        __nanosleep(256);
+                        sg.step(a.err, 109);
+                    }
                     s_exp[u] = (int)((v >> 32) & 0xFF);  // slot
                     s_prob[u] = __uint_as_float((uint32_t)v);
                 }
                 __syncwarp();
                 if (ts3 && lane == 0) ts3[13] = ptx::globaltimer();
                 // (4) canonical positions (slot, resident order) and GEMM2 tables
-                for (int u = lane; u < n; u += 32) atomicAdd(&s_cnt[s_exp[u]], 1);
-                __syncwarp();
-                if (lane == 0) {
-                    int acc = 0;
-                    for (int e = 0; e < a.E_loc; ++e) {
-                        int32_t* tb = tab + e * S::kTabInts;
-                        tb[0] = s_cnt[e];
-                        tb[1] = acc;
-                        s_start[e] = acc;
-                        acc += s_cnt[e];
+                // counts per slot by match_any leaders (routes cluster on a few
+                // slots: smem atomics on one counter serialised ~32-way), then a
+                // warp scan for the starts (E_loc <= 64: two values per lane)
+                for (int r = 0; r < n; r += 32) {
+                    const int key = r + lane < n ? s_exp[r + lane] : -1;
+                    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+                    if (key >= 0 && (peers & lanemask_lt()) == 0) s_cnt[key] += __popc(peers);
+                    __syncwarp();
+                }
+                {
+                    const int c0 = lane < a.E_loc ? s_cnt[lane] : 0;
+                    const int c1 = lane + 32 < a.E_loc ? s_cnt[lane + 32] : 0;
+                    int x0 = c0, x1 = c1;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y0 = __shfl_up_sync(0xffffffffu, x0, o);
+                        const int y1 = __shfl_up_sync(0xffffffffu, x1, o);
+                        if (lane >= o) {
+                            x0 += y0;
+                            x1 += y1;
+                        }
+                    }
+                    const int tot0 = __shfl_sync(0xffffffffu, x0, 31);
+                    if (lane < a.E_loc) {
+                        tab[lane * S::kTabInts] = c0;
+                        tab[lane * S::kTabInts + 1] = s_start[lane] = x0 - c0;
+                    }
+                    if (lane + 32 < a.E_loc) {
+                        tab[(lane + 32) * S::kTabInts] = c1;
+                        tab[(lane + 32) * S::kTabInts + 1] = s_start[lane + 32] = tot0 + x1 - c1;
                     }
                 }
                 __syncwarp();
@@ -936,6 +1007,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 if (ts2 && et == 0 && job == 1) ts2[11] = ptx::globaltimer();
                 ptx::mbar_wait(&tmem_full[buf], (job / NBUF) & 1, a.err, 110);
                 if (ts2 && et == 0 && job == 0) ts2[10] = ptx::globaltimer();
+                if (DENSE && ts4 && et == 0 && job < 8) ts4[2 * job] = ptx::globaltimer();
                 ptx::tc_fence_after();
                 const uint32_t t_base = tmem + buf * NMAX + ((uint32_t)lane_base << 16);
                 auto tmem16 = [&](int col, float (&v)[16]) {
@@ -976,7 +1048,10 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         if (s_flag) a.item_ctr[slot] = 0;  // next use is a later launch
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (!s_flag) continue;
+                    if (!s_flag) {
+                        if (DENSE && ts4 && et == 0 && job < 8) ts4[2 * job + 1] = ptx::globaltimer() | (1ull << 62);
+                        continue;
+                    }
                     from_ws = true;
                 }
                 // Final values 4 tokens at a time in a ROLLED loop. ncu showed the
@@ -1106,6 +1181,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     if (!DENSE && mt == 0 && et < nc)  // dense: the token's own CTA wrote it
                         a.res_meta_out[off_e + cb + et] = ResMeta{s_rtok[et], s_rexp[et]};
                 }
+                if (DENSE && ts4 && et == 0 && job < 8) ts4[2 * job + 1] = ptx::globaltimer() | ((uint64_t)from_ws << 63);
             }
         }
         if (ts2 && et == 0) ts2[12] = ptx::globaltimer();
@@ -1322,6 +1398,7 @@ exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int n
     // r01_tma_stream_bench.txt); the deeper token-row ring hides per-piece
     // setup and row-load latency at job boundaries
     if (nmax <= 32) return launch_nmax<32, 4, 10>(maps, a, s);
+    // (64, 3, 7) measured 0.2 us/layer slower than (64, 4, 5) in dense mode
     if (nmax <= 64) return launch_nmax<64, 4, 5>(maps, a, s);
     return launch_nmax<128, 3, 3>(maps, a, s);
 }

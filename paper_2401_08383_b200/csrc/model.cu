@@ -36,6 +36,7 @@ exf_status make_weight_tmap(CUtensorMap* map, const void* base, int64_t rows, in
 exf_status launch_ffn_gemm(const CUtensorMap& map, const CUtensorMap& mapB, const FfnArgs& a,
                            int nmax, int clusters, cudaStream_t s);
 exf_status make_gather_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols);
+exf_status make_tile_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
 exf_status plan_ffn_gemm(int nmax, int mode, int items, int K, int* ksplit, int* clusters);
 exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int nmax, cudaStream_t s);
 bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece>& pieces,
@@ -109,6 +110,7 @@ struct exf_model {
     __nv_bfloat16* b2 = nullptr;            // [L][E_loc][d]
     std::vector<CUtensorMap> tmap1, tmap2;  // per layer (weights, TMA tiles)
     CUtensorMap gmap_recv{}, gmap_h{};      // token rows for TMA gather4
+    CUtensorMap tmap_x[2]{}, tmap_ht{};     // dense fused mode: resident rows / H as B tiles
     // symmetric region
     Symm sym{};
     uint8_t* sym_base = nullptr;
@@ -138,6 +140,7 @@ struct exf_model {
     bool fused = true;
     bool dense = false;                     // fused, single GPU: dense over resident tokens
     int xpre = 0;                           // dense: pieces L2-prefetched before the PDL wait
+    int knob = 0;                           // tuning experiments (EXF_KNOB)
     int f_ctas = 148, f_tpc = 8, f_max_chunks = 1, f_nmax = 32, f_max_contrib = 1, f_max_pieces = 0;
     Piece* f_pieces = nullptr;              // stream-K schedule of the fused kernel
     int32_t* f_piece_off = nullptr;         // [ctas + 1]
@@ -385,6 +388,7 @@ FusedArgs fused_args(exf_model* m, int j) {
     a.b2 = m->b2 + (int64_t)j * m->E_loc * c.d_model;
     a.dense = m->dense ? 1 : 0;
     a.xpre = m->xpre;
+    a.knob = m->knob;
     a.res_x_out = m->res_x[(j + 1) & 1];
     a.res_meta_out = m->res_meta[(j + 1) & 1];
     a.n_res_out = m->n_res + ((j + 1) & 1);
@@ -408,7 +412,8 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
     switch (phase) {
         case 5: {  // fused layer kernel (gate..GEMM2 in one launch)
             if (j < 0 || j >= c.num_layers) return invalid("layer out of range");
-            const CUtensorMap maps[4] = {m->tmap1[j], m->tmap2[j], m->gmap_recv, m->gmap_h};
+            const CUtensorMap maps[4] = {m->tmap1[j], m->tmap2[j], m->dense ? m->tmap_x[j & 1] : m->gmap_recv,
+                                         m->dense ? m->tmap_ht : m->gmap_h};
             return launch_layer_fused(maps, fused_args(m, j), m->f_nmax, s);
         }
         case 0:
@@ -520,6 +525,7 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         m->dense = m->fused && c.world_size == 1 && m->f_tpc == 1;
         if (const char* env = std::getenv("EXF_DENSE")) m->dense = m->dense && std::atoi(env) != 0;
         if (const char* env = std::getenv("EXF_XPRE")) m->xpre = std::atoi(env);
+        if (const char* env = std::getenv("EXF_KNOB")) m->knob = std::atoi(env);
         const int tok = m->dense ? C : m->nmax;
         const int nmax_f = tok <= 32 ? 32 : (tok <= 64 ? 64 : 128);
         m->f_nmax = nmax_f;
@@ -545,13 +551,17 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         EXF_M(dalloc(&m->f_cta_cnt, (size_t)m->f_ctas * E));
     }
     if (std::getenv("EXF_FFN_TIMELINE")) {
-        EXF_M(dalloc(&m->tstamp, (size_t)5 * kTimelineCtas * 16));
+        EXF_M(dalloc(&m->tstamp, (size_t)6 * kTimelineCtas * 16));
         EXF_M(dalloc(&m->tl, (size_t)L * 3 * 8));
     }
     EXF_M(dalloc(&m->d_peers, (size_t)c.world_size));
     EXF_M(build_layout(m));
     EXF_M(make_gather_tmap(&m->gmap_recv, m->sym_base + m->sym.recv_x, 2LL * c.world_size * C, d));
     EXF_M(make_gather_tmap(&m->gmap_h, m->H, C, f));
+    if (m->dense) {
+        for (int i = 0; i < 2; ++i) EXF_M(make_tile_tmap(&m->tmap_x[i], m->res_x[i], C, d, m->f_nmax));
+        EXF_M(make_tile_tmap(&m->tmap_ht, m->H, C, f, m->f_nmax));
+    }
     if (cudaMemset(m->trace, 0xff, sizeof(int32_t) * C * L) != cudaSuccess) return fail(EXF_CUDA);
     EXF_M(init_weights(m));
     // split-K / persistent-cluster plan of the two-kernel (phased) path
@@ -813,7 +823,7 @@ exf_status exf_model_read_ffn_timeline(exf_model* m, uint64_t* h, int32_t ctas) 
     if (!m || !h || ctas < 1 || ctas > kTimelineCtas) return invalid("bad argument");
     if (!m->tstamp) return invalid("timeline not enabled (set EXF_FFN_TIMELINE=1 before create)");
     EXF_CUDA_TRY(cudaDeviceSynchronize());
-    for (int g = 0; g < 5; ++g)
+    for (int g = 0; g < 6; ++g)
         EXF_CUDA_TRY(cudaMemcpy(h + (int64_t)g * ctas * 16, m->tstamp + (int64_t)g * kTimelineCtas * 16,
                                 sizeof(uint64_t) * ctas * 16, cudaMemcpyDeviceToHost));
     return EXF_OK;

@@ -30,7 +30,7 @@ def main():
     s.synchronize()
     m.check()
     ctas = 4096
-    buf = np.zeros((5, ctas, 16), np.uint64)
+    buf = np.zeros((6, ctas, 16), np.uint64)
     _capi.call("exf_model_read_ffn_timeline", m.handle, buf.ctypes.data, ctas)
     for g, key in ((0, "gemm1"), (1, "gemm2")):
         n = plan[key]["clusters"] * plan[key]["ksplit"]

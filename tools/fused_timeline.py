@@ -39,7 +39,7 @@ def main():
         if rank != 0:
             return
     ctas = 148
-    buf = np.zeros((5, ctas, 16), np.uint64)
+    buf = np.zeros((6, ctas, 16), np.uint64)
     _capi.call("exf_model_read_ffn_timeline", m.handle, buf.ctypes.data, ctas)
     t = buf[0].astype(np.int64)
     t0 = t[:, 0].min()
@@ -69,9 +69,27 @@ def main():
     print("  rel. token-row producer start: rows ready %.2f, first stage issued %.2f, landed %.2f, MMA role entry "
           "%.2f, MMA saw it %.2f us" % tuple(np.median((v - b_start) / 1e3)
                                             for v in (t2[:, 9], t2[:, 1], t2[:, 2], t2[:, 3], mma_full_b)))
-    t4 = buf[4].astype(np.int64)
-    print("  token-row producer per-piece setup (start -> rows ready), median us, pieces 0..3:",
-          [round(float(np.median((t4[:, 2 * p + 1] - t4[:, 2 * p]) / 1e3)), 2) for p in range(4)])
+    if G == 1:  # dense: epilogue per job (accumulator ready -> done), by kind
+        t4 = buf[4]
+        for j in range(5):
+            st = t4[:, 2 * j].astype(np.int64)
+            en_raw = t4[:, 2 * j + 1]
+            ok = (st > 0) & (en_raw > 0)
+            if not ok.any():
+                break
+            kind = (en_raw >> np.uint64(62)).astype(np.int64)
+            en = (en_raw & np.uint64((1 << 62) - 1)).astype(np.int64)
+            mma_end = t[:, 3 + 2 * j]
+            for kd, nm in ((0, "direct"), (2, "finisher"), (1, "park")):
+                sel = ok & (kind == kd)
+                if sel.any():
+                    print(f"  epilogue job {j} {nm:8s} ctas {sel.sum():3d}: acc ready {np.median((st - mma_end)[sel]) / 1e3:5.2f} "
+                          f"after last MMA, duration median {np.median((en - st)[sel]) / 1e3:5.2f} max "
+                          f"{((en - st)[sel]).max() / 1e3:5.2f} us")
+    t5 = buf[5].astype(np.int64)
+    print("  token-row stage issue (emptyB passed) rel. job 0 first MMA, median us, it 0..15:",
+          [round(float(np.median((t5[:, i] - t[:, 2]) / 1e3)), 2) for i in range(16)])
+    print("  job 0 last MMA rel. its first: median %.2f" % np.median((t[:, 3] - t[:, 2]) / 1e3))
     its = np.maximum(t2[:, 7], 1)
     print(f"weight stage hold (MMA issue -> stage freed): median {np.median(t2[:, 4]):.0f} ns; "
           f"MMA warp blocked per stage on token rows {np.median(t2[:, 5] / its):.0f} ns, "
