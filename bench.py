@@ -310,6 +310,25 @@ def main():
         model.phase(PHASE_GATHER_SEND, 0, None, stream)
         model.phase(PHASE_GATHER_WAIT, 0, None, stream)
         stream.synchronize()
+    # in-stream launch duration: the L layer kernels back to back as in a
+    # decode step (each one's prologue overlapping its predecessor's tail via
+    # PDL), events on the launching stream around the run: mean interval
+    # between consecutive completions. The isolated per-launch events above
+    # (a sync between layers) add each launch's cold start.
+    stream_ms = []
+    if fused:
+        for _ in range(reps):
+            model.reset_stats()
+            model.phase(PHASE_BEGIN, 0, x_dev, stream)
+            e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            e0.record(stream)
+            for j in range(a.layers):
+                model.phase(PHASE_FUSED, j, None, stream)
+            e1.record(stream)
+            model.phase(PHASE_GATHER_SEND, 0, None, stream)
+            model.phase(PHASE_GATHER_WAIT, 0, None, stream)
+            stream.synchronize()
+            stream_ms.append(e0.elapsed_time(e1) / a.layers)
     model.check()
     r_local = model.routes()
     # algorithmic bytes of one FFN pair on this rank: weights of every local
@@ -323,7 +342,8 @@ def main():
         active = len(set(mine.tolist()))
         nt = len(mine)
         bytes_layers.append(active * (2 * d * f * 2 + (d + f) * 2) + nt * (2 * d + 4 * f + 4 * d))
-    ffn_avg_ms = statistics.mean(ffn_ms)
+    ffn_iso_ms = statistics.mean(ffn_ms)
+    ffn_avg_ms = statistics.mean(stream_ms) if stream_ms else ffn_iso_ms
     ffn_bytes = statistics.mean(bytes_layers)
     achieved = ffn_bytes / (ffn_avg_ms * 1e-3) / 1e9
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
@@ -366,6 +386,9 @@ def main():
                      "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
                      "bytes_per_launch": ffn_bytes, "ms_per_launch": ffn_avg_ms,
+                     "ms_per_launch_timing": ("in-stream: events around the L layer launches back to back, "
+                                              "mean interval" if stream_ms else "isolated per-launch events"),
+                     "ms_per_launch_isolated": ffn_iso_ms,
                      "bytes_model": "active local experts x (W1+W2+b1+b2) + tokens x (2d in, 4f H rw, 4d out)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                      "step_achieved_gbs": ffn_bytes * a.layers / (aff["ms_per_step"] * 1e-3) / 1e9,
