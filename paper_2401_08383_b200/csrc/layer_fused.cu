@@ -84,6 +84,11 @@ __device__ __forceinline__ int32_t atom_add_acq_rel(int32_t* p, int32_t v) {
     asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
     return old;
 }
+__device__ __forceinline__ int32_t atom_add_release(int32_t* p, int32_t v) {
+    int32_t old;
+    asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
 __device__ __forceinline__ void red_add_release(int32_t* p, int32_t v) {
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -1043,7 +1048,10 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     release_tmem();
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     if (et == 0) {
-                        const int prev = atom_add_acq_rel(a.item_ctr + slot, 1);  // release partials
+                        // release this piece's partials; only the last arriver
+                        // acquires (one load on the counter)
+                        const int prev = atom_add_release(a.item_ctr + slot, 1);
+                        if (prev == Sg - 1) (void)ld_acq_s32(a.item_ctr + slot);
                         s_flag = (prev == Sg - 1);
                         if (s_flag) a.item_ctr[slot] = 0;  // next use is a later launch
                     }
@@ -1285,23 +1293,31 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
     for (int g = 0; g < 2; ++g) psz[g] = std::max(kKPS, psz[g] / kKPS * kKPS);  // whole stages
     const int kk[2] = {k1, k2}, mts[2] = {mt1, mt2};
     constexpr double kSwitch = 1.0;   // per-piece pipeline cost, in k-blocks
-    constexpr double kReady = 6.0;    // GEMM1 epilogue + hdone + token-row load latency
+    double kReady = 6.0;              // GEMM1 epilogue + hdone + token-row load latency
+    if (const char* s = std::getenv("EXF_KREADY")) kReady = std::atof(s);
+    double kSw = kSwitch;
+    if (const char* s = std::getenv("EXF_KSWITCH")) kSw = std::atof(s);
     std::vector<double> free_at(ctas, 0.0), done1(E_loc, 0.0);
     std::vector<std::vector<Piece>> per(ctas);
     // EXF_FILL2=1: GEMM2 as a stream-K fill (below); measured slower at
     // configs[1] (48.3 vs 45.8 us/layer): long GEMM2 runs stall on hdone
     const bool fill2 = std::getenv("EXF_FILL2") != nullptr;
+    // EXF_TAIL=t: GEMM2 of the last t experts in half-size pieces, so the
+    // last round of pieces spreads over more CTAs
+    int tail = 0;
+    if (const char* s = std::getenv("EXF_TAIL")) tail = std::atoi(s);
     for (int g = 0; g < (fill2 ? 1 : 2); ++g) {
-        const int S = (kk[g] + psz[g] - 1) / psz[g];
-        for (int e = 0; e < E_loc; ++e)
+        for (int e = 0; e < E_loc; ++e) {
+            const int pz = (g == 1 && e >= E_loc - tail) ? std::max(kKPS, psz[g] / 2 / kKPS * kKPS) : psz[g];
+            const int S = (kk[g] + pz - 1) / pz;
             for (int mt = 0; mt < mts[g]; ++mt)
                 for (int s = 0; s < S; ++s) {
                     Piece p{};
                     p.g = (int16_t)g;
                     p.e = (int16_t)e;
                     p.mt = (int16_t)mt;
-                    p.kb0 = (int16_t)(s * psz[g]);
-                    p.nkb = (int16_t)std::min(psz[g], kk[g] - s * psz[g]);
+                    p.kb0 = (int16_t)(s * pz);
+                    p.nkb = (int16_t)std::min(pz, kk[g] - s * pz);
                     p.kidx = (int16_t)s;
                     p.S = (int16_t)S;
                     const double ready = g == 0 ? 0.0 : done1[e] + kReady;
@@ -1314,10 +1330,11 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
                             best = c;
                         }
                     }
-                    free_at[best] = best_start + p.nkb + kSwitch;
+                    free_at[best] = best_start + p.nkb + kSw;
                     if (g == 0) done1[e] = std::max(done1[e], free_at[best]);
                     per[best].push_back(p);
                 }
+        }
     }
     if (fill2) {
         // GEMM2 as a stream-K fill: CTAs in order of the time they finish
