@@ -183,10 +183,10 @@ def main():
         dist.all_reduce(t)
         return t.cpu().numpy()
 
-    def make_model(assign):
+    def make_model(assign, ep_mode=0):
         cfg = MoeModelConfig(num_experts=a.experts, num_layers=a.layers, d_model=a.d_model,
                              d_ffn=a.d_ffn, tokens_per_gpu=a.batch, world_size=n, rank=rank,
-                             seed=1234, gate_affinity=a.gate_affinity)
+                             seed=1234, gate_affinity=a.gate_affinity, ep_mode=ep_mode)
         m = MoeModel(cfg, assign)
         if n > 1:
             hs = [None] * n
@@ -260,6 +260,36 @@ def main():
                          "routed_fraction": frac}
         log(f"[bench] {name}: {ms:.3f} ms/step, {results[name]['value']:.0f} tok/s, "
             f"routed fraction {frac:.4f}")
+
+    # ---- the baseline ExFlow is measured against: vanilla expert parallelism
+    # (contiguous placement, dispatch + combine back home every layer: 2L
+    # exchanges per step instead of L + 1; proj/src/sim.cpp:60-64, :153-157)
+    vm = make_model(vanilla, ep_mode=1)
+    vm.capture(x_dev, stream)
+    for _ in range(a.warmup):
+        vm.replay(stream)
+    stream.synchronize()
+    vm.check()
+    vm.reset_stats()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(a.steps):
+        vm.replay(stream)
+    ev1.record(stream)
+    stream.synchronize()
+    vm.check()
+    ms_v = allmax(ev0.elapsed_time(ev1)) / a.steps
+    barrier()
+    crossed_v = allsum_i64(vm.crossed())
+    results_ep_vanilla = {"value": a.batch * n / (ms_v * 1e-3), "ms_per_step": ms_v,
+                          "routed_fraction": float(crossed_v.sum()) / (a.batch * n * a.layers * a.steps),
+                          "exchanges_per_step": 2 * a.layers + 1,
+                          "note": "vanilla EP: contiguous placement, outputs combined back to the home GPU "
+                                  "after every layer; routed_fraction = away-from-home token-layers"}
+    log(f"[bench] vanilla EP (2 exchanges/layer): {ms_v:.3f} ms/step, {results_ep_vanilla['value']:.0f} tok/s")
+    vm.close()
 
     # ---- e2e through the public API with host buffers (affinity placement)
     out_host = torch.empty(a.batch * n, a.d_model, dtype=torch.bfloat16).pin_memory()
@@ -375,6 +405,7 @@ def main():
         "config": dict(workload(a, n), launch_plan=plan),
         "routed_fraction": aff["routed_fraction"],
         "placements": results,
+        "ep_vanilla_2exchange": results_ep_vanilla,
         "g8_replay_routed_fraction": {"vanilla": rep_v8.p_star, "affinity": rep_a8.p_star,
                                       "note": "p_star of this run's routes replayed on a 1x8 "
                                               "topology (GPU replay kernel)"},

@@ -199,7 +199,12 @@ typedef struct { /* in the style of SynthConfig (proj/include/exflow/synth.hpp:1
     uint64_t seed;           /* weight-init seed */
     float init_std;          /* expert weight std (0.02) */
     float gate_affinity;     /* planted inter-layer gate correlation rho in [0,1] */
+    int32_t ep_mode;         /* EXF_EP_COHERENT (ExFlow: tokens stay on their expert's GPU,
+                                one exchange per layer) or EXF_EP_VANILLA (dispatch + combine
+                                back to the home GPU every layer, proj/src/sim.cpp:60-64) */
 } exf_model_config;
+#define EXF_EP_COHERENT 0
+#define EXF_EP_VANILLA 1
 
 /* assign: [L][E] placement table (exf_contiguous_placement = vanilla,
  * exf_solve_staged = affinity). Allocates weights (generated on device from
@@ -220,7 +225,9 @@ exf_status exf_model_step(exf_model* model, const void* d_x_in, exf_stream_t str
  * phase 0 begin(x_in) | 1 gate+dispatch(layer) | 2 ffn(layer) |
  * 5 fused layer (gate..GEMM2 in one launch; needs every rank's kernel to run
  * concurrently, i.e. one process or GPU per rank) |
- * 3 gather send | 4 gather wait. */
+ * 3 gather send | 4 gather wait |
+ * 6 combine send(layer) | 7 combine wait(layer) (ep_mode EXF_EP_VANILLA, after
+ * each layer: outputs back to the tokens' home ranks). */
 exf_status exf_model_step_phase(exf_model* model, int32_t phase, int32_t layer,
                                 const void* d_x_in, exf_stream_t stream);
 /* Device pointer to the [G*B][d] bf16 step output (token-id order). */

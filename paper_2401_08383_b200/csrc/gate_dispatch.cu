@@ -377,6 +377,72 @@ __global__ void gather_wait_kernel(uint8_t* own_sym, Symm sym, int G, uint64_t* 
     if (threadIdx.x == 0) *step = epoch;
 }
 
+// ------------------------------------------------------------------ vanilla-EP combine
+// Vanilla expert parallelism (the DeepSpeed-MoE-style baseline ExFlow is
+// compared against): after every layer each token's output row goes back to
+// its home rank (proj/src/sim.cpp:60-64: 2 hops per crossed token, dispatch +
+// combine; collective counts :153-157). Row of token t lands in slot t / G of
+// home rank t % G's combine buffer (double-buffered by layer parity), followed
+// by a per-slot release flag {epoch = step * L + layer + 1}: the home rank
+// needs no counts, it waits for its B slots.
+__global__ void __launch_bounds__(256) combine_send_kernel(
+    const __nv_bfloat16* __restrict__ res_x, const ResMeta* __restrict__ res_meta, const int32_t* n_res,
+    uint8_t* const* peers, Symm sym, int G, int B, int d, int L, int layer, const uint64_t* step,
+    int32_t* err) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    const int n = *n_res;
+    const uint64_t epoch = *step * (uint64_t)L + (uint64_t)layer + 1;
+    const int par = layer & 1;
+    const int vec = d >> 3;
+    for (int r = blockIdx.x * nwarp + warp; r < n; r += gridDim.x * nwarp) {
+        const ResMeta m = res_meta[r];
+        if ((unsigned)m.token >= (unsigned)(B * G)) {
+            if (lane == 0) atomicExch(err, ERR_CAPACITY);
+            continue;
+        }
+        const int home = m.token % G, slot = m.token / G;
+        uint8_t* base = peers[home];
+        int4* dst = reinterpret_cast<int4*>(base + sym.comb_x + ((int64_t)par * B + slot) * d * 2);
+        const int4* src = reinterpret_cast<const int4*>(res_x + (int64_t)r * d);
+        for (int v = lane; v < vec; v += 32) dst[v] = src[v];
+        if (lane == 0) reinterpret_cast<ResMeta*>(base + sym.comb_meta)[par * B + slot] = m;
+        __syncwarp();  // the warp's row stores precede lane 0's release
+        if (lane == 0) {
+            uint64_t* f = reinterpret_cast<uint64_t*>(base + sym.comb_flags) + par * B + slot;
+            if (G > 1) ptx::st_release_sys(f, epoch); else ptx::st_release_gpu_u64(f, epoch);
+        }
+    }
+}
+
+// Home side: wait for the B slots, then copy them (home order) into the
+// resident buffers the next layer reads.
+__global__ void __launch_bounds__(256) combine_wait_kernel(
+    const uint8_t* own_sym, Symm sym, int G, int B, int d, int L, int layer, const uint64_t* step,
+    __nv_bfloat16* res_x_next, ResMeta* res_meta_next, int32_t* n_res_next, int32_t* err) {
+    ptx::pdl_wait();
+    ptx::pdl_trigger();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    const uint64_t epoch = *step * (uint64_t)L + (uint64_t)layer + 1;
+    const int par = layer & 1;
+    const int vec = d >> 3;
+    for (int slot = blockIdx.x * nwarp + warp; slot < B; slot += gridDim.x * nwarp) {
+        const uint64_t* f = reinterpret_cast<const uint64_t*>(own_sym + sym.comb_flags) + par * B + slot;
+        if (lane == 0) {
+            ptx::SpinGuard g;
+            while (ptx::ld_relaxed_u64(f, G > 1) < epoch) g.step(err, ERR_TIMEOUT_GATHER);
+            (void)ptx::flag_read(f, G > 1);  // acquire on the flag itself
+        }
+        __syncwarp();
+        const int4* src = reinterpret_cast<const int4*>(own_sym + sym.comb_x + ((int64_t)par * B + slot) * d * 2);
+        int4* dst = reinterpret_cast<int4*>(res_x_next + (int64_t)slot * d);
+        for (int v = lane; v < vec; v += 32) dst[v] = src[v];
+        if (lane == 0) res_meta_next[slot] = reinterpret_cast<const ResMeta*>(own_sym + sym.comb_meta)[par * B + slot];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_res_next = B;
+}
+
 // ------------------------------------------------------------------ launchers
 // Tokens per CTA of gate_dispatch: the CTA stages its token rows (and, when
 // they fit, Wg) in shared memory; at most 128 CTAs so that all active CTAs
@@ -436,6 +502,22 @@ exf_status launch_gather_send(const __nv_bfloat16* res_x, const ResMeta* res_met
     const int blocks = std::max(1, std::min(132, (C * G + 15) / 16));
     EXF_CUDA_TRY(launch_pdl(gather_send_kernel, dim3(blocks), dim3(512), 0, s, 0, res_x, res_meta,
                             n_res, peers, sym, G, rank, d, C, step, done_ctr, err));
+    return EXF_OK;
+}
+
+exf_status launch_combine(const __nv_bfloat16* res_x_out, const ResMeta* res_meta_out, const int32_t* n_res_out,
+                          uint8_t* const* peers, uint8_t* own_sym, const Symm& sym, int G, int B, int d, int L,
+                          int layer, const uint64_t* step, __nv_bfloat16* res_x_next, ResMeta* res_meta_next,
+                          int32_t* n_res_next, int32_t* err, int part, cudaStream_t s) {
+    const int blocks = std::max(1, std::min(148, (B * G + 7) / 8));
+    if (part == 0) {
+        EXF_CUDA_TRY(launch_pdl(combine_send_kernel, dim3(blocks), dim3(256), 0, s, 0, res_x_out, res_meta_out,
+                                n_res_out, peers, sym, G, B, d, L, layer, step, err));
+        return EXF_OK;
+    }
+    EXF_CUDA_TRY(launch_pdl(combine_wait_kernel, dim3(std::max(1, std::min(148, (B + 7) / 8))), dim3(256), 0, s, 0,
+                            (const uint8_t*)own_sym, sym, G, B, d, L, layer, step, res_x_next, res_meta_next,
+                            n_res_next, err));
     return EXF_OK;
 }
 

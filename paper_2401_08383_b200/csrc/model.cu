@@ -29,6 +29,10 @@ exf_status launch_gather_send(const __nv_bfloat16* res_x, const ResMeta* res_met
                               const int32_t* n_res, uint8_t* const* peers, const Symm& sym, int G,
                               int rank, int d, int C, const uint64_t* step, int32_t* done_ctr,
                               int32_t* err, cudaStream_t s);
+exf_status launch_combine(const __nv_bfloat16* res_x_out, const ResMeta* res_meta_out, const int32_t* n_res_out,
+                          uint8_t* const* peers, uint8_t* own_sym, const Symm& sym, int G, int B, int d, int L,
+                          int layer, const uint64_t* step, __nv_bfloat16* res_x_next, ResMeta* res_meta_next,
+                          int32_t* n_res_next, int32_t* err, int part, cudaStream_t s);
 exf_status launch_gather_wait(uint8_t* own_sym, const Symm& sym, int G, uint64_t* step,
                               int32_t* err, cudaStream_t s);
 exf_status make_weight_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols);
@@ -180,6 +184,8 @@ exf_status validate_config(const exf_model_config& c) {
         return invalid("num_experts " + std::to_string(c.num_experts) + " not divisible by total GPUs " +
                        std::to_string(c.world_size));
     if (!(c.gate_affinity >= 0.f && c.gate_affinity <= 1.f)) return invalid("gate_affinity must be in [0,1]");
+    if (c.ep_mode != EXF_EP_COHERENT && c.ep_mode != EXF_EP_VANILLA)
+        return invalid("ep_mode must be EXF_EP_COHERENT (0) or EXF_EP_VANILLA (1)");
     {
         const int64_t C = (int64_t)c.tokens_per_gpu * c.world_size;
         if (C > 128LL * 256 || (int64_t)gate_dispatch_tpc((int)C) * (2 * c.d_model + 8) > 200 * 1024)
@@ -205,6 +211,10 @@ exf_status build_layout(exf_model* m) {
     m->sym.gather_x = take((int64_t)C * d * 2);
     m->sym.gflags = take((int64_t)G * 8);
     m->sym.cflags = take(2LL * G * std::max<int64_t>(C, kMaxCtas) * 8);  // route flags [2][G][max(C, 256)]
+    const int64_t B = c.tokens_per_gpu;
+    m->sym.comb_x = take(2LL * B * d * 2);
+    m->sym.comb_meta = take(2LL * B * (int64_t)sizeof(ResMeta));
+    m->sym.comb_flags = take(2LL * B * 8);
     m->sym.total = o;
     EXF_CUDA_TRY(cudaMalloc(&m->sym_base, (size_t)o));
     EXF_CUDA_TRY(cudaMemset(m->sym_base, 0, (size_t)o));
@@ -438,6 +448,15 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
         }
         case 4:
             return launch_gather_wait(m->sym_base, m->sym, c.world_size, m->step, m->err, s);
+        case 6:    // vanilla EP: layer j's outputs back to their home ranks (send)
+        case 7: {  // ... and the home side's wait + copy into the resident buffers
+            if (j < 0 || j >= c.num_layers) return invalid("layer out of range");
+            if (c.ep_mode != EXF_EP_VANILLA) return invalid("combine phases need ep_mode = EXF_EP_VANILLA");
+            const int o = (j + 1) & 1;
+            return launch_combine(m->res_x[o], m->res_meta[o], m->n_res + o, m->d_peers, m->sym_base, m->sym,
+                                  c.world_size, c.tokens_per_gpu, c.d_model, c.num_layers, j, m->step,
+                                  m->res_x[o], m->res_meta[o], m->n_res + o, m->err, phase - 6, s);
+        }
         default:
             return invalid("unknown phase");
     }
@@ -451,6 +470,10 @@ exf_status run_step(exf_model* m, const void* x_in, cudaStream_t s) {
         } else {
             EXF_TRY(run_phase(m, 1, j, nullptr, s));
             EXF_TRY(run_phase(m, 2, j, nullptr, s));
+        }
+        if (m->cfg.ep_mode == EXF_EP_VANILLA) {
+            EXF_TRY(run_phase(m, 6, j, nullptr, s));
+            EXF_TRY(run_phase(m, 7, j, nullptr, s));
         }
     }
     EXF_TRY(run_phase(m, 3, 0, nullptr, s));
@@ -801,8 +824,9 @@ exf_status exf_model_replay(exf_model* m, exf_stream_t stream) {
 
 int32_t exf_model_launches_per_step(exf_model* m) {
     if (!m) return 0;
-    // begin, L x (fused layer | gate_dispatch + GEMM1 + GEMM2), gather send + wait
-    return 1 + (m->fused ? 1 : 3) * m->cfg.num_layers + 2;
+    // begin, L x (fused layer | gate_dispatch + GEMM1 + GEMM2) [+ combine send + wait], gather send + wait
+    const int per_layer = (m->fused ? 1 : 3) + (m->cfg.ep_mode == EXF_EP_VANILLA ? 2 : 0);
+    return 1 + per_layer * m->cfg.num_layers + 2;
 }
 
 exf_status exf_model_read_step_timeline(exf_model* m, uint64_t* h, int32_t reset) {
@@ -833,7 +857,8 @@ exf_status exf_model_describe(exf_model* m, char* buf, int32_t len) {
     if (!m || !buf || len < 1) return invalid("bad argument");
     std::string s = "{\"token_tile\": " + std::to_string(m->nmax) +
                     ", \"experts_per_rank\": " + std::to_string(m->E_loc) +
-                    ", \"capacity_tokens\": " + std::to_string(m->C);
+                    ", \"capacity_tokens\": " + std::to_string(m->C) +
+                    ", \"ep_mode\": \"" + std::string(m->cfg.ep_mode == EXF_EP_VANILLA ? "vanilla" : "coherent") + "\"";
     if (m->fused)
         s += ", \"path\": \"fused\", \"layer_kernel\": {\"ctas\": " + std::to_string(m->f_ctas) +
              ", \"tokens_per_cta\": " + std::to_string(m->f_tpc) +

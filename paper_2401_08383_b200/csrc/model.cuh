@@ -37,7 +37,9 @@ struct ResMeta {
 };
 
 struct Symm {  // byte offsets inside the symmetric region
-    int64_t recv_x, recv_meta, recv_cnt, flags, gather_x, gflags, cflags, total;
+    int64_t recv_x, recv_meta, recv_cnt, flags, gather_x, gflags, cflags;
+    int64_t comb_x, comb_meta, comb_flags;  // vanilla-EP combine: [2 layer parity][B] home slots
+    int64_t total;
 };
 // fused layer kernel: per-(parity, src rank, src CTA) dispatch-complete flags
 constexpr int kMaxCtas = 256;

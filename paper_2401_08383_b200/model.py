@@ -15,7 +15,9 @@ import numpy as np
 
 from . import _capi
 
-PHASE_BEGIN, PHASE_DISPATCH, PHASE_FFN, PHASE_GATHER_SEND, PHASE_GATHER_WAIT, PHASE_FUSED = range(6)
+PHASE_BEGIN, PHASE_DISPATCH, PHASE_FFN, PHASE_GATHER_SEND, PHASE_GATHER_WAIT, PHASE_FUSED, \
+    PHASE_COMBINE_SEND, PHASE_COMBINE_WAIT = range(8)
+EP_COHERENT, EP_VANILLA = 0, 1  # include/exflow_c.h EXF_EP_*
 
 
 @dataclass
@@ -32,6 +34,9 @@ class MoeModelConfig:
     seed: int = 0
     init_std: float = 0.02
     gate_affinity: float = 0.0
+    # EP_COHERENT (ExFlow) or EP_VANILLA (dispatch + combine back home every
+    # layer, proj/src/sim.cpp:60-64)
+    ep_mode: int = 0
 
     @property
     def capacity(self) -> int:
@@ -44,7 +49,7 @@ class MoeModelConfig:
     def _c(self) -> _capi.ModelConfigC:
         return _capi.ModelConfigC(self.num_experts, self.num_layers, self.d_model, self.d_ffn,
                                   self.top_k, self.tokens_per_gpu, self.world_size, self.rank,
-                                  self.seed, self.init_std, self.gate_affinity)
+                                  self.seed, self.init_std, self.gate_affinity, self.ep_mode)
 
 
 def _stream_ptr(stream) -> Optional[int]:

@@ -29,6 +29,7 @@ def main():
     p.add_argument("--d-ffn", type=int, default=512)
     p.add_argument("--batch", type=int, default=16)
     p.add_argument("--phased", action="store_true")
+    p.add_argument("--vanilla", action="store_true", help="vanilla EP: combine back home every layer")
     p.add_argument("--steps", type=int, default=2)
     a = p.parse_args()
 
@@ -36,7 +37,8 @@ def main():
     import torch.distributed as dist
     from paper_2401_08383_b200 import dist as xd, placement as pl
     from paper_2401_08383_b200.affinity import Topology
-    from paper_2401_08383_b200.model import (PHASE_BEGIN, PHASE_DISPATCH, PHASE_FFN, PHASE_FUSED,
+    from paper_2401_08383_b200.model import (EP_COHERENT, EP_VANILLA, PHASE_BEGIN, PHASE_COMBINE_SEND,
+                                             PHASE_COMBINE_WAIT, PHASE_DISPATCH, PHASE_FFN, PHASE_FUSED,
                                              PHASE_GATHER_SEND, PHASE_GATHER_WAIT, MoeModel,
                                              MoeModelConfig)
     rank = int(os.environ["RANK"])
@@ -46,7 +48,8 @@ def main():
     E, L = a.experts, a.layers
     assign = pl.random_placement(E, L, Topology(1, G), seed=7)
     cfg = MoeModelConfig(num_experts=E, num_layers=L, d_model=a.d_model, d_ffn=a.d_ffn,
-                         tokens_per_gpu=a.batch, world_size=G, rank=rank, seed=99, gate_affinity=0.6)
+                         tokens_per_gpu=a.batch, world_size=G, rank=rank, seed=99, gate_affinity=0.6,
+                         ep_mode=EP_VANILLA if a.vanilla else EP_COHERENT)
     m = MoeModel(cfg, assign)
     m.connect(xd.exchange_handles(m.ipc_handle()))
     fused = m.describe().get("path") == "fused" and not a.phased
@@ -112,6 +115,23 @@ def main():
                         err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
                         assert err <= REL_TOL, f"layer {j} token {want_tok[k]} rel err {err}"
             dist.barrier()
+            if a.vanilla:  # outputs back to the home ranks, exact copies in home order
+                m.phase(PHASE_COMBINE_SEND, j)
+                m.phase(PHASE_COMBINE_WAIT, j)
+                torch.cuda.synchronize()
+                home = gather(m.resident((j + 1) % 2))
+                if rank == 0:
+                    row_of = {}
+                    for xa, meta_a in after:
+                        for k in range(len(meta_a)):
+                            row_of[int(meta_a[k, 0])] = (xa[k], int(meta_a[k, 1]))
+                    for r in range(G):
+                        xh, meta_h = home[r]
+                        assert (meta_h[:, 0] == cfg.home_tokens(r)).all(), f"layer {j} rank {r}: combine order"
+                        for k, t in enumerate(meta_h[:, 0]):
+                            assert np.array_equal(xh[k], row_of[int(t)][0]), f"layer {j} token {t}: combine row"
+                            assert meta_h[k, 1] == row_of[int(t)][1]
+                dist.barrier()
         final = m.resident(L % 2)
         m.phase(PHASE_GATHER_SEND)
         m.phase(PHASE_GATHER_WAIT)
@@ -131,11 +151,16 @@ def main():
             assert (routes >= 0).all()
             c = sum(crossed)
             assert (c == moves).all(), f"crossed {c} != moves {moves}"
-            rep = co.orc.simulate(routes, assign, 1, G, co.orc.COHERENT)
-            assert int(c.sum()) == rep.coherent_moves
+            if a.vanilla:
+                rep = co.orc.simulate(routes, assign, 1, G, co.orc.VANILLA)
+                assert int(c.sum()) == rep.away_from_home_events
+            else:
+                rep = co.orc.simulate(routes, assign, 1, G, co.orc.COHERENT)
+                assert int(c.sum()) == rep.coherent_moves
             want, _ = co.orc.count_transitions(routes, E)
             assert np.array_equal(sum(hists), want)
-            print(f"[mgpu] step {step}: G={G} {'fused' if fused else 'two-kernel'} path OK "
+            print(f"[mgpu] step {step}: G={G} {'fused' if fused else 'two-kernel'} path "
+                  f"{'vanilla' if a.vanilla else 'coherent'} OK "
                   f"(crossed {int(c.sum())} of {a.batch * G * L} token-layers)", flush=True)
         dist.barrier()
     m.close()

@@ -63,10 +63,14 @@ def _union_routes(models):
 
 def run_checked(torch, models, xs, assign, ffn_samples=48, seed=0, forced=None, fused=False):
     """Lock-step phased run with per-layer oracle checks; returns final routes.
-    fused=True drives the one-launch-per-layer kernel (layer_fused.cu)."""
-    from paper_2401_08383_b200.model import (PHASE_BEGIN, PHASE_DISPATCH, PHASE_FFN, PHASE_FUSED,
+    fused=True drives the one-launch-per-layer kernel (layer_fused.cu). With
+    ep_mode EP_VANILLA every layer is followed by the combine (outputs back to
+    the home ranks), checked as an exact copy in home order."""
+    from paper_2401_08383_b200.model import (EP_VANILLA, PHASE_BEGIN, PHASE_COMBINE_SEND,
+                                             PHASE_COMBINE_WAIT, PHASE_DISPATCH, PHASE_FFN, PHASE_FUSED,
                                              PHASE_GATHER_SEND, PHASE_GATHER_WAIT)
     cfg = models[0].config
+    vanilla = cfg.ep_mode == EP_VANILLA
     G, L, E = cfg.world_size, cfg.num_layers, cfg.num_experts
     rng = np.random.default_rng(seed)
     for m in models:
@@ -128,6 +132,23 @@ def run_checked(torch, models, xs, assign, ffn_samples=48, seed=0, forced=None, 
                 budget = 5e-2 * np.linalg.norm(ref - xin) + 2.0 ** -8 * np.linalg.norm(ref)
                 assert np.linalg.norm(got - ref) <= budget, \
                     f"layer {j} token {want_tok[k]} FFN-delta error above budget"
+        if vanilla:
+            # combine: every token's row back to slot t / G of home rank t % G
+            for m in models:
+                m.phase(PHASE_COMBINE_SEND, j)
+            for m in models:
+                m.phase(PHASE_COMBINE_WAIT, j)
+            row_of = {}
+            for p_rank in range(G):
+                xa, meta_a = after[p_rank]
+                for k in range(len(meta_a)):
+                    row_of[int(meta_a[k, 0])] = (xa[k], int(meta_a[k, 1]))
+            for r in range(G):
+                xh, meta_h = models[r].resident((j + 1) % 2)
+                assert (meta_h[:, 0] == cfg.home_tokens(r)).all(), f"combine order layer {j} rank {r}"
+                for k, t in enumerate(meta_h[:, 0]):
+                    assert np.array_equal(xh[k], row_of[int(t)][0]), f"combine row layer {j} token {t}"
+                    assert meta_h[k, 1] == row_of[int(t)][1]
     final = [m.resident(L % 2) for m in models]
     for m in models:
         m.phase(PHASE_GATHER_SEND)
@@ -144,11 +165,16 @@ def run_checked(torch, models, xs, assign, ffn_samples=48, seed=0, forced=None, 
         assert np.array_equal(outs[0][meta[:, 0]], xf)
     routes = _union_routes(models)
     assert (routes >= 0).all()
-    # crossed counters == coherent moves of the replay on the emitted trace
+    # crossed counters == coherent moves (vanilla: away-from-home events) of
+    # the replay on the emitted trace
     crossed = sum(m.crossed() for m in models)
     assert (crossed == moves).all()
-    rep = co.orc.simulate(routes, assign, 1, G, co.orc.COHERENT)
-    assert int(crossed.sum()) == rep.coherent_moves
+    if vanilla:
+        rep = co.orc.simulate(routes, assign, 1, G, co.orc.VANILLA)
+        assert int(crossed.sum()) == rep.away_from_home_events
+    else:
+        rep = co.orc.simulate(routes, assign, 1, G, co.orc.COHERENT)
+        assert int(crossed.sum()) == rep.coherent_moves
     # fused histogram == count_transitions of the emitted trace (bit-exact)
     hist = sum(m.affinity_counts() for m in models)
     want, _ = co.orc.count_transitions(routes, E)
@@ -290,3 +316,27 @@ def test_model_rejects_bad_configs(torch_cuda, orc):
     bad = assign.copy()
     with pytest.raises(_capi.ExflowInvalidArgument):
         _models(2, bad, num_experts=8, num_layers=4, d_model=256, d_ffn=256, tokens_per_gpu=8)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_vanilla_ep_lockstep(torch_cuda, orc, G):
+    # vanilla expert parallelism (dispatch + combine back home every layer,
+    # proj/src/sim.cpp:60-64): same routes and FFN math, tokens at home after
+    # every layer, crossed counters == simulate(VANILLA) away-from-home events
+    from paper_2401_08383_b200.model import EP_VANILLA
+    E, L = 8, 3
+    assign = orc.random_placement(E, L, G, 11)
+    models = _models(G, assign, num_experts=E, num_layers=L, d_model=256, d_ffn=512,
+                     tokens_per_gpu=24, seed=5, gate_affinity=0.8, ep_mode=EP_VANILLA)
+    xs = _inputs(torch_cuda, models, 40 + G)
+    run_checked(torch_cuda, models, xs, assign, ffn_samples=16)
+
+
+def test_vanilla_ep_single_device_fused(torch_cuda, orc):
+    from paper_2401_08383_b200.model import EP_VANILLA
+    E, L, B = 8, 3, 64
+    assign = orc.contiguous_placement(E, L, 1)
+    models = _models(1, assign, num_experts=E, num_layers=L, d_model=1024, d_ffn=4096,
+                     tokens_per_gpu=B, seed=9, gate_affinity=0.8, ep_mode=EP_VANILLA)
+    xs = _inputs(torch_cuda, models, 77)
+    run_checked(torch_cuda, models, xs, assign, ffn_samples=8, fused=True)
