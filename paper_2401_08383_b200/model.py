@@ -140,6 +140,14 @@ class MoeModel:
         _capi.call("exf_model_read_routes", self._h, out.ctypes.data)
         return out
 
+    def save_trace(self, path) -> None:
+        """Emit the routes of the last step as an EXFLOW-TRACE v1 file (the
+        format the reference CLI reads, proj/src/trace.cpp:152-168). Rows are
+        token ids; with G > 1 merge every rank's routes first (dist.merge_routes)
+        and use traceio.save_trace directly."""
+        from . import traceio
+        traceio.save_trace(path, self.routes(), self.config.num_experts)
+
     def crossed(self) -> np.ndarray:
         out = np.empty(self.config.num_layers, np.int64)
         _capi.call("exf_model_read_crossed", self._h, out.ctypes.data)

@@ -340,3 +340,27 @@ def test_vanilla_ep_single_device_fused(torch_cuda, orc):
                      tokens_per_gpu=B, seed=9, gate_affinity=0.8, ep_mode=EP_VANILLA)
     xs = _inputs(torch_cuda, models, 77)
     run_checked(torch_cuda, models, xs, assign, ffn_samples=8, fused=True)
+
+
+def test_emitted_trace_round_trip(torch_cuda, orc, tmp_path):
+    # a GPU run's routes saved as EXFLOW-TRACE v1 and read back reproduce the
+    # run's fused histogram (count_transitions) and crossed counters (simulate)
+    from paper_2401_08383_b200 import traceio
+    E, L, B = 8, 4, 64
+    assign = orc.contiguous_placement(E, L, 1)
+    models = _models(1, assign, num_experts=E, num_layers=L, d_model=512, d_ffn=2048,
+                     tokens_per_gpu=B, seed=21, gate_affinity=0.8)
+    m = models[0]
+    xs = _inputs(torch_cuda, models, 5)
+    m.reset_stats()
+    m.step(xs[0])
+    torch_cuda.cuda.synchronize()
+    m.check()
+    f = tmp_path / "run.trace"
+    m.save_trace(f)
+    paths, e = traceio.load_trace(f)
+    assert e == E and np.array_equal(paths, m.routes())
+    want, _ = orc.count_transitions(paths, E)
+    assert np.array_equal(m.affinity_counts(), want)
+    rep = orc.simulate(paths, assign, 1, 1, orc.COHERENT)
+    assert int(m.crossed().sum()) == rep.coherent_moves
