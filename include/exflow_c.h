@@ -254,6 +254,17 @@ exf_status exf_model_check(exf_model* model);
 exf_status exf_model_read_expert(exf_model* model, int32_t layer, int32_t expert, uint16_t* h_w1,
                                  uint16_t* h_b1, uint16_t* h_w2, uint16_t* h_b2);
 exf_status exf_model_read_gate(exf_model* model, int32_t layer, uint16_t* h_wg /* [E][d] */);
+/* Expert migration (online placement change): device
+ * pointers of local weight slot `slot` of `layer` (W1 [d_ffn][d], b1, W2
+ * [d][d_ffn], b2, bf16; slot k holds the k-th expert of this rank in expert
+ * order), so a caller can move weights between ranks (NCCL send/recv or
+ * peer copies) into the slots of a new placement, then install the new
+ * table with exf_model_set_placement on every rank (validated like
+ * Placement::validate, proj/src/placement.cpp:434-470; between steps only;
+ * captured graphs stay valid: the tables are updated in place). */
+exf_status exf_model_expert_storage(exf_model* model, int32_t layer, int32_t slot, void** d_w1,
+                                    void** d_b1, void** d_w2, void** d_b2);
+exf_status exf_model_set_placement(exf_model* model, const int32_t* h_assign /* [L][E] */);
 /* Resident tokens of buffer `which` (layer j reads buffer j%2 and writes
  * (j+1)%2): h_x [n][d] bf16 bits, h_meta [n][2] int32 {token, prev_expert},
  * *n_out = n. Buffers must hold G*B rows. Synchronous (tests/diagnostics). */

@@ -113,6 +113,8 @@ SIGNATURES = {
     "exf_model_describe": (C.c_int, [_VP, _VP, _I32]),
     "exf_model_read_ffn_timeline": (C.c_int, [_VP, _VP, _I32]),
     "exf_debug_last_timeout": (C.c_int32, [_VP]),
+    "exf_model_expert_storage": (C.c_int, [_VP, _I32, _I32, _VP, _VP, _VP, _VP]),
+    "exf_model_set_placement": (C.c_int, [_VP, _VP]),
     "exf_model_read_step_timeline": (C.c_int, [_VP, _VP, _I32]),
 }
 

@@ -768,6 +768,27 @@ exf_status exf_model_read_expert(exf_model* m, int32_t layer, int32_t expert, ui
     return EXF_OK;
 }
 
+exf_status exf_model_expert_storage(exf_model* m, int32_t layer, int32_t slot, void** d_w1, void** d_b1,
+                                    void** d_w2, void** d_b2) {
+    if (!m || !d_w1 || !d_b1 || !d_w2 || !d_b2) return invalid("null argument");
+    const auto& c = m->cfg;
+    if (layer < 0 || layer >= c.num_layers || slot < 0 || slot >= m->E_loc)
+        return invalid("layer/slot out of range");
+    const int64_t ls = (int64_t)layer * m->E_loc + slot;
+    const int64_t d = c.d_model, f = c.d_ffn;
+    *d_w1 = m->w1 + ls * f * d;
+    *d_b1 = m->b1 + ls * f;
+    *d_w2 = m->w2 + ls * d * f;
+    *d_b2 = m->b2 + ls * d;
+    return EXF_OK;
+}
+
+exf_status exf_model_set_placement(exf_model* m, const int32_t* h_assign) {
+    if (!m || !h_assign) return invalid("null argument");
+    EXF_CUDA_TRY(cudaDeviceSynchronize());  // no step may be in flight
+    return set_placement(m, h_assign);
+}
+
 exf_status exf_model_read_gate(exf_model* m, int32_t layer, uint16_t* h_wg) {
     if (!m || !h_wg) return invalid("null argument");
     if (layer < 0 || layer >= m->cfg.num_layers) return invalid("layer out of range");

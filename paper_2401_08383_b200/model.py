@@ -181,6 +181,26 @@ class MoeModel:
                    b1.ctypes.data, w2.ctypes.data, b2.ctypes.data)
         return w1, b1, w2, b2
 
+    def expert_storage(self, layer: int, slot: int):
+        """torch int16 (bf16 bits) views of local weight slot `slot` of `layer`:
+        (W1 [d_ffn][d], b1 [d_ffn], W2 [d][d_ffn], b2 [d]) -- device memory of
+        this model, for expert migration (migrate.py)."""
+        import torch
+        cfg = self.config
+        ptrs = [C.c_void_p() for _ in range(4)]
+        _capi.call("exf_model_expert_storage", self._h, layer, slot, *[C.byref(p) for p in ptrs])
+        shapes = [(cfg.d_ffn, cfg.d_model), (cfg.d_ffn,), (cfg.d_model, cfg.d_ffn), (cfg.d_model,)]
+        return tuple(torch.as_tensor(_CudaArray(p.value, sh), device="cuda") for p, sh in zip(ptrs, shapes))
+
+    def set_placement(self, assign: np.ndarray) -> None:
+        """Install a new [L][E] placement (same table on every rank, weights
+        already in their new slots: see migrate.py)."""
+        a = np.ascontiguousarray(assign, dtype=np.int32)
+        if a.shape != (self.config.num_layers, self.config.num_experts):
+            raise _capi.ExflowInvalidArgument("placement must be [L][E]")
+        _capi.call("exf_model_set_placement", self._h, a.ctypes.data)
+        self.assign = a
+
     def gate_weights(self, layer: int) -> np.ndarray:
         cfg = self.config
         wg = np.empty((cfg.num_experts, cfg.d_model), np.uint16)

@@ -30,6 +30,9 @@ def main():
     p.add_argument("--batch", type=int, default=16)
     p.add_argument("--phased", action="store_true")
     p.add_argument("--vanilla", action="store_true", help="vanilla EP: combine back home every layer")
+    p.add_argument("--migrate", action="store_true",
+                   help="start from the contiguous placement and migrate the experts (NCCL) to the "
+                        "random one before the checked steps")
     p.add_argument("--steps", type=int, default=2)
     a = p.parse_args()
 
@@ -50,8 +53,26 @@ def main():
     cfg = MoeModelConfig(num_experts=E, num_layers=L, d_model=a.d_model, d_ffn=a.d_ffn,
                          tokens_per_gpu=a.batch, world_size=G, rank=rank, seed=99, gate_affinity=0.6,
                          ep_mode=EP_VANILLA if a.vanilla else EP_COHERENT)
-    m = MoeModel(cfg, assign)
-    m.connect(xd.exchange_handles(m.ipc_handle()))
+    if a.migrate:
+        from paper_2401_08383_b200 import migrate
+        m = MoeModel(cfg, pl.contiguous_placement(E, L, Topology(1, G)))
+        m.connect(xd.exchange_handles(m.ipc_handle()))
+        nccl = dist.new_group(backend="nccl")
+        moved = migrate.migrate_nccl(m, assign, group=nccl)
+        # the migrated slots hold exactly what a model built on the new
+        # placement generates for them
+        ref = MoeModel(cfg, assign)
+        for j in range(L):
+            for e in range(E):
+                if assign[j][e] == rank:
+                    got, want = m.expert_weights(j, e), ref.expert_weights(j, e)
+                    assert all(np.array_equal(x, y) for x, y in zip(got, want)), f"layer {j} expert {e}"
+        ref.close()
+        if rank == 0:
+            print(f"[mgpu] migrated {moved} experts over NCCL", flush=True)
+    else:
+        m = MoeModel(cfg, assign)
+        m.connect(xd.exchange_handles(m.ipc_handle()))
     fused = m.describe().get("path") == "fused" and not a.phased
     g = torch.Generator().manual_seed(1000 + rank)
     rng = np.random.default_rng(0)

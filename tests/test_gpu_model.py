@@ -364,3 +364,44 @@ def test_emitted_trace_round_trip(torch_cuda, orc, tmp_path):
     assert np.array_equal(m.affinity_counts(), want)
     rep = orc.simulate(paths, assign, 1, 1, orc.COHERENT)
     assert int(m.crossed().sum()) == rep.coherent_moves
+
+
+def test_expert_migration_local(torch_cuda, orc):
+    # online placement change (histogram -> solver -> migration): after
+    # migrate_local every rank's slots hold exactly the weights a model built
+    # on the new placement has, and a decode step matches it bit for bit
+    from paper_2401_08383_b200 import migrate
+    from paper_2401_08383_b200.model import (PHASE_BEGIN, PHASE_DISPATCH, PHASE_FFN,
+                                             PHASE_GATHER_SEND, PHASE_GATHER_WAIT)
+    E, L, G = 8, 3, 2
+    p0 = orc.contiguous_placement(E, L, G)
+    p1 = orc.random_placement(E, L, G, 5)
+    kw = dict(num_experts=E, num_layers=L, d_model=256, d_ffn=512, tokens_per_gpu=16, seed=13,
+              gate_affinity=0.7)
+    models = _models(G, p0, **kw)
+    fresh = _models(G, p1, **kw)
+    moved = migrate.migrate_local(models, p1)
+    assert moved == sum(int((p0[j] != p1[j]).sum()) for j in range(L))
+    for j in range(L):
+        for e in range(E):
+            g = int(p1[j][e])
+            got, want = models[g].expert_weights(j, e), fresh[g].expert_weights(j, e)
+            assert all(np.array_equal(a, b) for a, b in zip(got, want)), f"layer {j} expert {e}"
+    xs = _inputs(torch_cuda, models, 3)
+    outs = []
+    for ms in (models, fresh):
+        for r, m in enumerate(ms):
+            m.phase(PHASE_BEGIN, 0, xs[r])
+        for j in range(L):
+            for m in ms:
+                m.phase(PHASE_DISPATCH, j)
+            for m in ms:
+                m.phase(PHASE_FFN, j)
+        for m in ms:
+            m.phase(PHASE_GATHER_SEND)
+        for m in ms:
+            m.phase(PHASE_GATHER_WAIT)
+        for m in ms:
+            m.check()
+        outs.append((_bf16_bits(ms[0].output()), _union_routes(ms)))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])

@@ -19,16 +19,19 @@ def _gpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("phased,vanilla", [(False, False), (True, False), (False, True)])
-def test_two_gpu_parity(phased, vanilla):
+@pytest.mark.parametrize("phased,vanilla,migrate", [(False, False, False), (True, False, False),
+                                                    (False, True, False), (False, False, True)])
+def test_two_gpu_parity(phased, vanilla, migrate):
     n = _gpus()
     if n < 2:
         pytest.skip("needs two GPUs")
-    port = "29631" if phased else ("29635" if vanilla else "29633")
+    port = "29631" if phased else ("29635" if vanilla else ("29637" if migrate else "29633"))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", port,
            os.path.join(HERE, "mgpu_worker.py")] + (["--phased"] if phased else []) + \
-        (["--vanilla"] if vanilla else [])
+        (["--vanilla"] if vanilla else []) + (["--migrate"] if migrate else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert " OK " in r.stdout
+    if migrate:
+        assert "migrated" in r.stdout
