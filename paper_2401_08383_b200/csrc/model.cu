@@ -422,6 +422,9 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
     switch (phase) {
         case 5: {  // fused layer kernel (gate..GEMM2 in one launch)
             if (j < 0 || j >= c.num_layers) return invalid("layer out of range");
+            if (!m->fused)
+                return invalid("the fused layer kernel is not available for this configuration "
+                               "(describe()[\"path\"] is the two-kernel path)");
             const CUtensorMap maps[4] = {m->tmap1[j], m->tmap2[j], m->dense ? m->tmap_x[j & 1] : m->gmap_recv,
                                          m->dense ? m->tmap_ht : m->gmap_h};
             return launch_layer_fused(maps, fused_args(m, j), m->f_nmax, s);

@@ -109,7 +109,7 @@ struct Piece {
     int16_t g, e, mt, kb0;
     int16_t nkb, kidx, S, pad;
 };
-constexpr int kMaxPieces = 16;  // per CTA
+constexpr int kMaxPieces = 64;  // per CTA (static smem: 1 KB)
 
 // Arguments of the fused per-layer kernel (layer_fused.cu).
 struct FusedArgs {

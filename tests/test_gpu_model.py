@@ -194,7 +194,11 @@ def test_tiny_config_single_device(torch_cuda, orc):
 FUSED_CONFIGS = [(8, 4, 512, 2048, 256), (8, 4, 1024, 4096, 64), (16, 3, 256, 512, 8),
                  (64, 3, 1024, 1024, 96), (32, 2, 2048, 2048, 48),
                  # > 4 jobs per CTA: TMEM accumulator buffers wrap around
-                 (8, 2, 1024, 8192, 64), (16, 2, 1024, 4096, 64)]
+                 (8, 2, 1024, 8192, 64), (16, 2, 1024, 4096, 64),
+                 # BASELINE configs[3] (1.3B: E=32, d=2048, d_ffn=4d) at the largest
+                 # decode batch of its sweep (B=512 > #SMs: dispatch path, 4 tokens
+                 # per CTA) and configs[4] (E=64, d=1024, d_ffn=4d)
+                 (32, 2, 2048, 8192, 512), (64, 2, 1024, 4096, 64)]
 
 
 @pytest.mark.parametrize("E,L,d,dff,B", FUSED_CONFIGS)
