@@ -1287,7 +1287,11 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
     const int k1 = d / kBK, k2 = dff / kBK, mt1 = dff / kBM, mt2 = d / kBM;
     // measured at configs[1]: (16, 16) 45.9 us/layer; (16, 8) 53.2, (16, 12) 49.8,
     // (16, 32) 50.9, (8, 8) 65.2: per-piece costs exceed the model's estimate
-    int psz[2] = {16, 16};
+    // GEMM1 pieces are whole tiles up to 32 k-blocks (d <= 2048): split-K
+    // GEMM1 tiles cost a partial park + finisher reduction over every token
+    // column (d=2048, E=32, 64 tokens: 525 -> 338 us/layer dense, 300 -> 295
+    // dispatch)
+    int psz[2] = {std::min(k1, 32), 16};
     if (const char* s = std::getenv("EXF_PIECE1")) psz[0] = std::atoi(s);
     if (const char* s = std::getenv("EXF_PIECE2")) psz[1] = std::atoi(s);
     for (int g = 0; g < 2; ++g) psz[g] = std::max(kKPS, psz[g] / kKPS * kKPS);  // whole stages

@@ -548,7 +548,14 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         if (m->f_tpc > 32 || d > 2048 || E > 64 || (int64_t)c.world_size * C > 4096) m->fused = false;
         // single GPU: every expert is local, so the layer runs dense over all
         // resident tokens and the token phase leaves the GEMMs' critical path
-        m->dense = m->fused && c.world_size == 1 && m->f_tpc == 1;
+        // (measured at N=1, tokens 64: dense wins while a layer's weights are
+        // small -- E=8/16/32 at d=1024: 28.0/43.6/80.1 vs 33.8/51.7/87.7
+        // us/layer -- and loses once they are large: dense GEMM1 streams every
+        // expert's W1 even for experts without tokens and its fixed saving
+        // (no token phase) matters less: E=64 d=1024 152.7 vs 134.1, E=32
+        // d=2048 338 vs 295)
+        const double layer_weight_bytes = (double)m->E_loc * 4.0 * d * f;
+        m->dense = m->fused && c.world_size == 1 && m->f_tpc == 1 && layer_weight_bytes <= 0.8e9;
         if (const char* env = std::getenv("EXF_DENSE")) m->dense = m->dense && std::atoi(env) != 0;
         if (const char* env = std::getenv("EXF_XPRE")) m->xpre = std::atoi(env);
         if (const char* env = std::getenv("EXF_KNOB")) m->knob = std::atoi(env);

@@ -15,15 +15,17 @@ def main():
     p.add_argument("--batch", type=int, default=64)
     p.add_argument("--experts", type=int, default=8)
     p.add_argument("--layers", type=int, default=24)
+    p.add_argument("--d-model", type=int, default=1024)
+    p.add_argument("--d-ffn", type=int, default=4096)
     a = p.parse_args()
     import torch
     from paper_2401_08383_b200 import placement as pl
     from paper_2401_08383_b200.affinity import Topology
     from paper_2401_08383_b200.model import MoeModel, MoeModelConfig
-    cfg = MoeModelConfig(num_experts=a.experts, num_layers=a.layers, d_model=1024, d_ffn=4096,
+    cfg = MoeModelConfig(num_experts=a.experts, num_layers=a.layers, d_model=a.d_model, d_ffn=a.d_ffn,
                          tokens_per_gpu=a.batch, seed=1234, gate_affinity=0.8)
     m = MoeModel(cfg, pl.contiguous_placement(a.experts, a.layers, Topology(1, 1)))
-    x = torch.randn(a.batch, 1024).to(torch.bfloat16).cuda()
+    x = torch.randn(a.batch, a.d_model).to(torch.bfloat16).cuda()
     s = torch.cuda.Stream()
     for _ in range(3):
         m.step(x, s)
@@ -40,7 +42,10 @@ def main():
     m.check()
     us = e0.elapsed_time(e1) * 1000.0 / a.reps
     knobs = {k: v for k, v in os.environ.items() if k.startswith("EXF_")}
-    print(f"step {us:.1f} us  ({us / a.layers:.2f} us/layer, {a.batch / us * 1e6:.0f} tok/s)  {knobs}")
+    wbytes = a.experts * 2 * a.d_model * a.d_ffn * 2  # every expert active (weights dominate)
+    print(f"step {us:.1f} us  ({us / a.layers:.2f} us/layer, {a.batch / us * 1e6:.0f} tok/s, "
+          f"weights {wbytes / (us / a.layers * 1e-6) / 1e12:.2f} TB/s, {m.describe().get('path')}"
+          f"{' dense' if m.describe().get('layer_kernel', {}).get('dense') else ''})  {knobs}")
 
 
 if __name__ == "__main__":
