@@ -516,6 +516,8 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         for (int k = tid; k < K; k += kThreads) {
             ptx::SpinGuard g;
             uint64_t v;
+            // (a poll back-off, which helped the dense route flags, measured
+            // no gain here at N=4: the flags arrive late, they are not polled late)
             while (((v = ptx::ld_relaxed_u64(f + k, sys)) >> 40) != e24) g.step(a.err, 112);
             // acquire once, on the flag itself (orders this slot's row + meta;
             // bar.sync below extends it to the CTA)
