@@ -667,7 +667,9 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     }
                     if (ts3 && lane == 0 && it == 0) ts3[10] = ptx::globaltimer();
                     ptx::tc_fence_after();
-                    ptx::fence_proxy_async_smem();  // cp.async (generic) rows -> tensor-core reads
+                    // cp.async (generic-proxy) rows -> tensor-core reads; dense-mode
+                    // rows arrive by TMA (async proxy): no fence
+                    if (!DENSE) ptx::fence_proxy_async_smem();
                     if (lane == 0) {
 #pragma unroll
                         for (int j = 0; j < kKPS; ++j) {
