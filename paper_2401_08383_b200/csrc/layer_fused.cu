@@ -209,8 +209,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // [2] gate done, [3] ranks done, [4] barrier passed, [5] dispatch stored,
     // [6] completion done, [7] flags seen / tables built, [15] exit
     uint64_t* ts3 = ts ? ts + (int64_t)(2 + (a.layer & 1)) * 4096 * 16 : nullptr;
-    // dense: [2j], [2j+1] epilogue job j got its accumulator / finished (j < 8);
-    // dispatch path: [8 + g] flags of source g all seen
+    // dense: [2j], [2j+1] epilogue job j got its accumulator / finished (j < 8)
     uint64_t* ts4 = ts ? ts + (int64_t)4 * 4096 * 16 : nullptr;
     uint64_t* ts5 = ts ? ts + (int64_t)5 * 4096 * 16 : nullptr;  // B stage it < 16 issued (emptyB passed)
     auto mark3 = [&](int k) {

@@ -144,7 +144,6 @@ struct exf_model {
     bool fused = true;
     bool dense = false;                     // fused, single GPU: dense over resident tokens
     int xpre = 0;                           // dense: pieces L2-prefetched before the PDL wait
-    int knob = 0;                           // tuning experiments (EXF_KNOB)
     int f_ctas = 148, f_tpc = 8, f_max_chunks = 1, f_nmax = 32, f_max_contrib = 1, f_max_pieces = 0;
     Piece* f_pieces = nullptr;              // stream-K schedule of the fused kernel
     int32_t* f_piece_off = nullptr;         // [ctas + 1]
@@ -398,7 +397,6 @@ FusedArgs fused_args(exf_model* m, int j) {
     a.b2 = m->b2 + (int64_t)j * m->E_loc * c.d_model;
     a.dense = m->dense ? 1 : 0;
     a.xpre = m->xpre;
-    a.knob = m->knob;
     a.res_x_out = m->res_x[(j + 1) & 1];
     a.res_meta_out = m->res_meta[(j + 1) & 1];
     a.n_res_out = m->n_res + ((j + 1) & 1);
@@ -558,7 +556,6 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         m->dense = m->fused && c.world_size == 1 && m->f_tpc == 1 && layer_weight_bytes <= 0.8e9;
         if (const char* env = std::getenv("EXF_DENSE")) m->dense = m->dense && std::atoi(env) != 0;
         if (const char* env = std::getenv("EXF_XPRE")) m->xpre = std::atoi(env);
-        if (const char* env = std::getenv("EXF_KNOB")) m->knob = std::atoi(env);
         const int tok = m->dense ? C : m->nmax;
         const int nmax_f = tok <= 32 ? 32 : (tok <= 64 ? 64 : 128);
         m->f_nmax = nmax_f;

@@ -152,7 +152,6 @@ struct FusedArgs {
     // epilogue keeps routed rows only, GEMM2 runs on the compact H
     int32_t dense;
     int32_t xpre;  // dense: pieces whose weights are L2-prefetched before the PDL wait
-    int32_t knob;  // tuning experiments (EXF_KNOB); no kernel reads it by default
     unsigned long long* tl;
     uint64_t* tstamp;    // optional per-CTA stamps [grid][16] (diagnostics)
 };

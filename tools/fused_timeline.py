@@ -130,11 +130,6 @@ def main():
               f" | B start {(cur[c, 8] - z) / 1e3:6.2f} fullB {(cur[c, 9] - z) / 1e3:6.2f} "
               f"fullA {(cur[c, 10] - z) / 1e3:6.2f} mma {(t[c, 2] - z) / 1e3:6.2f}")
     print(f"  exit       min {(cur[:, 15] - z).min() / 1e3:7.2f} max {(cur[:, 15] - z).max() / 1e3:7.2f}")
-    if G > 1:
-        t4b = buf[4].astype(np.int64)
-        print("  dispatch flags of source rank g all seen (median over CTAs, rel. prev exit):",
-              [round(float(np.median((t4b[:, 8 + g] - z) / 1e3)), 2) for g in range(min(G, 8))],
-              "; own completion median %.2f" % np.median((cur[:, 6] - z) / 1e3))
     ok = t[:, 12] > 0
     print(f"job 1 first A TMA issued {(rel[:, 12] - rel[:, 3])[ok].mean():.2f} us after job 0's last MMA; "
           f"first B gather {(rel[:, 13] - rel[:, 3])[ok].mean():.2f}; job 1 first MMA "
