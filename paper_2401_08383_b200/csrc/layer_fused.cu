@@ -275,7 +275,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         }
         // dense: the rest of the first pieces into L2 while the previous layer
         // drains (its tail leaves HBM bandwidth idle)
-        for (int p = 0; DENSE && p < min(npc, a.xpre); ++p) {
+        for (int p = 0; p < min(npc, a.xpre); ++p) {
             const Piece q = s_pc[p];
             const CUtensorMap* tq = q.g == 0 ? &tmA1 : &tmA2;
             const int rq = q.g == 0 ? a.dff : a.d;
