@@ -35,3 +35,17 @@ def test_two_gpu_parity(phased, vanilla, migrate):
     assert " OK " in r.stdout
     if migrate:
         assert "migrated" in r.stdout
+
+
+@pytest.mark.parametrize("vanilla", [False, True])
+def test_four_gpu_parity(vanilla):
+    # G=4: 2 experts per GPU at E=8, every layer checked against the oracle
+    n = _gpus()
+    if n < 4:
+        pytest.skip("needs four GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "4",
+           "--master-addr", "127.0.0.1", "--master-port", "29645" if vanilla else "29643",
+           os.path.join(HERE, "mgpu_worker.py"), "--batch", "32"] + (["--vanilla"] if vanilla else [])
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert " OK " in r.stdout
