@@ -1,29 +1,34 @@
 // layer_fused.cu -- one MoE layer of the context-coherent decode step as ONE
-// persistent sm_100a kernel (one CTA per SM):
+// persistent sm_100a kernel (one CTA per SM, 8 warps):
 //
-//   token phase (all warps of all CTAs)
+//   token phase
 //     (1) gate GEMM + softmax/top-1 (fixed-order fp32, bit-exact with the
 //         oracle), fused affinity histogram and trace emission;
-//     (2) atomic-free stable bucketing by (dest GPU, local slot): per-CTA
-//         warp-aggregated ranks, one grid barrier, prefix over CTAs;
-//     (3) ExFlow's single dispatch exchange: rows stored straight into the
-//         destination rank's receive region (P2P over NVLink), last CTA
-//         publishes counts and release-flags every destination;
-//   expert phase (warp-specialised roles)
-//     (4) grouped expert FFN, GEMM1 then GEMM2, as uniform split-K "pieces"
-//         (item = expert x 128-row tile, k-range = kbp 64-wide blocks)
-//         statically round-robined over the CTAs: TMA weight tiles (A),
-//         TMA gather4 token rows (B), tcgen05.mma into double-buffered TMEM,
-//         epilogue either finishes the tile (1 piece) or parks an fp32 partial
-//         in a workspace slot; the last-arriving piece of a tile sums the
-//         partials in k order (deterministic) and applies bias+GELU (GEMM1)
-//         or bias, gate-prob scale and residual (GEMM2). GEMM2 pieces of an
-//         expert start once all its GEMM1 tiles are complete (per-expert
-//         counters; every CTA runs its GEMM1 pieces first and all CTAs are
-//         co-resident, so the wait always resolves).
+//     dense mode (one GPU, C <= #SMs): CTA t gates token t while GEMM1 already
+//         runs over all resident tokens; the route travels as one 64-bit flag
+//         {epoch | slot | prob} and every CTA builds the canonical (slot,
+//         resident order) tables itself;
+//     dispatch path (G > 1 or C > #SMs): (2)+(3) ExFlow's single dispatch
+//         exchange: each token row is stored straight into slot (source, t) of
+//         its destination's receive region (P2P over NVLink) and every slot
+//         gets a per-slot route flag at every destination; each CTA derives
+//         the canonical (slot, source, order) lists from the G*C flags (no
+//         grid barrier, no count prefix, one exchange round);
+//   expert phase (warp-specialised: w0 weight TMA, w1 MMA issuer, w2 token-row
+//   producer, w4-7 epilogue; w3 the dense token warp)
+//     (4) grouped expert FFN, GEMM1 then GEMM2, as "pieces" (expert x 128-row
+//         tile x k-range) placed per CTA by a host greedy list scheduler:
+//         weights by TMA (2 k-blocks per 32 KB stage), token rows by TMA tile
+//         boxes (dense) or cp.async (dispatch path), tcgen05.mma into TMEM
+//         accumulator buffers; the epilogue finishes a whole-K piece directly
+//         or parks an fp32 partial, the last-arriving piece of a tile summing
+//         the partials in k order (deterministic), with bias+GELU (GEMM1) or
+//         bias, gate-prob scale and residual (GEMM2). GEMM2 pieces of an
+//         expert wait for its GEMM1 tiles (per-expert counters; a CTA's GEMM1
+//         pieces precede its GEMM2 pieces and all CTAs are co-resident).
 // Weights do not depend on the previous layer: the first weight stages are
-// prefetched before griddepcontrol.wait (PDL), overlapping the previous
-// kernel's tail. One launch per layer replaces gate/dispatch/GEMM1/GEMM2.
+// prefetched before griddepcontrol.wait (PDL); in dense mode only the warps
+// that read the previous layer's output wait at all. One launch per layer.
 #include "common.cuh"
 #include "model.cuh"
 #include "ptx.cuh"
