@@ -294,6 +294,25 @@ int32_t exf_debug_last_timeout(int32_t* out12);
  * phase marks 4..7] ([L][3][8] u64); reset != 0 re-arms the timeline. */
 exf_status exf_model_read_step_timeline(exf_model* model, uint64_t* h_stamps, int32_t reset);
 
+/* ------------------------------------------------------------------------
+ * Coherent decode attention over the replicated context cache (SURVEY §8(f)
+ * rank 1). No reference code: the protocol is PAPER.md:180-184 and the
+ * per-step context AllGather it relies on is counted at proj/src/sim.cpp:
+ * 161-162. Every GPU holds the whole K/V cache, so a token the dispatch left
+ * on this GPU attends over its own sequence's rows here (no combine).
+ *   d_q   [N][H][Dh] bf16     d_seq [N] int32 sequence id of each token
+ *   d_ctx_len [S] int32 (<= C) d_k, d_v [S][H][C][Dh] bf16 (head-major)
+ *   d_out [N][H][Dh] bf16 = softmax(scale * q k^T) v over keys < ctx_len;
+ *   an empty context gives 0. Dh in {64, 128}. fp32 scores/softmax/accum.
+ * d_workspace: exf_coherent_attention_workspace_bytes(N, H, Dh, C) bytes
+ * (0 -> may be NULL). Deterministic (fixed merge order).
+ * ---------------------------------------------------------------------- */
+int64_t exf_coherent_attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh, int32_t C);
+exf_status exf_coherent_attention(const void* d_q, const int32_t* d_seq, const int32_t* d_ctx_len,
+                                  const void* d_k, const void* d_v, int64_t N, int32_t S,
+                                  int32_t H, int32_t Dh, int32_t C, float scale,
+                                  void* d_workspace, void* d_out, exf_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

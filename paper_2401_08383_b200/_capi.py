@@ -116,6 +116,9 @@ SIGNATURES = {
     "exf_model_expert_storage": (C.c_int, [_VP, _I32, _I32, _VP, _VP, _VP, _VP]),
     "exf_model_set_placement": (C.c_int, [_VP, _VP]),
     "exf_model_read_step_timeline": (C.c_int, [_VP, _VP, _I32]),
+    "exf_coherent_attention_workspace_bytes": (_I64, [_I64, _I32, _I32, _I32]),
+    "exf_coherent_attention": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _I64, _I32, _I32, _I32, _I32,
+                                         C.c_float, _VP, _VP, _VP]),
 }
 
 

@@ -1,0 +1,47 @@
+"""Coherent decode attention over the replicated context cache (host side of
+exf_coherent_attention, include/exflow_c.h). SURVEY §8(f) rank 1.
+
+No CPU fallback: the call goes through libexflow_b200.so or raises. torch is
+plumbing only (device buffers, the current stream).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _capi
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def coherent_attention(q: torch.Tensor, seq: torch.Tensor, ctx_len: torch.Tensor,
+                       k: torch.Tensor, v: torch.Tensor, scale: float | None = None,
+                       out: torch.Tensor | None = None,
+                       workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """q [N][H][Dh] bf16, seq [N] int32, ctx_len [S] int32, k/v [S][H][C][Dh]
+    bf16 (all on the same CUDA device) -> out [N][H][Dh] bf16."""
+    N, H, Dh = q.shape
+    S, Hk, Cap, Dk = k.shape
+    if (Hk, Dk) != (H, Dh) or v.shape != k.shape:
+        raise _capi.ExflowInvalidArgument("coherent_attention: q/k/v shape mismatch")
+    for t in (q, k, v):
+        if t.dtype != torch.bfloat16 or not t.is_contiguous():
+            raise _capi.ExflowInvalidArgument("coherent_attention: contiguous bf16 q/k/v required")
+    if seq.dtype != torch.int32 or ctx_len.dtype != torch.int32:
+        raise _capi.ExflowInvalidArgument("coherent_attention: int32 seq/ctx_len required")
+    if scale is None:
+        scale = Dh ** -0.5
+    if out is None:
+        out = torch.empty_like(q)
+    lib = _capi.load()
+    ws_bytes = lib.exf_coherent_attention_workspace_bytes(N, H, Dh, Cap)
+    if ws_bytes and (workspace is None or workspace.numel() * workspace.element_size() < ws_bytes):
+        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
+    stream = torch.cuda.current_stream(q.device).cuda_stream
+    _capi.call("exf_coherent_attention", _ptr(q), _ptr(seq), _ptr(ctx_len), _ptr(k), _ptr(v),
+               N, S, H, Dh, Cap, C.c_float(scale), _ptr(workspace) if ws_bytes else None,
+               _ptr(out), C.c_void_p(stream))
+    return out

@@ -1,0 +1,258 @@
+// attention.cu -- coherent decode attention over the replicated context cache
+// (SURVEY.md §8(f) rank 1).
+//
+// ExFlow drops the combine Alltoall because every GPU holds the whole context
+// (one AllGather per step, proj/src/sim.cpp:161-162; protocol PAPER.md:180-184):
+// a token that the dispatch left on GPU X attends over ITS OWN sequence's K/V
+// rows in X's replica. The kernel therefore takes a per-token sequence id
+// (tokens arrive in dispatch order, not sequence order).
+//
+// Layouts (row-major, bf16):
+//   q     [N][H][Dh]       one decode query per resident token
+//   seq   [N] int32        sequence (context row) of each token
+//   ctx   [S] int32        valid context length of each sequence (<= C)
+//   k, v  [S][H][C][Dh]    head-major so one (sequence, head) is one contiguous
+//                          C*Dh*2-byte stream
+//   out   [N][H][Dh]
+// HBM-bound (AI ~ 1 flop/B): every K/V byte is read once, 16 B per lane,
+// a lane group of Dh/8 lanes per key, 4 keys in flight per group. Long
+// contexts are split across CTAs (flash-decoding) so the grid covers the
+// 148 SMs several times; the partial (m, l, acc) are merged by a second
+// kernel in split order (deterministic).
+#include "common.cuh"
+
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+namespace exf {
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float2 t = __bfloat1622float2(h[i]);
+        f[2 * i] = t.x;
+        f[2 * i + 1] = t.y;
+    }
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// grid (H, N, splits). Partial results go to ws (splits > 1) or straight to out.
+template <int Dh>
+__global__ void __launch_bounds__(kThreads) coherent_attn_kernel(
+    const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ seq,
+    const int32_t* __restrict__ ctx, const __nv_bfloat16* __restrict__ k,
+    const __nv_bfloat16* __restrict__ v, int32_t H, int32_t C, int32_t chunk, float scale_log2,
+    float* __restrict__ ws, __nv_bfloat16* __restrict__ out) {
+    constexpr int LPK = Dh / 8;                  // lanes per key
+    constexpr int GROUPS = kThreads / LPK;       // keys in flight per CTA step
+    const int h = blockIdx.x, n = blockIdx.y, split = blockIdx.z, splits = gridDim.z;
+    const int s = seq[n];
+    const int len = ctx[s];
+    const int lane_in = threadIdx.x % LPK, grp = threadIdx.x / LPK;
+    const int k_begin = split * chunk;
+    const int k_end = min(len, k_begin + chunk);
+
+    float qf[8];
+    bf16x8_to_f32(reinterpret_cast<const uint4*>(q + ((size_t)n * H + h) * Dh)[lane_in], qf);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) qf[i] *= scale_log2;
+
+    const size_t base = ((size_t)s * H + h) * (size_t)C * Dh;
+    const uint4* kp = reinterpret_cast<const uint4*>(k + base) + lane_in;
+    const uint4* vp = reinterpret_cast<const uint4*>(v + base) + lane_in;
+
+    float m = -CUDART_INF_F, l = 0.f, acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+
+    for (int key0 = k_begin + grp; key0 < k_end; key0 += GROUPS * kUnroll) {
+        uint4 kr[kUnroll], vr[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int key = key0 + u * GROUPS;
+            if (key < k_end) {
+                kr[u] = ld_stream(kp + (size_t)key * LPK);
+                vr[u] = ld_stream(vp + (size_t)key * LPK);
+            }
+        }
+        float sc[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            float kf[8];
+            bf16x8_to_f32(kr[u], kf);
+            float d = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) d = fmaf(qf[i], kf[i], d);
+#pragma unroll
+            for (int o = LPK / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            sc[u] = (key0 + u * GROUPS < k_end) ? d : -CUDART_INF_F;
+        }
+        float mx = m;
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) mx = fmaxf(mx, sc[u]);
+        const float corr = exp2f(m - mx);  // m = -inf, mx finite -> 0
+        l *= corr;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] *= corr;
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (key0 + u * GROUPS < k_end) {
+                const float p = exp2f(sc[u] - mx);
+                l += p;
+                float vf[8];
+                bf16x8_to_f32(vr[u], vf);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[i] = fmaf(p, vf[i], acc[i]);
+            }
+        }
+        m = mx;
+    }
+
+    // merge the GROUPS lane groups of this CTA (fixed order -> deterministic)
+    __shared__ float s_m[GROUPS], s_l[GROUPS];
+    __shared__ float s_acc[GROUPS][Dh];
+    if (lane_in == 0) {
+        s_m[grp] = m;
+        s_l[grp] = l;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s_acc[grp][lane_in * 8 + i] = acc[i];
+    __syncthreads();
+    if (threadIdx.x < Dh) {
+        const int c = threadIdx.x;
+        float M = -CUDART_INF_F;
+        for (int g = 0; g < GROUPS; ++g) M = fmaxf(M, s_m[g]);
+        float L = 0.f, A = 0.f;
+        if (M != -CUDART_INF_F) {
+            for (int g = 0; g < GROUPS; ++g) {
+                const float w = exp2f(s_m[g] - M);
+                L += s_l[g] * w;
+                A += s_acc[g][c] * w;
+            }
+        }
+        const size_t nh = (size_t)n * H + h;
+        if (splits == 1) {
+            out[nh * Dh + c] = __float2bfloat16(L > 0.f ? A / L : 0.f);
+        } else {
+            float* p = ws + (nh * splits + split) * (Dh + 2);
+            p[2 + c] = A;
+            if (c == 0) {
+                p[0] = M;
+                p[1] = L;
+            }
+        }
+    }
+}
+
+// grid (H, N), Dh threads: merge the splits in split order.
+template <int Dh>
+__global__ void __launch_bounds__(Dh) coherent_attn_merge_kernel(const float* __restrict__ ws,
+                                                                 int32_t H, int32_t splits,
+                                                                 __nv_bfloat16* __restrict__ out) {
+    const size_t nh = (size_t)blockIdx.y * H + blockIdx.x;
+    const float* p = ws + nh * splits * (Dh + 2);
+    const int c = threadIdx.x;
+    float M = -CUDART_INF_F;
+    for (int s = 0; s < splits; ++s) M = fmaxf(M, p[s * (Dh + 2)]);
+    float L = 0.f, A = 0.f;
+    if (M != -CUDART_INF_F) {
+        for (int s = 0; s < splits; ++s) {
+            const float* ps = p + s * (Dh + 2);
+            const float w = exp2f(ps[0] - M);
+            L += ps[1] * w;
+            A += ps[2 + c] * w;
+        }
+    }
+    out[nh * Dh + c] = __float2bfloat16(L > 0.f ? A / L : 0.f);
+}
+
+int attn_splits(int64_t N, int32_t H, int32_t C) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t heads = N * (int64_t)H;
+    const int64_t target = (int64_t)sms * 8;  // ~8 resident 128-thread CTAs per SM
+    int64_t splits = (target + heads - 1) / heads;
+    const int64_t max_splits = (C + 255) / 256;  // at least 256 keys per split
+    if (splits > max_splits) splits = max_splits;
+    if (splits < 1) splits = 1;
+    return (int)splits;
+}
+
+}  // namespace
+}  // namespace exf
+
+extern "C" int64_t exf_coherent_attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh,
+                                                          int32_t C) {
+    if (N <= 0 || H <= 0 || Dh <= 0 || C <= 0) return 0;
+    int splits = exf::attn_splits(N, H, C);
+    cudaGetLastError();
+    if (splits <= 1) return 0;
+    return N * (int64_t)H * splits * (Dh + 2) * (int64_t)sizeof(float);
+}
+
+extern "C" exf_status exf_coherent_attention(const void* d_q, const int32_t* d_seq,
+                                             const int32_t* d_ctx_len, const void* d_k,
+                                             const void* d_v, int64_t N, int32_t S, int32_t H,
+                                             int32_t Dh, int32_t C, float scale,
+                                             void* d_workspace, void* d_out,
+                                             exf_stream_t stream) {
+    using namespace exf;
+    if (N < 0 || S <= 0 || H <= 0 || C <= 0) {
+        set_error("coherent_attention: N >= 0, S, H, C > 0 required");
+        return EXF_INVALID;
+    }
+    if (Dh != 64 && Dh != 128) {
+        set_error("coherent_attention: head dim " + std::to_string(Dh) + " unsupported (64, 128)");
+        return EXF_INVALID;
+    }
+    if (N > 65535) {
+        set_error("coherent_attention: at most 65535 tokens per call");
+        return EXF_INVALID;
+    }
+    if (N == 0) return EXF_OK;
+    if (!d_q || !d_seq || !d_ctx_len || !d_k || !d_v || !d_out) {
+        set_error("coherent_attention: null buffer");
+        return EXF_INVALID;
+    }
+    const int splits = attn_splits(N, H, C);
+    if (splits > 1 && !d_workspace) {
+        set_error("coherent_attention: workspace required (exf_coherent_attention_workspace_bytes)");
+        return EXF_INVALID;
+    }
+    const int chunk = ((C + splits - 1) / splits + 63) / 64 * 64;
+    const float scale_log2 = scale * 1.4426950408889634f;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const dim3 grid(H, (unsigned)N, splits);
+    auto q = static_cast<const __nv_bfloat16*>(d_q);
+    auto k = static_cast<const __nv_bfloat16*>(d_k);
+    auto v = static_cast<const __nv_bfloat16*>(d_v);
+    auto o = static_cast<__nv_bfloat16*>(d_out);
+    auto ws = static_cast<float*>(d_workspace);
+    if (Dh == 64) {
+        coherent_attn_kernel<64><<<grid, kThreads, 0, st>>>(q, d_seq, d_ctx_len, k, v, H, C, chunk,
+                                                            scale_log2, ws, o);
+        if (splits > 1)
+            coherent_attn_merge_kernel<64><<<dim3(H, (unsigned)N), 64, 0, st>>>(ws, H, splits, o);
+    } else {
+        coherent_attn_kernel<128><<<grid, kThreads, 0, st>>>(q, d_seq, d_ctx_len, k, v, H, C,
+                                                             chunk, scale_log2, ws, o);
+        if (splits > 1)
+            coherent_attn_merge_kernel<128><<<dim3(H, (unsigned)N), 128, 0, st>>>(ws, H, splits, o);
+    }
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return cuda_status(err, "coherent_attention launch");
+    return EXF_OK;
+}
