@@ -17,8 +17,8 @@
 // HBM-bound (AI ~ 1 flop/B): every K/V byte is read once, 16 B per lane,
 // a lane group of Dh/8 lanes per key, 4 keys in flight per group. Long
 // contexts are split across CTAs (flash-decoding) so the grid covers the
-// 148 SMs several times; the partial (m, l, acc) are merged by a second
-// kernel in split order (deterministic).
+// 148 SMs in one wave; the last CTA of each (token, head) to arrive merges
+// the partial (m, l, acc) in split order (deterministic, no second launch).
 #include "common.cuh"
 
 #include <cuda_bf16.h>
@@ -77,11 +77,16 @@ __global__ void __launch_bounds__(kThreads) coherent_attn_kernel(
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = 0.f;
 
-    for (int key0 = k_begin + grp; key0 < k_end; key0 += GROUPS * kUnroll) {
+    // CTA-uniform trip count: the lane groups of a warp share the shuffles
+    // below, so keys past k_end are masked rather than skipped
+    for (int kb = k_begin; kb < k_end; kb += GROUPS * kUnroll) {
+        const int key0 = kb + grp;
         uint4 kr[kUnroll], vr[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             const int key = key0 + u * GROUPS;
+            kr[u] = make_uint4(0, 0, 0, 0);
+            vr[u] = make_uint4(0, 0, 0, 0);
             if (key < k_end) {
                 kr[u] = ld_stream(kp + (size_t)key * LPK);
                 vr[u] = ld_stream(vp + (size_t)key * LPK);
@@ -102,7 +107,8 @@ __global__ void __launch_bounds__(kThreads) coherent_attn_kernel(
         float mx = m;
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) mx = fmaxf(mx, sc[u]);
-        const float corr = exp2f(m - mx);  // m = -inf, mx finite -> 0
+        // no valid key for this group yet (mx = -inf): keep the state as is
+        const float corr = (mx == -CUDART_INF_F) ? 1.f : exp2f(m - mx);  // m = -inf -> 0
         l *= corr;
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] *= corr;
@@ -154,28 +160,35 @@ __global__ void __launch_bounds__(kThreads) coherent_attn_kernel(
             }
         }
     }
-}
-
-// grid (H, N), Dh threads: merge the splits in split order.
-template <int Dh>
-__global__ void __launch_bounds__(Dh) coherent_attn_merge_kernel(const float* __restrict__ ws,
-                                                                 int32_t H, int32_t splits,
-                                                                 __nv_bfloat16* __restrict__ out) {
-    const size_t nh = (size_t)blockIdx.y * H + blockIdx.x;
-    const float* p = ws + nh * splits * (Dh + 2);
-    const int c = threadIdx.x;
-    float M = -CUDART_INF_F;
-    for (int s = 0; s < splits; ++s) M = fmaxf(M, p[s * (Dh + 2)]);
-    float L = 0.f, A = 0.f;
-    if (M != -CUDART_INF_F) {
-        for (int s = 0; s < splits; ++s) {
-            const float* ps = p + s * (Dh + 2);
-            const float w = exp2f(ps[0] - M);
-            L += ps[1] * w;
-            A += ps[2 + c] * w;
+    if (splits == 1) return;
+    // the last CTA of this (token, head) to finish merges all splits, in split
+    // order (deterministic); the arrival counter is reset for the next call
+    __shared__ int s_last;
+    unsigned int* counters = reinterpret_cast<unsigned int*>(ws + (size_t)gridDim.y * H * splits * (Dh + 2));
+    const size_t nh = (size_t)n * H + h;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&counters[nh], 1u) == (unsigned)(splits - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x < Dh) {
+        const int c = threadIdx.x;
+        const float* p = ws + nh * splits * (Dh + 2);
+        float M = -CUDART_INF_F;
+        for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, __ldcg(p + sp * (Dh + 2)));
+        float L = 0.f, A = 0.f;
+        if (M != -CUDART_INF_F) {
+            for (int sp = 0; sp < splits; ++sp) {
+                const float* ps = p + sp * (Dh + 2);
+                const float w = exp2f(__ldcg(ps) - M);
+                L += __ldcg(ps + 1) * w;
+                A += __ldcg(ps + 2 + c) * w;
+            }
         }
+        out[nh * Dh + c] = __float2bfloat16(L > 0.f ? A / L : 0.f);
+        if (c == 0) counters[nh] = 0u;
     }
-    out[nh * Dh + c] = __float2bfloat16(L > 0.f ? A / L : 0.f);
 }
 
 int attn_splits(int64_t N, int32_t H, int32_t C) {
@@ -184,7 +197,7 @@ int attn_splits(int64_t N, int32_t H, int32_t C) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t heads = N * (int64_t)H;
     const int64_t target = (int64_t)sms * 8;  // ~8 resident 128-thread CTAs per SM
-    int64_t splits = (target + heads - 1) / heads;
+    int64_t splits = target / heads;  // round down: one full wave, no tail
     const int64_t max_splits = (C + 255) / 256;  // at least 256 keys per split
     if (splits > max_splits) splits = max_splits;
     if (splits < 1) splits = 1;
@@ -200,7 +213,7 @@ extern "C" int64_t exf_coherent_attention_workspace_bytes(int64_t N, int32_t H, 
     int splits = exf::attn_splits(N, H, C);
     cudaGetLastError();
     if (splits <= 1) return 0;
-    return N * (int64_t)H * splits * (Dh + 2) * (int64_t)sizeof(float);
+    return N * (int64_t)H * ((int64_t)splits * (Dh + 2) * (int64_t)sizeof(float) + 4);
 }
 
 extern "C" exf_status exf_coherent_attention(const void* d_q, const int32_t* d_seq,
@@ -244,13 +257,9 @@ extern "C" exf_status exf_coherent_attention(const void* d_q, const int32_t* d_s
     if (Dh == 64) {
         coherent_attn_kernel<64><<<grid, kThreads, 0, st>>>(q, d_seq, d_ctx_len, k, v, H, C, chunk,
                                                             scale_log2, ws, o);
-        if (splits > 1)
-            coherent_attn_merge_kernel<64><<<dim3(H, (unsigned)N), 64, 0, st>>>(ws, H, splits, o);
     } else {
         coherent_attn_kernel<128><<<grid, kThreads, 0, st>>>(q, d_seq, d_ctx_len, k, v, H, C,
                                                              chunk, scale_log2, ws, o);
-        if (splits > 1)
-            coherent_attn_merge_kernel<128><<<dim3(H, (unsigned)N), 128, 0, st>>>(ws, H, splits, o);
     }
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_status(err, "coherent_attention launch");
