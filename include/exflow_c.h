@@ -315,6 +315,21 @@ exf_status exf_coherent_attention(const void* d_q, const int32_t* d_seq, const i
                                   int32_t H, int32_t Dh, int32_t C, float scale,
                                   void* d_workspace, void* d_out, exf_stream_t stream);
 
+/* Per-step K/V append into every replica of the context cache (the data the
+ * context AllGather moves, proj/src/sim.cpp:161-162). For each token n (one
+ * token per sequence per call): pos = ctx_len[seq[n]] of replica 0; the rows
+ * d_k_new/d_v_new [N][H][Dh] bf16 are written at [seq][h][pos][:] of every
+ * replica's [S][H][C][Dh] cache, then each replica's ctx_len[seq] = pos + 1.
+ * Replicas are device pointers reachable from this GPU (local buffers or
+ * CUDA-IPC-mapped NVLink peers), up to 8; h_* arrays hold `replicas` entries,
+ * replica 0 is the local one. Tokens whose sequence is full (pos == C) are
+ * skipped and counted in *d_overflow (nullable). Cross-GPU readers must
+ * synchronise (stream sync + barrier) before attending. */
+exf_status exf_kv_append(const void* d_k_new, const void* d_v_new, const int32_t* d_seq,
+                         int64_t N, int32_t S, int32_t H, int32_t Dh, int32_t C,
+                         int32_t replicas, void* const* h_k_caches, void* const* h_v_caches,
+                         int32_t* const* h_ctx_lens, int32_t* d_overflow, exf_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

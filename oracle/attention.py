@@ -39,3 +39,20 @@ def coherent_attention(q, seq, ctx_len, k, v, scale):
         p /= p.sum(axis=1, keepdims=True)
         out[n] = np.einsum("hl,hld->hd", p, vv)
     return out
+
+
+def kv_append(k_new, v_new, seq, k_cache, v_cache, ctx_len):
+    """In-place restatement of exf_kv_append on one replica (numpy arrays).
+    Returns the number of tokens skipped because their sequence was full."""
+    C = k_cache.shape[2]
+    overflow = 0
+    for n in range(k_new.shape[0]):
+        s = int(seq[n])
+        pos = int(ctx_len[s])
+        if pos >= C:
+            overflow += 1
+            continue
+        k_cache[s, :, pos, :] = k_new[n]
+        v_cache[s, :, pos, :] = v_new[n]
+        ctx_len[s] = pos + 1
+    return overflow

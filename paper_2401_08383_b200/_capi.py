@@ -119,6 +119,8 @@ SIGNATURES = {
     "exf_coherent_attention_workspace_bytes": (_I64, [_I64, _I32, _I32, _I32]),
     "exf_coherent_attention": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _I64, _I32, _I32, _I32, _I32,
                                          C.c_float, _VP, _VP, _VP]),
+    "exf_kv_append": (C.c_int, [_VP, _VP, _VP, _I64, _I32, _I32, _I32, _I32, _I32, _VP, _VP, _VP,
+                                _VP, _VP]),
 }
 
 

@@ -46,3 +46,29 @@ def coherent_attention(q: torch.Tensor, seq: torch.Tensor, ctx_len: torch.Tensor
                N, S, H, Dh, Cap, C.c_float(scale), _ptr(workspace) if ws_bytes else None,
                _ptr(out), C.c_void_p(stream))
     return out
+
+
+def kv_append(k_new: torch.Tensor, v_new: torch.Tensor, seq: torch.Tensor,
+              k_caches, v_caches, ctx_lens, overflow: torch.Tensor | None = None) -> None:
+    """Append one token per sequence to every replica of the context cache.
+
+    k_new/v_new [N][H][Dh] bf16, seq [N] int32 (distinct); k_caches/v_caches
+    lists of [S][H][C][Dh] bf16 replicas (replica 0 local; the others may be
+    CUDA-IPC peer tensors), ctx_lens the matching [S] int32 lengths.
+    """
+    N, H, Dh = k_new.shape
+    S, Hk, Cap, Dk = k_caches[0].shape
+    if (Hk, Dk) != (H, Dh) or v_new.shape != k_new.shape:
+        raise _capi.ExflowInvalidArgument("kv_append: shape mismatch")
+    for t in [k_new, v_new, *k_caches, *v_caches]:
+        if t.dtype != torch.bfloat16 or not t.is_contiguous() or t.shape[-1] != Dh:
+            raise _capi.ExflowInvalidArgument("kv_append: contiguous bf16 tensors required")
+    R = len(k_caches)
+    if len(v_caches) != R or len(ctx_lens) != R:
+        raise _capi.ExflowInvalidArgument("kv_append: replica lists differ in length")
+    ks = (C.c_void_p * R)(*[t.data_ptr() for t in k_caches])
+    vs = (C.c_void_p * R)(*[t.data_ptr() for t in v_caches])
+    cs = (C.c_void_p * R)(*[t.data_ptr() for t in ctx_lens])
+    stream = torch.cuda.current_stream(k_new.device).cuda_stream
+    _capi.call("exf_kv_append", _ptr(k_new), _ptr(v_new), _ptr(seq), N, S, H, Dh, Cap, R,
+               ks, vs, cs, _ptr(overflow), C.c_void_p(stream))

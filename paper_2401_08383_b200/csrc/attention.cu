@@ -265,3 +265,101 @@ extern "C" exf_status exf_coherent_attention(const void* d_q, const int32_t* d_s
     if (err != cudaSuccess) return cuda_status(err, "coherent_attention launch");
     return EXF_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Per-step K/V append into every replica of the context cache: the data the
+// ExFlow context AllGather moves (proj/src/sim.cpp:161-162). The rank that
+// holds a token writes its new K/V rows at position ctx_len[seq] of each
+// replica (local or NVLink peer pointers, up to 8) and advances ctx_len there.
+// One token per sequence per call (decode), so positions are race-free and
+// every replica stays identical.
+namespace exf {
+namespace {
+
+constexpr int kMaxReplicas = 8;
+struct KvReplicas {
+    __nv_bfloat16* k[kMaxReplicas];
+    __nv_bfloat16* v[kMaxReplicas];
+    int32_t* ctx[kMaxReplicas];
+};
+
+// grid (N), 128 threads: one token's H*Dh K and V values per block.
+__global__ void __launch_bounds__(128) kv_append_kernel(const uint4* __restrict__ k_new,
+                                                        const uint4* __restrict__ v_new,
+                                                        const int32_t* __restrict__ seq,
+                                                        int32_t H, int32_t Dh, int32_t C,
+                                                        int32_t replicas, KvReplicas rep,
+                                                        int32_t* overflow) {
+    const int n = blockIdx.x;
+    const int s = seq[n];
+    const int pos = rep.ctx[0][s];
+    if (pos >= C) {
+        if (threadIdx.x == 0 && overflow) atomicAdd(overflow, 1);
+        return;
+    }
+    const int vec_per_head = Dh / 8;
+    const int vecs = H * vec_per_head;
+    for (int i = threadIdx.x; i < vecs; i += blockDim.x) {
+        const int h = i / vec_per_head, c = i % vec_per_head;
+        const uint4 kv = k_new[(size_t)n * vecs + i];
+        const uint4 vv = v_new[(size_t)n * vecs + i];
+        const size_t off = (((size_t)s * H + h) * C + pos) * vec_per_head + c;
+        for (int r = 0; r < replicas; ++r) {
+            reinterpret_cast<uint4*>(rep.k[r])[off] = kv;
+            reinterpret_cast<uint4*>(rep.v[r])[off] = vv;
+        }
+    }
+    __threadfence_system();  // rows visible before the new length
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int r = 0; r < replicas; ++r) rep.ctx[r][s] = pos + 1;
+}
+
+}  // namespace
+}  // namespace exf
+
+extern "C" exf_status exf_kv_append(const void* d_k_new, const void* d_v_new,
+                                    const int32_t* d_seq, int64_t N, int32_t S, int32_t H,
+                                    int32_t Dh, int32_t C, int32_t replicas,
+                                    void* const* h_k_caches, void* const* h_v_caches,
+                                    int32_t* const* h_ctx_lens, int32_t* d_overflow,
+                                    exf_stream_t stream) {
+    using namespace exf;
+    if (N < 0 || S <= 0 || H <= 0 || C <= 0) {
+        set_error("kv_append: N >= 0, S, H, C > 0 required");
+        return EXF_INVALID;
+    }
+    if (Dh <= 0 || Dh % 8 != 0) {
+        set_error("kv_append: head dim must be a positive multiple of 8");
+        return EXF_INVALID;
+    }
+    if (replicas < 1 || replicas > kMaxReplicas) {
+        set_error("kv_append: replicas must be in [1, 8]");
+        return EXF_INVALID;
+    }
+    if (N > S) {
+        set_error("kv_append: more tokens than sequences (one token per sequence per call)");
+        return EXF_INVALID;
+    }
+    if (N == 0) return EXF_OK;
+    if (!d_k_new || !d_v_new || !d_seq || !h_k_caches || !h_v_caches || !h_ctx_lens) {
+        set_error("kv_append: null buffer");
+        return EXF_INVALID;
+    }
+    KvReplicas rep{};
+    for (int r = 0; r < replicas; ++r) {
+        if (!h_k_caches[r] || !h_v_caches[r] || !h_ctx_lens[r]) {
+            set_error("kv_append: null replica " + std::to_string(r));
+            return EXF_INVALID;
+        }
+        rep.k[r] = static_cast<__nv_bfloat16*>(h_k_caches[r]);
+        rep.v[r] = static_cast<__nv_bfloat16*>(h_v_caches[r]);
+        rep.ctx[r] = h_ctx_lens[r];
+    }
+    kv_append_kernel<<<(unsigned)N, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(d_k_new), static_cast<const uint4*>(d_v_new), d_seq, H, Dh, C,
+        replicas, rep, d_overflow);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return cuda_status(err, "kv_append launch");
+    return EXF_OK;
+}

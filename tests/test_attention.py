@@ -101,3 +101,58 @@ def test_deterministic_across_calls():
     a = coherent_attention(q, seq, ctx, k, v)
     b = coherent_attention(q, seq, ctx, k, v)
     assert torch.equal(a, b)
+
+
+def test_kv_append_oracle_and_validation_without_gpu():
+    k = np.zeros((3, 2, 2, 8), np.float32)
+    v = np.zeros_like(k)
+    ctx = np.array([0, 2, 1], np.int32)
+    kn = np.ones((2, 2, 8), np.float32)
+    assert oatt.kv_append(kn, 2 * kn, np.array([0, 1]), k, v, ctx) == 1  # seq 1 full
+    assert ctx.tolist() == [1, 2, 1] and k[0, :, 0].min() == 1 and v[0, :, 0].max() == 2
+    from paper_2401_08383_b200 import _capi
+    nul = [None] * 3
+    with pytest.raises(_capi.ExflowInvalidArgument, match="replicas must be in"):
+        _capi.call("exf_kv_append", *nul, 1, 1, 1, 64, 4, 9, None, None, None, None, None)
+    with pytest.raises(_capi.ExflowInvalidArgument, match="one token per sequence"):
+        _capi.call("exf_kv_append", *nul, 2, 1, 1, 64, 4, 1, None, None, None, None, None)
+    with pytest.raises(_capi.ExflowInvalidArgument, match="multiple of 8"):
+        _capi.call("exf_kv_append", *nul, 1, 1, 1, 60, 4, 1, None, None, None, None, None)
+
+
+@pytest.mark.gpu
+def test_kv_append_replicas_then_attention():
+    """Two decode steps: tokens in dispatch order append to 3 replicas (virtual
+    ranks on one GPU); every replica equals the oracle bit for bit, the full
+    sequence is counted as overflow, and attention over any replica matches."""
+    import torch
+    from paper_2401_08383_b200.attention import coherent_attention, kv_append
+    S, H, Dh, Cap, R = 6, 4, 64, 40, 3
+    g = torch.Generator().manual_seed(7)
+    k0 = torch.randn(S, H, Cap, Dh, generator=g).to(torch.bfloat16)
+    v0 = torch.randn(S, H, Cap, Dh, generator=g).to(torch.bfloat16)
+    ctx0 = torch.tensor([0, 5, 39, 40, 12, 1], dtype=torch.int32)
+    ks = [k0.clone().cuda() for _ in range(R)]
+    vs = [v0.clone().cuda() for _ in range(R)]
+    cs = [ctx0.clone().cuda() for _ in range(R)]
+    ok, ov, oc = k0.float().numpy().copy(), v0.float().numpy().copy(), ctx0.numpy().copy()
+    overflow = torch.zeros(1, dtype=torch.int32, device="cuda")
+    want_over = 0
+    for step in range(2):
+        seq = torch.randperm(S, generator=g).to(torch.int32)[:5]
+        kn = torch.randn(5, H, Dh, generator=g).to(torch.bfloat16)
+        vn = torch.randn(5, H, Dh, generator=g).to(torch.bfloat16)
+        kv_append(kn.cuda(), vn.cuda(), seq.cuda(), ks, vs, cs, overflow)
+        want_over += oatt.kv_append(kn.float().numpy(), vn.float().numpy(), seq.numpy(), ok, ov, oc)
+    torch.cuda.synchronize()
+    assert int(overflow.item()) == want_over
+    for r in range(R):
+        assert cs[r].cpu().numpy().tolist() == oc.tolist()
+        assert np.array_equal(ks[r].float().cpu().numpy(), ok)
+        assert np.array_equal(vs[r].float().cpu().numpy(), ov)
+    q = torch.randn(S, H, Dh, generator=g).to(torch.bfloat16)
+    seq = torch.arange(S, dtype=torch.int32).flip(0).contiguous()
+    out = coherent_attention(q.cuda(), seq.cuda(), cs[2], ks[2], vs[2])
+    torch.cuda.synchronize()
+    ref = oatt.coherent_attention(q.float().numpy(), seq.numpy(), oc, ok, ov, Dh ** -0.5)
+    assert np.abs(out.float().cpu().numpy() - ref).max() <= 1e-2 * max(np.abs(ref).max(), 1.0)
