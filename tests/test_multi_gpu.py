@@ -49,3 +49,16 @@ def test_four_gpu_parity(vanilla):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert " OK " in r.stdout
+
+
+def test_kv_append_replicated():
+    """exf_kv_append writing every rank's replica over NVLink (CUDA-IPC peers)."""
+    n = _gpus()
+    if n < 2:
+        pytest.skip("needs two GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29641",
+           os.path.join(HERE, "kv_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "OK" in r.stdout
