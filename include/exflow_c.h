@@ -330,6 +330,13 @@ exf_status exf_kv_append(const void* d_k_new, const void* d_v_new, const int32_t
                          int32_t replicas, void* const* h_k_caches, void* const* h_v_caches,
                          int32_t* const* h_ctx_lens, int32_t* d_overflow, exf_stream_t stream);
 
+/* Replica wiring for exf_kv_append across processes: export a device buffer
+ * as a 64-byte CUDA-IPC handle + byte offset inside its allocation, import it
+ * on the caller's current device (peer access enabled lazily), close it. */
+exf_status exf_ipc_export(const void* d_ptr, void* h_handle64, int64_t* h_offset);
+exf_status exf_ipc_import(const void* h_handle64, int64_t offset, void** d_ptr);
+exf_status exf_ipc_close(void* d_ptr, int64_t offset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -121,6 +121,9 @@ SIGNATURES = {
                                          C.c_float, _VP, _VP, _VP]),
     "exf_kv_append": (C.c_int, [_VP, _VP, _VP, _I64, _I32, _I32, _I32, _I32, _I32, _VP, _VP, _VP,
                                 _VP, _VP]),
+    "exf_ipc_export": (C.c_int, [_VP, _VP, _VP]),
+    "exf_ipc_import": (C.c_int, [_VP, _I64, _VP]),
+    "exf_ipc_close": (C.c_int, [_VP, _I64]),
 }
 
 

@@ -72,3 +72,35 @@ def kv_append(k_new: torch.Tensor, v_new: torch.Tensor, seq: torch.Tensor,
     stream = torch.cuda.current_stream(k_new.device).cuda_stream
     _capi.call("exf_kv_append", _ptr(k_new), _ptr(v_new), _ptr(seq), N, S, H, Dh, Cap, R,
                ks, vs, cs, _ptr(overflow), C.c_void_p(stream))
+
+
+def export_replica(t: torch.Tensor):
+    """(64-byte CUDA-IPC handle, byte offset) of a device tensor's buffer."""
+    h = (C.c_char * 64)()
+    off = C.c_int64()
+    _capi.call("exf_ipc_export", _ptr(t), h, C.byref(off))
+    return bytes(h), off.value
+
+
+class _Cai:
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def import_replica(handle: bytes, offset: int, shape, dtype: torch.dtype) -> torch.Tensor:
+    """Map a peer's buffer on the current device (NVLink peer access). The
+    returned tensor aliases the peer's HBM; pass it to kv_append as a replica.
+    Release with close_replica(t, offset)."""
+    h = (C.c_char * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    _capi.call("exf_ipc_import", h, offset, C.byref(p))
+    if dtype == torch.bfloat16:
+        return torch.as_tensor(_Cai(p.value, shape, "<i2"), device="cuda").view(torch.bfloat16)
+    if dtype == torch.int32:
+        return torch.as_tensor(_Cai(p.value, shape, "<i4"), device="cuda")
+    raise _capi.ExflowInvalidArgument("import_replica: bf16 or int32 buffers only")
+
+
+def close_replica(t: torch.Tensor, offset: int) -> None:
+    _capi.call("exf_ipc_close", C.c_void_p(t.data_ptr()), offset)

@@ -24,6 +24,8 @@
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
+#include <cstring>
+
 namespace exf {
 namespace {
 
@@ -361,5 +363,57 @@ extern "C" exf_status exf_kv_append(const void* d_k_new, const void* d_v_new,
         replicas, rep, d_overflow);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_status(err, "kv_append launch");
+    return EXF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Buffer sharing for the cache replicas: a 64-byte CUDA-IPC handle plus the
+// byte offset of the pointer inside its allocation (caching allocators hand
+// out sub-ranges), opened on the CALLER's current device so that kernels
+// launched there can store into the peer's HBM over NVLink.
+#include <cuda.h>
+
+extern "C" exf_status exf_ipc_export(const void* d_ptr, void* h_handle64, int64_t* h_offset) {
+    using namespace exf;
+    if (!d_ptr || !h_handle64 || !h_offset) return invalid("ipc_export: null argument");
+    // driver entry point resolved at run time (no link-time libcuda dependency)
+    using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static RangeFn range_fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<RangeFn>(p);
+        return static_cast<RangeFn>(nullptr);
+    }();
+    if (!range_fn) return runtime_err("ipc_export: cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS)
+        return runtime_err("ipc_export: pointer is not a device allocation");
+    cudaIpcMemHandle_t h;
+    EXF_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    static_assert(sizeof(h) == 64, "CUDA IPC handle is 64 bytes");
+    memcpy(h_handle64, &h, 64);
+    *h_offset = (int64_t)(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
+    return EXF_OK;
+}
+
+extern "C" exf_status exf_ipc_import(const void* h_handle64, int64_t offset, void** d_ptr) {
+    using namespace exf;
+    if (!h_handle64 || !d_ptr || offset < 0) return invalid("ipc_import: bad argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, h_handle64, 64);
+    void* base = nullptr;
+    EXF_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *d_ptr = static_cast<char*>(base) + offset;
+    return EXF_OK;
+}
+
+extern "C" exf_status exf_ipc_close(void* d_ptr, int64_t offset) {
+    using namespace exf;
+    if (!d_ptr) return invalid("ipc_close: null pointer");
+    EXF_CUDA_TRY(cudaIpcCloseMemHandle(static_cast<char*>(d_ptr) - offset));
     return EXF_OK;
 }

@@ -11,18 +11,18 @@ import sys
 import numpy as np
 import torch
 import torch.distributed as dist
-from torch.multiprocessing.reductions import reduce_tensor
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle import attention as oatt  # noqa: E402
-from paper_2401_08383_b200.attention import coherent_attention, kv_append  # noqa: E402
+from paper_2401_08383_b200.attention import (close_replica, coherent_attention,  # noqa: E402
+                                             export_replica, import_replica, kv_append)
 
 
 def main():
     rank, G = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
     dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
-    B, H, Dh, Cap, steps = 6, 8, 64, 64, 3
+    B, H, Dh, Cap, steps = 6, 8, 64, 256, 3  # >1 MB caches: one allocator segment each
     S = G * B
     g = torch.Generator().manual_seed(11)
     k0 = torch.randn(S, H, Cap, Dh, generator=g).to(torch.bfloat16)
@@ -30,11 +30,13 @@ def main():
     ctx0 = torch.randint(0, Cap - steps, (S,), generator=g, dtype=torch.int32)
     ctx0[0] = Cap - 1  # fills up during the run -> overflow on the next steps
     k, v, ctx = k0.cuda(), v0.cuda(), ctx0.clone().cuda()
-    shared = [reduce_tensor(t) for t in (k, v, ctx)]
+    shared = [export_replica(t) for t in (k, v, ctx)]
     everyone = [None] * G
     dist.all_gather_object(everyone, shared)
-    # map the peers' buffers (CUDA IPC; own handle is not reopened)
-    peers = [None if p == rank else [fn(*args) for fn, args in everyone[p]] for p in range(G)]
+    # map the peers' buffers on this GPU (CUDA IPC, NVLink peer access)
+    peers = [None if p == rank else
+             [import_replica(h, off, t.shape, t.dtype) for (h, off), t in zip(everyone[p], (k, v, ctx))]
+             for p in range(G)]
     order = [rank] + [p for p in range(G) if p != rank]  # replica 0 = local
     ks = [k if p == rank else peers[p][0] for p in order]
     vs = [v if p == rank else peers[p][1] for p in order]
@@ -72,8 +74,12 @@ def main():
     if rank == 0:
         print(f"kv_append replicated over {G} GPUs: OK (steps {steps}, overflow "
               f"{want_over})", flush=True)
-    del peers, ks, vs, cs
     torch.cuda.synchronize()
+    dist.barrier()
+    for p in range(G):
+        if peers[p] is not None:
+            for t, (h, off) in zip(peers[p], everyone[p]):
+                close_replica(t, off)
     dist.barrier()
     dist.destroy_process_group()
 
