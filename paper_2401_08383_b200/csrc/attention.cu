@@ -193,12 +193,21 @@ __global__ void __launch_bounds__(kThreads) coherent_attn_kernel(
     }
 }
 
-int attn_splits(int64_t N, int32_t H, int32_t C) {
-    int dev = 0, sms = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess)
+int attn_splits(int64_t N, int32_t H, int32_t Dh, int32_t C) {
+    int dev = 0, sms = 148, per_sm = 8;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int b = 0;
+        const cudaError_t e =
+            Dh == 128 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, coherent_attn_kernel<128>,
+                                                                      kThreads, 0)
+                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, coherent_attn_kernel<64>,
+                                                                      kThreads, 0);
+        if (e == cudaSuccess && b > 0) per_sm = b;
+    }
+    cudaGetLastError();
     const int64_t heads = N * (int64_t)H;
-    const int64_t target = (int64_t)sms * 8;  // ~8 resident 128-thread CTAs per SM
+    const int64_t target = (int64_t)sms * per_sm;  // one full wave of resident CTAs
     int64_t splits = target / heads;  // round down: one full wave, no tail
     const int64_t max_splits = (C + 255) / 256;  // at least 256 keys per split
     if (splits > max_splits) splits = max_splits;
@@ -212,7 +221,7 @@ int attn_splits(int64_t N, int32_t H, int32_t C) {
 extern "C" int64_t exf_coherent_attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh,
                                                           int32_t C) {
     if (N <= 0 || H <= 0 || Dh <= 0 || C <= 0) return 0;
-    int splits = exf::attn_splits(N, H, C);
+    int splits = exf::attn_splits(N, H, Dh, C);
     cudaGetLastError();
     if (splits <= 1) return 0;
     return N * (int64_t)H * ((int64_t)splits * (Dh + 2) * (int64_t)sizeof(float) + 4);
@@ -242,7 +251,7 @@ extern "C" exf_status exf_coherent_attention(const void* d_q, const int32_t* d_s
         set_error("coherent_attention: null buffer");
         return EXF_INVALID;
     }
-    const int splits = attn_splits(N, H, C);
+    const int splits = attn_splits(N, H, Dh, C);
     if (splits > 1 && !d_workspace) {
         set_error("coherent_attention: workspace required (exf_coherent_attention_workspace_bytes)");
         return EXF_INVALID;
