@@ -156,3 +156,13 @@ def test_kv_append_replicas_then_attention():
     torch.cuda.synchronize()
     ref = oatt.coherent_attention(q.float().numpy(), seq.numpy(), oc, ok, ov, Dh ** -0.5)
     assert np.abs(out.float().cpu().numpy() - ref).max() <= 1e-2 * max(np.abs(ref).max(), 1.0)
+
+
+def test_ipc_entry_points_validate_without_gpu():
+    from paper_2401_08383_b200 import _capi
+    with pytest.raises(_capi.ExflowInvalidArgument, match="ipc_export: null"):
+        _capi.call("exf_ipc_export", None, None, None)
+    with pytest.raises(_capi.ExflowInvalidArgument, match="ipc_import: bad"):
+        _capi.call("exf_ipc_import", None, 0, None)
+    with pytest.raises(_capi.ExflowInvalidArgument, match="ipc_close: null"):
+        _capi.call("exf_ipc_close", None, 0)
