@@ -50,7 +50,24 @@ def parse():
     p.add_argument("--d-ffn", type=int, default=4096)
     p.add_argument("--gate-affinity", type=float, default=0.8)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-parity", action="store_true", help="skip the per-placement checked step")
+    p.add_argument("--no-routing-kernels", action="store_true",
+                   help="skip the histogram / replay kernel measurements")
     return p.parse_args()
+
+
+def self_launch(a):
+    """`python bench.py --gpus N` without torchrun: spawn the N ranks (one per
+    GPU) the way the driver does, and relay rank 0's JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    log(f"[bench] WORLD_SIZE unset and --gpus {a.gpus}: launching {a.gpus} ranks")
+    return subprocess.call(cmd)
 
 
 def workload(a, n):
@@ -120,14 +137,16 @@ def run_reference(a, rank, n):
     from oracle import cpu_path, oracle as orc
     assign = orc.contiguous_placement(a.experts, a.layers, n)
     tokens = a.batch * n
-    layers_sample = 2
-    tps, dt, sample, threads = cpu_path.time_cpu_path(a.experts, a.layers, a.d_model, a.d_ffn,
-                                                      tokens, n, assign, layers_sample,
-                                                      max(1, a.steps // 4))
+    # every timed step is one whole decode step (all L layers) of the G*B
+    # tokens; K steps are bounded to a few minutes of CPU (steps_cpu <= K)
+    tps, dt, sample, threads, nsteps = cpu_path.time_cpu_path(
+        a.experts, a.layers, a.d_model, a.d_ffn, tokens, n, assign, steps=None,
+        min_seconds=20.0, max_steps=max(1, a.steps))
     routes = orc.generate_markov_trace(a.experts, a.layers, 1 << 18, 0.8, 4, 1)
     routing_tps = cpu_path.time_reference_routing(routes, a.experts, assign, n, threads)
     line = {"impl": "reference", "metric": METRIC, "value": tps, "unit": UNIT, "n_gpus": n,
-            "steps": a.steps, "warmup": a.warmup, "ms_per_step": tokens / tps * 1e3,
+            "steps": nsteps, "steps_requested": a.steps, "warmup": 1,
+            "ms_per_step": tokens / tps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": workload(a, n),
             "cpu_baseline": {"value": tps, "unit": UNIT, "cores": threads, "kind": "port",
@@ -143,18 +162,27 @@ def run_reference(a, rank, n):
 # ---------------------------------------------------------------- our arm
 def main():
     a = parse()
+    if a.impl == "ours" and a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(a))
     n_env = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     n = max(n_env, 1)
     if a.impl == "reference":
-        return run_reference(a, rank, n)
+        # under torchrun rank 0 alone runs the CPU arm; without it, --gpus N
+        # names the config (G*B tokens on an N-GPU placement)
+        return run_reference(a, rank, n if "WORLD_SIZE" in os.environ else max(a.gpus, 1))
+    if n != a.gpus:
+        log(f"[bench] --gpus {a.gpus} but WORLD_SIZE={n}: refusing to report a mislabeled run")
+        sys.exit(2)
 
     import numpy as np
     import torch
     import torch.distributed as dist
     from paper_2401_08383_b200 import _capi, affinity, placement as pl
     from paper_2401_08383_b200.model import MoeModel, MoeModelConfig
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from step_check import check_step  # the checker (CPU oracle), never timed
 
     torch.cuda.set_device(local_rank)
     if n > 1:
@@ -200,30 +228,32 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     topo = affinity.Topology(1, n)
 
-    # ---- vanilla placement + profiling pass for the affinity histogram
+    # ---- vanilla placement + profiling pass for the affinity histogram, on
+    # HELD-OUT batches (other seeds than the timed input): routing depends
+    # only on the tokens and the gate, so profiling the timed batch itself
+    # would fit the placement to exactly the routes it is then timed on
     vanilla = pl.contiguous_placement(a.experts, a.layers, topo)
     model = make_model(vanilla)
+    prof_batches = 4
     with torch.cuda.stream(stream):
-        for _ in range(4):
-            model.step(x_dev, stream)
-    stream.synchronize()
+        for k in range(prof_batches):
+            gp = torch.Generator(device="cpu").manual_seed(10_000 + 97 * k + rank)
+            xp = torch.randn(a.batch, a.d_model, generator=gp).to(torch.bfloat16).to(dev)
+            model.step(xp, stream)
+            stream.synchronize()
     model.check()
     counts = allsum_i64(model.affinity_counts())
     aff_assign, solve = pl.solve_staged(counts, topo, pl.AnnealParams(seed=7))
-    # G=8 view of the same routes (replay on the GPU): how much cross-GPU
-    # routing each placement would cause on the 8xB200 box
-    routes = model.routes()
+    prof_routes = model.routes()
     if n > 1:
         allr = [None] * n
-        dist.all_gather_object(allr, routes)
-        routes = np.max(np.stack(allr), axis=0)
+        dist.all_gather_object(allr, prof_routes)
+        prof_routes = np.max(np.stack(allr), axis=0)
+    # G=8 view (replay kernel): the placement solved from the held-out
+    # profile, evaluated on the timed batch's routes (below)
     g8 = affinity.Topology(1, 8)
-    g8_counts = affinity.count_transitions(routes, a.experts).matrices
+    g8_counts = affinity.count_transitions(prof_routes, a.experts).matrices
     g8_aff, _ = pl.solve_staged(g8_counts, g8, pl.AnnealParams(seed=7))
-    rep_v8 = affinity.simulate(routes, pl.contiguous_placement(a.experts, a.layers, g8),
-                               affinity.SimConfig(mode=affinity.COHERENT, topology=g8))
-    rep_a8 = affinity.simulate(routes, g8_aff, affinity.SimConfig(mode=affinity.COHERENT,
-                                                                   topology=g8))
 
     results = {}
     clocks = None
@@ -260,6 +290,16 @@ def main():
                          "routed_fraction": frac}
         log(f"[bench] {name}: {ms:.3f} ms/step, {results[name]['value']:.0f} tok/s, "
             f"routed fraction {frac:.4f}")
+        if name == "affinity":
+            timed_routes = model.routes()
+            if n > 1:
+                allr = [None] * n
+                dist.all_gather_object(allr, timed_routes)
+                timed_routes = np.max(np.stack(allr), axis=0)
+        if not a.no_parity:  # outside the timed region: one checked step
+            results[name]["check"] = check_step(model, x_dev, assign)
+            log(f"[bench] {name}: parity {results[name]['check']['parity']} "
+                f"{results[name]['check']['failures']}")
 
     # ---- the baseline ExFlow is measured against: vanilla expert parallelism
     # (contiguous placement, dispatch + combine back home every layer: 2L
@@ -283,9 +323,10 @@ def main():
     ms_v = allmax(ev0.elapsed_time(ev1)) / a.steps
     barrier()
     crossed_v = allsum_i64(vm.crossed())
+    check_v = check_step(vm, x_dev, vanilla) if not a.no_parity else None
     results_ep_vanilla = {"value": a.batch * n / (ms_v * 1e-3), "ms_per_step": ms_v,
                           "routed_fraction": float(crossed_v.sum()) / (a.batch * n * a.layers * a.steps),
-                          "exchanges_per_step": 2 * a.layers + 1,
+                          "exchanges_per_step": 2 * a.layers + 1, "check": check_v,
                           "note": "vanilla EP: contiguous placement, outputs combined back to the home GPU "
                                   "after every layer; routed_fraction = away-from-home token-layers"}
     log(f"[bench] vanilla EP (2 exchanges/layer): {ms_v:.3f} ms/step, {results_ep_vanilla['value']:.0f} tok/s")
@@ -388,14 +429,25 @@ def main():
         traffic, traffic_src = summ.get("traffic_bytes_per_launch"), "profiles/r01_fused_ncu_summary.json"
     launches = model.launches_per_step()
 
-    # ---- CPU baseline (rank 0, N=1 only)
+    # ---- CPU baseline (rank 0, at every N; the other ranks wait): whole
+    # decode steps of the same G*B tokens on the host cores, nothing
+    # extrapolated; the reference's own CPU routing bookkeeping included
     cpu = None
-    if rank == 0 and n == 1 and not a.no_cpu_baseline:
+    if rank == 0 and not a.no_cpu_baseline:
         from oracle import cpu_path
-        tps, dt, sample, threads = cpu_path.time_cpu_path(
-            a.experts, a.layers, a.d_model, a.d_ffn, a.batch, 1,
-            np.zeros((a.layers, a.experts), np.int32), 2, 2)
+        tps, dt, sample, threads, _ = cpu_path.time_cpu_path(
+            a.experts, a.layers, a.d_model, a.d_ffn, a.batch * n, n, vanilla, steps=None,
+            min_seconds=10.0, max_steps=5)
         cpu = {"value": tps, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+    # ---- the reference's own hot loops as GPU kernels: affinity histogram
+    # (proj/src/trace.cpp:205-209) and routing replay (proj/src/sim.cpp:110-145)
+    routing = None
+    if rank == 0 and not a.no_routing_kernels:
+        try:
+            routing = measure_routing_kernels(hbm_peak, stream)
+        except Exception as e:  # informational; never blocks the headline line
+            routing = {"error": f"{type(e).__name__}: {e}"}
+    barrier()
 
     # ---- coherent decode attention over the replicated context (SURVEY §8(f)
     # rank 1), measured beside the MoE step at BASELINE configs[4]'s shape:
@@ -407,18 +459,29 @@ def main():
         except Exception as e:  # informational; never blocks the headline line
             attn = {"error": f"{type(e).__name__}: {e}"}
 
+    rep_v8 = affinity.simulate(timed_routes, pl.contiguous_placement(a.experts, a.layers, g8),
+                               affinity.SimConfig(mode=affinity.COHERENT, topology=g8))
+    rep_a8 = affinity.simulate(timed_routes, g8_aff, affinity.SimConfig(mode=affinity.COHERENT,
+                                                                         topology=g8))
     aff = results["affinity"]
+    checks = [r.get("check") for r in results.values()] + [check_v]
+    parity = "unchecked" if a.no_parity else \
+        ("ok" if all(c and c["parity"] == "ok" for c in checks) else "FAIL")
     line = {
         "metric": METRIC, "value": aff["value"], "unit": UNIT, "n_gpus": n, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": aff["ms_per_step"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": dict(workload(a, n), launch_plan=plan),
         "routed_fraction": aff["routed_fraction"],
+        "parity": parity,
+        "affinity_profile": f"held-out: histogram of {prof_batches} other input batches "
+                            "(seeds != timed batch), solve_staged on the CPU",
         "placements": results,
         "ep_vanilla_2exchange": results_ep_vanilla,
         "g8_replay_routed_fraction": {"vanilla": rep_v8.p_star, "affinity": rep_a8.p_star,
-                                      "note": "p_star of this run's routes replayed on a 1x8 "
-                                              "topology (GPU replay kernel)"},
+                                      "note": "p_star of the timed batch's routes replayed on a 1x8 "
+                                              "topology (GPU replay kernel); the affinity placement "
+                                              "is solved from the held-out profiling batches"},
         "affinity_solve": {"solver": solve.solver, "objective": solve.objective},
         "e2e": {"value": a.batch * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
@@ -438,6 +501,7 @@ def main():
         "gpu_launches": launches * (a.steps) * n,
         "cpu_baseline": cpu,
         "coherent_attention": attn,
+        "routing_kernels": routing,
     }
     if rank == 0:
         sys.stdout.write(json.dumps(line) + "\n")
@@ -448,6 +512,105 @@ def main():
     model.close()
     if n > 1:
         dist.destroy_process_group()
+
+
+def measure_routing_kernels(hbm_peak, stream, T=1 << 21, L=24, iters=10):
+    """exf_count_transitions (kernel 5, bulk rebuild) and exf_route_replay
+    (coherent simulate counters) on synthetic Markov traces of T tokens x L
+    layers at E = 8 and E = 64 (int32 ids; 201 MB at T = 2^21 > the 126 MB L2,
+    so every call streams the trace from HBM). Device time: CUDA events on the
+    launching stream around `iters` back-to-back calls. Host entry points
+    (exf_*_host: host-side id validation, pinned H2D, kernel, D2H): wall clock.
+    CPU: the reference's loops (C restatement, all host threads, integer sums)
+    on the same trace. Algorithmic bytes: histogram 4*T*L (ids) + 8*(L-1)*E*(E+1)
+    (counts + row totals); replay 4*T*L + 4*L*E (placement)."""
+    import torch
+    from paper_2401_08383_b200 import _capi, placement as pl
+    from oracle import oracle as orc
+    lib = _capi.load()
+    out = {"trace": f"generate_markov_trace T={T} L={L} alpha=0.8, int32 ids", "peak_gbs": hbm_peak,
+           "per_E": {}}
+    threads = os.cpu_count() or 1
+    for E in (8, 64):
+        paths = pl.generate_markov_trace(E, L, T, 0.8, 8, 3)
+        assign = pl.contiguous_placement(E, L, affinity_topology(8))
+        dp = torch.from_numpy(paths).to("cuda")
+        da = torch.from_numpy(np.ascontiguousarray(assign, np.int32)).to("cuda")
+        pairs = L - 1
+        cnt = torch.empty(pairs * E * E, dtype=torch.int64, device="cuda")
+        tot = torch.empty(pairs * E, dtype=torch.int64, device="cuda")
+        wsb = lib.exf_count_transitions_workspace_bytes(T, L, E, 1)
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+        ctr = torch.empty(6, dtype=torch.int64, device="cuda")
+        sp = stream.cuda_stream
+
+        def hist():
+            _capi.call("exf_count_transitions", dp.data_ptr(), T, L, E, 1, cnt.data_ptr(),
+                       tot.data_ptr(), ws.data_ptr(), sp)
+
+        def replay():
+            _capi.call("exf_route_replay", dp.data_ptr(), None, da.data_ptr(), T, L, E, 1, 8, 1,
+                       ctr.data_ptr(), sp)
+
+        res = {}
+        for name, fn, byts in (("count_transitions", hist, 4 * T * L + 8 * pairs * E * (E + 1)),
+                               ("route_replay", replay, 4 * T * L + 4 * L * E)):
+            for _ in range(3):
+                fn()
+            stream.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(iters):
+                fn()
+            e1.record(stream)
+            stream.synchronize()
+            ms = e0.elapsed_time(e1) / iters
+            gbs = byts / (ms * 1e-3) / 1e9
+            res[name] = {"ms_per_call": ms, "bytes_per_call": byts, "achieved_gbs": gbs,
+                         "frac": gbs / hbm_peak, "tokens_per_s": T / (ms * 1e-3)}
+        # parity of this very run: counts and the coherent-move counter
+        want, wtot = orc.count_transitions(paths, E, 1, threads=threads)
+        got = cnt.view(pairs, E, E).cpu().numpy()
+        rep_o = orc.simulate(paths, assign, 1, 8, orc.COHERENT, threads=threads)
+        res["parity"] = bool(np.array_equal(got, want) and
+                             int(ctr.cpu().numpy()[3]) == rep_o.coherent_moves)
+        # host entry points (what exflow::count_transitions / simulate call)
+        t0 = time.perf_counter()
+        affinity_count_host(paths, E)
+        t1 = time.perf_counter()
+        affinity_simulate_host(paths, assign, 8)
+        t2 = time.perf_counter()
+        res["count_transitions"]["host_entry_ms"] = (t1 - t0) * 1e3
+        res["route_replay"]["host_entry_ms"] = (t2 - t1) * 1e3
+        # the reference's own loops on the CPU (same trace, all threads)
+        t0 = time.perf_counter()
+        orc.count_transitions(paths, E, 1, threads=threads)
+        t1 = time.perf_counter()
+        orc.simulate(paths, assign, 1, 8, orc.COHERENT, threads=threads)
+        t2 = time.perf_counter()
+        res["cpu_reference_loops"] = {"count_transitions_ms": (t1 - t0) * 1e3,
+                                      "simulate_ms": (t2 - t1) * 1e3, "cores": threads,
+                                      "kind": "port (C restatement, integer-sum threads)"}
+        out["per_E"][str(E)] = res
+        del dp, da, cnt, tot, ws
+    torch.cuda.empty_cache()
+    return out
+
+
+def affinity_topology(g):
+    from paper_2401_08383_b200 import affinity
+    return affinity.Topology(1, g)
+
+
+def affinity_count_host(paths, E):
+    from paper_2401_08383_b200 import affinity
+    return affinity.count_transitions(paths, E, 1)
+
+
+def affinity_simulate_host(paths, assign, g):
+    from paper_2401_08383_b200 import affinity
+    return affinity.simulate(paths, assign, affinity.SimConfig(mode=affinity.COHERENT,
+                                                               topology=affinity_topology(g)))
 
 
 def measure_attention(hbm_peak, B=8, H=16, Dh=64, ctx=16384, iters=20):

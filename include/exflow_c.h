@@ -305,9 +305,10 @@ exf_status exf_model_read_step_timeline(exf_model* model, uint64_t* h_stamps, in
  *   d_out [N][H][Dh] bf16 = softmax(scale * q k^T) v over keys < ctx_len;
  *   an empty context gives 0. Dh in {64, 128}. fp32 scores/softmax/accum.
  * d_workspace: exf_coherent_attention_workspace_bytes(N, H, Dh, C) bytes
- * (0 -> may be NULL), ZEROED before its first use; every call leaves it
- * zeroed again (split arrival counters). Deterministic (fixed merge order).
- * One launch per call.
+ * (0 -> may be NULL); no initialisation needed: the call zeroes the split
+ * arrival counters at the front of it on `stream` (one memset node) and
+ * the same workspace may be reused across calls of any N, H, C.
+ * Deterministic (fixed merge order). One kernel launch per call.
  * ---------------------------------------------------------------------- */
 int64_t exf_coherent_attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh, int32_t C);
 exf_status exf_coherent_attention(const void* d_q, const int32_t* d_seq, const int32_t* d_ctx_len,

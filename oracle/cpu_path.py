@@ -30,22 +30,25 @@ def _gelu(v: np.ndarray) -> np.ndarray:
 
 
 class CpuDecodePath:
-    def __init__(self, E, L, d, dff, tokens, G, assign, seed=0, layers=None):
+    """Every one of the L layers runs each step. To bound host memory, the
+    expert weights come from `weight_sets` distinct sets (layer j uses set
+    j % weight_sets; each set is E x 2 x d x dff fp32, far larger than the
+    CPU caches, so nothing is served from cache that HBM-sized weights would
+    not be)."""
+
+    def __init__(self, E, L, d, dff, tokens, G, assign, seed=0, weight_sets=2):
         self.E, self.L, self.d, self.dff, self.T, self.G = E, L, d, dff, tokens, G
         self.assign = np.ascontiguousarray(assign, np.int32)
-        self.layers = list(range(L)) if layers is None else list(layers)
         rng = np.random.default_rng(seed)
-        self.wg = {j: (rng.standard_normal((E, d), dtype=np.float32) / math.sqrt(d))
-                   for j in self.layers}
-        self.w1 = {}
-        self.w2 = {}
-        self.b1 = {}
-        self.b2 = {}
-        for j in self.layers:
-            self.w1[j] = [rng.standard_normal((dff, d), dtype=np.float32) * 0.02 for _ in range(E)]
-            self.w2[j] = [rng.standard_normal((d, dff), dtype=np.float32) * 0.02 for _ in range(E)]
-            self.b1[j] = [rng.standard_normal(dff, dtype=np.float32) * 0.02 for _ in range(E)]
-            self.b2[j] = [rng.standard_normal(d, dtype=np.float32) * 0.02 for _ in range(E)]
+        self.wg = [rng.standard_normal((E, d), dtype=np.float32) / math.sqrt(d) for _ in range(L)]
+        nset = max(1, min(weight_sets, L))
+        sets = []
+        for _ in range(nset):
+            sets.append(([rng.standard_normal((dff, d), dtype=np.float32) * 0.02 for _ in range(E)],
+                         [rng.standard_normal(dff, dtype=np.float32) * 0.02 for _ in range(E)],
+                         [rng.standard_normal((d, dff), dtype=np.float32) * 0.02 for _ in range(E)],
+                         [rng.standard_normal(d, dtype=np.float32) * 0.02 for _ in range(E)]))
+        self.w = [sets[j % nset] for j in range(L)]
         self.slot = np.zeros_like(self.assign)
         for j in range(L):
             seen = np.zeros(G, np.int32)
@@ -55,11 +58,12 @@ class CpuDecodePath:
                 seen[g] += 1
 
     def step(self, x: np.ndarray, threads: int):
-        """One decode step over all G*B tokens; returns (x_out, routes)."""
+        """One decode step over all G*B tokens and all L layers; returns
+        (x_out, routes, counts, report)."""
         T = self.T
         routes = np.zeros((T, self.L), np.int32)
-        loc = np.arange(T) % self.G
-        for j in self.layers:
+        for j in range(self.L):
+            w1, b1, w2, b2 = self.w[j]
             logits = x @ self.wg[j].T
             e = np.argmax(logits, axis=1).astype(np.int32)   # first max = lowest index
             z = np.exp(logits - logits.max(axis=1, keepdims=True))
@@ -68,7 +72,6 @@ class CpuDecodePath:
             dest = self.assign[j][e]
             # coherent dispatch: stable bucketing by (destination GPU, local slot)
             order = np.lexsort((np.arange(T), self.slot[j][e], dest))
-            loc = dest
             xs = x[order]
             es = e[order]
             out = np.empty_like(xs)
@@ -76,8 +79,8 @@ class CpuDecodePath:
                 sel = np.nonzero(es == ex)[0]
                 if sel.size == 0:
                     continue
-                h = _gelu(xs[sel] @ self.w1[j][ex].T + self.b1[j][ex])
-                y = h @ self.w2[j][ex].T + self.b2[j][ex]
+                h = _gelu(xs[sel] @ w1[ex].T + b1[ex])
+                y = h @ w2[ex].T + b2[ex]
                 out[sel] = xs[sel] + prob[order][sel, None] * y
             x = np.empty_like(out)
             x[order] = out
@@ -88,23 +91,28 @@ class CpuDecodePath:
         return x, routes, counts, rep
 
 
-def time_cpu_path(E, L, d, dff, tokens, G, assign, layers_sample, steps, seed=0):
-    """Times `steps` steps over `layers_sample` of the L layers; returns
-    (tokens_per_s extrapolated to all L layers, seconds measured, sample str, threads)."""
+def time_cpu_path(E, L, d, dff, tokens, G, assign, steps=None, seed=0, min_seconds=8.0,
+                  max_steps=20):
+    """Times whole decode steps (all L layers, nothing extrapolated): at least
+    `steps` steps if given, else as many as fit `min_seconds` (>= 1, <=
+    max_steps). Returns (tokens_per_s, seconds measured, sample str, threads,
+    steps timed)."""
     threads = os.cpu_count() or 1
-    layers = list(range(min(layers_sample, L)))
-    path = CpuDecodePath(E, L, d, dff, tokens, G, assign, seed, layers)
+    path = CpuDecodePath(E, L, d, dff, tokens, G, assign, seed)
     rng = np.random.default_rng(seed + 1)
     x = rng.standard_normal((tokens, d), dtype=np.float32)
     path.step(x, threads)  # warm-up (BLAS threads, page faults)
+    n = 0
     t0 = time.perf_counter()
-    for _ in range(steps):
+    while True:
         path.step(x, threads)
-    dt = time.perf_counter() - t0
-    per_step_full = dt / steps * (L / len(layers))
-    sample = (f"{steps} steps x {len(layers)}/{L} layers x {tokens} tokens (numpy fp32 gate+FFN, "
-              f"C oracle histogram+replay), extrapolated linearly to {L} layers")
-    return tokens / per_step_full, dt, sample, threads
+        n += 1
+        dt = time.perf_counter() - t0
+        if (steps is not None and n >= steps) or (steps is None and (dt >= min_seconds or n >= max_steps)):
+            break
+    sample = (f"{n} full decode steps x {L}/{L} layers x {tokens} tokens (numpy fp32 gate+FFN on "
+              f"{threads} threads, C oracle histogram+replay); no extrapolation")
+    return n * tokens / dt, dt, sample, threads, n
 
 
 def time_reference_routing(paths: np.ndarray, E: int, assign: np.ndarray, G: int, threads: int,

@@ -39,8 +39,8 @@ def coherent_attention(q: torch.Tensor, seq: torch.Tensor, ctx_len: torch.Tensor
     lib = _capi.load()
     ws_bytes = lib.exf_coherent_attention_workspace_bytes(N, H, Dh, Cap)
     if ws_bytes and (workspace is None or workspace.numel() * workspace.element_size() < ws_bytes):
-        # zeroed once; the kernel leaves its arrival counters at zero
-        workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=q.device)
+        # any contents: the call zeroes its arrival counters on the stream
+        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
     stream = torch.cuda.current_stream(q.device).cuda_stream
     _capi.call("exf_coherent_attention", _ptr(q), _ptr(seq), _ptr(ctx_len), _ptr(k), _ptr(v),
                N, S, H, Dh, Cap, C.c_float(scale), _ptr(workspace) if ws_bytes else None,

@@ -220,23 +220,17 @@ extern "C" exf_status exf_count_transitions_host(const int32_t* h_paths, int64_t
     const size_t paths_b = (size_t)T * L * 4;
     const size_t counts_b = (size_t)p.pairs * E * E * 8;
     const size_t tot_b = (size_t)p.pairs * E * 8;
-    uint8_t* buf = nullptr;
     const size_t total = paths_b + counts_b + tot_b + (size_t)p.workspace_bytes + 64;
-    EXF_CUDA_TRY(cudaMalloc(&buf, total));
+    HostScratch* hs = nullptr;  // cached per thread and device: no per-call cudaMalloc
+    EXF_TRY(host_scratch(total, std::max(paths_b, counts_b), &hs));
+    uint8_t* buf = hs->dev;
     int32_t* d_paths = reinterpret_cast<int32_t*>(buf);
     int64_t* d_counts = reinterpret_cast<int64_t*>(buf + ((paths_b + 15) & ~size_t(15)));
     int64_t* d_tot = d_counts + (size_t)p.pairs * E * E;
     void* d_ws = d_tot + (size_t)p.pairs * E;
-    exf_status st = EXF_OK;
-    cudaError_t e = cudaMemcpy(d_paths, h_paths, paths_b, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) st = cuda_status(e, "cudaMemcpy H2D paths");
-    if (st == EXF_OK) st = exf_count_transitions(d_paths, T, L, E, gap, d_counts, d_tot, d_ws, nullptr);
-    if (st == EXF_OK) {
-        e = cudaMemcpy(h_counts, d_counts, counts_b, cudaMemcpyDeviceToHost);
-        if (e == cudaSuccess && h_row_totals)
-            e = cudaMemcpy(h_row_totals, d_tot, tot_b, cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) st = cuda_status(e, "cudaMemcpy D2H counts");
-    }
-    cudaFree(buf);
-    return st;
+    EXF_TRY(hs->h2d(d_paths, h_paths, paths_b));
+    EXF_TRY(exf_count_transitions(d_paths, T, L, E, gap, d_counts, d_tot, d_ws, hs->stream));
+    EXF_TRY(hs->d2h(h_counts, d_counts, counts_b));
+    if (h_row_totals) EXF_TRY(hs->d2h(h_row_totals, d_tot, tot_b));
+    return EXF_OK;
 }

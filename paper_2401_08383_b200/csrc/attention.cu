@@ -32,6 +32,13 @@ namespace {
 constexpr int kThreads = 128;
 constexpr int kUnroll = 4;
 
+// workspace layout: [N*H] u32 split-arrival counters (fixed offset 0, zeroed
+// per call), then the fp32 partials {m, l, acc[Dh]} per (token, head, split),
+// 16-byte aligned
+__host__ __device__ inline size_t ws_partials_off(int64_t N, int H) {
+    return (((size_t)N * H + 3) / 4) * 4;  // in floats
+}
+
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
@@ -154,7 +161,7 @@ __global__ void __launch_bounds__(kThreads) coherent_attn_kernel(
         if (splits == 1) {
             out[nh * Dh + c] = __float2bfloat16(L > 0.f ? A / L : 0.f);
         } else {
-            float* p = ws + (nh * splits + split) * (Dh + 2);
+            float* p = ws + ws_partials_off(gridDim.y, H) + (nh * splits + split) * (Dh + 2);
             p[2 + c] = A;
             if (c == 0) {
                 p[0] = M;
@@ -164,9 +171,11 @@ __global__ void __launch_bounds__(kThreads) coherent_attn_kernel(
     }
     if (splits == 1) return;
     // the last CTA of this (token, head) to finish merges all splits, in split
-    // order (deterministic); the arrival counter is reset for the next call
+    // order (deterministic). The arrival counters sit at the FRONT of the
+    // workspace (offset independent of N and splits) and are zeroed by the
+    // host wrapper on the launching stream before every call.
     __shared__ int s_last;
-    unsigned int* counters = reinterpret_cast<unsigned int*>(ws + (size_t)gridDim.y * H * splits * (Dh + 2));
+    unsigned int* counters = reinterpret_cast<unsigned int*>(ws);
     const size_t nh = (size_t)n * H + h;
     __threadfence();
     __syncthreads();
@@ -176,7 +185,7 @@ __global__ void __launch_bounds__(kThreads) coherent_attn_kernel(
     __threadfence();
     if (threadIdx.x < Dh) {
         const int c = threadIdx.x;
-        const float* p = ws + nh * splits * (Dh + 2);
+        const float* p = ws + ws_partials_off(gridDim.y, H) + nh * splits * (Dh + 2);
         float M = -CUDART_INF_F;
         for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, __ldcg(p + sp * (Dh + 2)));
         float L = 0.f, A = 0.f;
@@ -189,7 +198,6 @@ __global__ void __launch_bounds__(kThreads) coherent_attn_kernel(
             }
         }
         out[nh * Dh + c] = __float2bfloat16(L > 0.f ? A / L : 0.f);
-        if (c == 0) counters[nh] = 0u;
     }
 }
 
@@ -224,7 +232,8 @@ extern "C" int64_t exf_coherent_attention_workspace_bytes(int64_t N, int32_t H, 
     int splits = exf::attn_splits(N, H, Dh, C);
     cudaGetLastError();
     if (splits <= 1) return 0;
-    return N * (int64_t)H * ((int64_t)splits * (Dh + 2) * (int64_t)sizeof(float) + 4);
+    return (int64_t)exf::ws_partials_off(N, H) * (int64_t)sizeof(float) +
+           N * (int64_t)H * (int64_t)splits * (Dh + 2) * (int64_t)sizeof(float);
 }
 
 extern "C" exf_status exf_coherent_attention(const void* d_q, const int32_t* d_seq,
@@ -265,6 +274,10 @@ extern "C" exf_status exf_coherent_attention(const void* d_q, const int32_t* d_s
     auto v = static_cast<const __nv_bfloat16*>(d_v);
     auto o = static_cast<__nv_bfloat16*>(d_out);
     auto ws = static_cast<float*>(d_workspace);
+    if (splits > 1) {  // arrival counters (front of the workspace) start from zero
+        const cudaError_t ze = cudaMemsetAsync(ws, 0, (size_t)N * H * sizeof(unsigned int), st);
+        if (ze != cudaSuccess) return cuda_status(ze, "coherent_attention counter reset");
+    }
     if (Dh == 64) {
         coherent_attn_kernel<64><<<grid, kThreads, 0, st>>>(q, d_seq, d_ctx_len, k, v, H, C, chunk,
                                                             scale_log2, ws, o);

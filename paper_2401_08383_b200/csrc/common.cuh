@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <utility>
 #include <string>
@@ -31,6 +32,22 @@ inline exf_status runtime_err(const std::string& msg) {
     return EXF_RUNTIME;
 }
 exf_status cuda_status(cudaError_t err, const char* what);
+
+// Per-(host thread, device) scratch of the synchronous host-buffer entry
+// points (exf_count_transitions_host, exf_simulate_host): a device buffer and
+// a pinned staging buffer, both grown on demand and kept, plus a non-blocking
+// stream, so a decode-sized call costs no cudaMalloc/cudaFree/cudaHostAlloc.
+struct HostScratch {
+    uint8_t* dev = nullptr;
+    size_t dev_cap = 0;
+    uint8_t* pin = nullptr;
+    size_t pin_cap = 0;
+    cudaStream_t stream = nullptr;
+    // pageable host <-> device through the pinned buffer, on `stream`
+    exf_status h2d(void* d, const void* src, size_t bytes);
+    exf_status d2h(void* dst, const void* d, size_t bytes);  // synchronous
+};
+exf_status host_scratch(size_t dev_bytes, size_t pin_bytes, HostScratch** out);
 
 }  // namespace exf
 

@@ -163,6 +163,11 @@ struct exf_model {
 
 namespace {
 
+// cudaSuccess -> EXF_OK, else the CUDA status with its message
+inline exf_status cuda_status_ok(cudaError_t e, const char* what) {
+    return e == cudaSuccess ? EXF_OK : cuda_status(e, what);
+}
+
 template <class T>
 exf_status dalloc(T** p, size_t count) {
     EXF_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
@@ -567,10 +572,10 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
             m->fused = m->dense = false;  // too many pieces per CTA: two-kernel path
         EXF_M(dalloc(&m->f_pieces, pieces.size()));
         EXF_M(dalloc(&m->f_piece_off, off.size()));
-        EXF_CUDA_TRY(cudaMemcpy(m->f_pieces, pieces.data(), pieces.size() * sizeof(Piece),
-                                cudaMemcpyHostToDevice));
-        EXF_CUDA_TRY(cudaMemcpy(m->f_piece_off, off.data(), off.size() * sizeof(int32_t),
-                                cudaMemcpyHostToDevice));
+        EXF_M(cuda_status_ok(cudaMemcpy(m->f_pieces, pieces.data(), pieces.size() * sizeof(Piece),
+                                        cudaMemcpyHostToDevice), "piece table copy"));
+        EXF_M(cuda_status_ok(cudaMemcpy(m->f_piece_off, off.data(), off.size() * sizeof(int32_t),
+                                        cudaMemcpyHostToDevice), "piece offsets copy"));
         m->f_max_chunks = (C + nmax_f - 1) / nmax_f;
         const int64_t slots = (int64_t)m->E_loc * (f / 128 + d / 128) * m->f_max_chunks;
         const int smax = m->f_max_contrib;

@@ -149,25 +149,23 @@ extern "C" exf_status exf_simulate_host(const int32_t* h_paths, int64_t T, int32
                                         int32_t gpus_per_node, double intra_cost,
                                         double inter_cost, int32_t tokens_per_gpu, int32_t mode,
                                         const int32_t* h_homes, exf_sim_report* out) {
-    // validation order follows simulate (proj/src/sim.cpp:78-105)
+    // validation order follows simulate (proj/src/sim.cpp:78-105): the trace
+    // (trace.cpp:53-70), then the placement (placement.cpp:434-470), then the
+    // config (topology, then tokens_per_gpu; sim.cpp:24-32), then the homes
     if (E < 1) return invalid("num_experts must be >= 1, got " + std::to_string(E));
     if (L < 2) return invalid("num_layers must be >= 2, got " + std::to_string(L));
     if (T < 1) return invalid("trace contains no token paths");
     for (int64_t i = 0; i < T * (int64_t)L; ++i)
         if (h_paths[i] < 0 || h_paths[i] >= E)
             return invalid("expert id out of range [0," + std::to_string(E) + ")");
-    if (num_nodes < 1 || gpus_per_node < 1)
-        return invalid("topology must have at least one node and one GPU per node");
-    if (intra_cost < 0.0 || inter_cost < intra_cost)
-        return invalid("hop costs must satisfy inter >= intra >= 0");
-    if (tokens_per_gpu < 1) return invalid("tokens_per_gpu must be >= 1");
+    if (num_nodes < 1 || gpus_per_node < 1) return invalid("placement grid must be at least 1x1");
     const int32_t gpus = num_nodes * gpus_per_node;
     if (E % gpus != 0)
         return invalid("num_experts " + std::to_string(E) + " not divisible by total GPUs " +
                        std::to_string(gpus));
     const int32_t cap = E / gpus;
     std::vector<int32_t> load(gpus);
-    for (int32_t j = 0; j < L; ++j) {  // Placement::validate, placement.cpp:434-470
+    for (int32_t j = 0; j < L; ++j) {
         std::fill(load.begin(), load.end(), 0);
         for (int32_t e = 0; e < E; ++e) {
             const int32_t g = h_assign[j * E + e];
@@ -182,33 +180,29 @@ extern "C" exf_status exf_simulate_host(const int32_t* h_paths, int64_t T, int32
                                " experts on gpu " + std::to_string(g) + ", expected " +
                                std::to_string(cap));
     }
+    if (intra_cost < 0.0 || inter_cost < intra_cost)
+        return invalid("hop costs must satisfy inter >= intra >= 0");
+    if (tokens_per_gpu < 1) return invalid("tokens_per_gpu must be >= 1");
     if (h_homes)
         for (int64_t t = 0; t < T; ++t)
             if (h_homes[t] < 0 || h_homes[t] >= gpus) return invalid("home gpu out of range");
     const size_t paths_b = (size_t)T * L * 4, assign_b = (size_t)L * E * 4;
     const size_t homes_b = h_homes ? (size_t)T * 4 : 0;
-    uint8_t* buf = nullptr;
-    EXF_CUDA_TRY(cudaMalloc(&buf, paths_b + assign_b + homes_b + sizeof(exf_sim_counters) + 64));
+    const size_t cnt_off = (paths_b + assign_b + homes_b + 15) & ~size_t(15);
+    HostScratch* hs = nullptr;  // cached per thread and device: no per-call cudaMalloc
+    EXF_TRY(host_scratch(cnt_off + sizeof(exf_sim_counters) + 64, paths_b, &hs));
+    uint8_t* buf = hs->dev;
     int32_t* d_paths = reinterpret_cast<int32_t*>(buf);
     int32_t* d_assign = reinterpret_cast<int32_t*>(buf + paths_b);
     int32_t* d_homes = h_homes ? reinterpret_cast<int32_t*>(buf + paths_b + assign_b) : nullptr;
-    exf_sim_counters* d_out = reinterpret_cast<exf_sim_counters*>(
-        buf + ((paths_b + assign_b + homes_b + 15) & ~size_t(15)));
-    exf_status st = EXF_OK;
+    exf_sim_counters* d_out = reinterpret_cast<exf_sim_counters*>(buf + cnt_off);
     exf_sim_counters c{};
-    cudaError_t e = cudaMemcpy(d_paths, h_paths, paths_b, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(d_assign, h_assign, assign_b, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && h_homes) e = cudaMemcpy(d_homes, h_homes, homes_b, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) st = cuda_status(e, "cudaMemcpy H2D");
-    if (st == EXF_OK)
-        st = exf_route_replay(d_paths, d_homes, d_assign, T, L, E, num_nodes, gpus_per_node, mode,
-                              d_out, nullptr);
-    if (st == EXF_OK) {
-        e = cudaMemcpy(&c, d_out, sizeof(c), cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) st = cuda_status(e, "cudaMemcpy D2H counters");
-    }
-    cudaFree(buf);
-    if (st != EXF_OK) return st;
+    EXF_TRY(hs->h2d(d_paths, h_paths, paths_b));
+    EXF_TRY(hs->h2d(d_assign, h_assign, assign_b));
+    if (h_homes) EXF_TRY(hs->h2d(d_homes, h_homes, homes_b));
+    EXF_TRY(exf_route_replay(d_paths, d_homes, d_assign, T, L, E, num_nodes, gpus_per_node, mode,
+                             d_out, hs->stream));
+    EXF_TRY(hs->d2h(&c, d_out, sizeof(c)));
     return exf_sim_report_from_counters(&c, T, L, num_nodes, gpus_per_node, intra_cost,
                                         inter_cost, tokens_per_gpu, mode, out);
 }

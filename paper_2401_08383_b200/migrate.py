@@ -85,6 +85,11 @@ def migrate_nccl(model, new_assign: np.ndarray, group=None) -> int:
     for mv in moves:
         by_layer.setdefault(mv[0], []).append(mv)
     torch.cuda.synchronize()
+    # every rank joins one collective on the group first: PyTorch creates the
+    # NCCL communicator lazily, and its first batch_isend_irecv must include
+    # every rank of the group (a rank without moves in the first moving layer
+    # would otherwise leave the others' communicator init hanging)
+    dist.barrier(group=group)
     for j, mvs in sorted(by_layer.items()):
         ops, staged = [], []
         for (_, e, src, ss, dst, ds) in mvs:

@@ -166,3 +166,37 @@ def test_ipc_entry_points_validate_without_gpu():
         _capi.call("exf_ipc_import", None, 0, None)
     with pytest.raises(_capi.ExflowInvalidArgument, match="ipc_close: null"):
         _capi.call("exf_ipc_close", None, 0)
+
+
+@pytest.mark.gpu
+def test_workspace_reuse_with_changing_token_count():
+    """One workspace reused while the resident token count changes (it does
+    every coherent decode step): N=8 then N=4 then N=12 at C=1024 (split
+    grid). The arrival counters sit at a fixed offset and are reset per call,
+    so stale partials of an earlier, larger call can never be read as counters
+    (attention.cu)."""
+    import torch
+    from paper_2401_08383_b200 import _capi
+    from paper_2401_08383_b200.attention import coherent_attention
+    dev = "cuda:0"
+    S, H, Dh, Cap = 16, 4, 64, 1024
+    g = torch.Generator().manual_seed(21)
+    k = torch.randn(S, H, Cap, Dh, generator=g).to(torch.bfloat16)
+    v = torch.randn(S, H, Cap, Dh, generator=g).to(torch.bfloat16)
+    ctx = torch.full((S,), Cap, dtype=torch.int32)
+    lib = _capi.load()
+    big = max(lib.exf_coherent_attention_workspace_bytes(n, H, Dh, Cap) for n in (4, 8, 12))
+    assert big > 0
+    ws = torch.full((big,), 0x7f, dtype=torch.uint8, device=dev)  # garbage, never zeroed
+    kd, vd, cd = k.to(dev), v.to(dev), ctx.to(dev)
+    for N in (8, 4, 12, 4):
+        q = torch.randn(N, H, Dh, generator=g).to(torch.bfloat16)
+        seq = torch.randperm(S, generator=g)[:N].to(torch.int32)
+        out = torch.full((N, H, Dh), float("nan"), dtype=torch.bfloat16, device=dev)
+        coherent_attention(q.to(dev), seq.to(dev), cd, kd, vd, out=out, workspace=ws)
+        torch.cuda.synchronize()
+        ref = oatt.coherent_attention(q.float().numpy(), seq.numpy(), ctx.numpy(),
+                                      k.float().numpy(), v.float().numpy(), Dh ** -0.5)
+        got = out.float().cpu().numpy()
+        assert np.isfinite(got).all(), f"N={N}: merge did not run"
+        assert np.abs(got - ref).max() <= 1e-2 * max(np.abs(ref).max(), 1.0)
