@@ -115,6 +115,17 @@ exf_status exf_simulate_host(const int32_t* h_paths, int64_t T, int32_t L, int32
                              int32_t tokens_per_gpu, int32_t mode, const int32_t* h_homes,
                              exf_sim_report* out);
 
+/* token_hops, proj/src/sim.cpp:34-76 (proj/include/exflow/sim.hpp:28-30):
+ * the per-token hop semantics the replay kernel sums. h_path [L] expert ids
+ * of one token, its home GPU, h_assign [L][E]; per layer j: h_crossed[j]
+ * (0/1), h_tier[j] (0 intra-GPU, 1 intra-node, 2 inter-node) and h_hops[j]
+ * (vanilla: 2 when the expert is away from home; coherent: 1 when it is
+ * away from the token's current GPU, which then becomes the token's GPU).
+ * Host-only; validation and messages as the reference. */
+exf_status exf_token_hops(const int32_t* h_path, int32_t L, int32_t home, const int32_t* h_assign,
+                          int32_t E, int32_t num_nodes, int32_t gpus_per_node, int32_t mode,
+                          int32_t* h_crossed, int32_t* h_tier, int32_t* h_hops);
+
 /* ------------------------------------------------------------------------
  * Host (CPU) placement table and integer-program placement solver. These
  * stay on the CPU (BASELINE.json north_star); they consume the GPU

@@ -81,6 +81,7 @@ SIGNATURES = {
                                                _VP]),
     "exf_simulate_host": (C.c_int, [_VP, _I64, _I32, _I32, _VP, _I32, _I32, _D, _D, _I32, _I32,
                                     _VP, _VP]),
+    "exf_token_hops": (C.c_int, [_VP, _I32, _I32, _VP, _I32, _I32, _I32, _I32, _VP, _VP, _VP]),
     "exf_contiguous_placement": (C.c_int, [_I32, _I32, _I32, _I32, _VP]),
     "exf_random_placement": (C.c_int, [_I32, _I32, _I32, _I32, C.c_uint64, _VP]),
     "exf_validate_placement": (C.c_int, [_VP, _I32, _I32, _I32, _I32]),

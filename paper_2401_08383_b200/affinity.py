@@ -116,6 +116,21 @@ class SimReport:
         return self.hops_intra_node + self.hops_inter_node
 
 
+def token_hops(path, home_gpu: int, assign: np.ndarray, mode: int, topology: "Topology"):
+    """exflow::token_hops (proj/src/sim.cpp:34-76) through exf_token_hops:
+    per layer (crossed, tier, hops); tier 0 intra-GPU, 1 intra-node, 2 inter-node."""
+    p = np.ascontiguousarray(path, dtype=np.int32)
+    a = np.ascontiguousarray(assign, dtype=np.int32)
+    L = p.shape[0]
+    if a.ndim != 2:
+        raise _capi.ExflowInvalidArgument("assign must be [L][E]")
+    crossed, tier, hops = (np.zeros(L, np.int32) for _ in range(3))
+    _capi.call("exf_token_hops", p.ctypes.data, L, home_gpu, a.ctypes.data, a.shape[1],
+               topology.num_nodes, topology.gpus_per_node, mode, crossed.ctypes.data,
+               tier.ctypes.data, hops.ctypes.data)
+    return crossed.astype(bool), tier, hops
+
+
 @dataclass
 class Topology:
     """proj/include/exflow/placement.hpp:16-25."""

@@ -168,6 +168,24 @@ exf_status exf_solve_staged(const int64_t* h_counts, int32_t L, int32_t E, int32
     });
 }
 
+exf_status exf_token_hops(const int32_t* h_path, int32_t L, int32_t home, const int32_t* h_assign,
+                          int32_t E, int32_t nodes, int32_t gpn, int32_t mode, int32_t* h_crossed,
+                          int32_t* h_tier, int32_t* h_hops) {
+    return guarded([&] {
+        if (!h_path || !h_assign || L < 1) throw std::invalid_argument("null argument");
+        if (mode != 0 && mode != 1) throw std::invalid_argument("mode must be 0 (vanilla) or 1 (coherent)");
+        const auto hops = exflow::token_hops(std::span<const int32_t>(h_path, static_cast<size_t>(L)), home,
+                                             load(h_assign, L, E, nodes, gpn),
+                                             mode == 0 ? exflow::SimMode::vanilla : exflow::SimMode::coherent,
+                                             topo(nodes, gpn));
+        for (int32_t j = 0; j < L; ++j) {
+            if (h_crossed) h_crossed[j] = hops[j].crossed ? 1 : 0;
+            if (h_tier) h_tier[j] = static_cast<int32_t>(hops[j].tier);
+            if (h_hops) h_hops[j] = hops[j].hops;
+        }
+    });
+}
+
 exf_status exf_generate_markov_trace(int32_t E, int32_t L, int64_t T, double alpha,
                                      int32_t groups, uint64_t seed, int32_t* h_paths) {
     return guarded([&] {
