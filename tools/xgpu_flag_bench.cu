@@ -50,7 +50,7 @@ struct Args {
 //   pres  [2][G]       u64   per-source presence masks + epoch (variant 3, 64-bit epoch | count)
 //   ctr   [2]          u32   local arrival counters (variant 3)
 struct Layout {
-    size_t rows, sflag, cflag, pres, ctr, total;
+    size_t rows, sflag, cflag, pres, pacc, ctr, total;
 };
 __host__ __device__ inline Layout layout(int G, int C, int d) {
     Layout l{};
@@ -60,6 +60,7 @@ __host__ __device__ inline Layout layout(int G, int C, int d) {
     l.sflag = take((size_t)2 * G * C * 8);
     l.cflag = take((size_t)2 * G * kCtas * 8);
     l.pres = take((size_t)2 * G * 8 * 8);
+    l.pacc = take((size_t)2 * 8 * 4 * 8);
     l.ctr = take(64);
     l.total = o;
     return l;
@@ -87,15 +88,12 @@ __device__ __forceinline__ int dest_of(const Args& a, int t, int r) {
 }
 
 __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(Args a) {
-    __shared__ uint8_t pad[150 * 1024];  // one CTA per SM, like the fused kernel
-    if (threadIdx.x == 0) pad[0] = 0;
     const Layout L = layout(a.G, a.C, a.d);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int t0 = blockIdx.x * a.tpc;
     const int K = a.G * a.C;
     uint8_t* own = a.peers[a.me];
     __shared__ int s_dest[32];
-    __shared__ int s_ok;
     const uint64_t t_start = ptx::globaltimer();
     for (int r = 0; r < a.rounds; ++r) {
         const int par = r & 1;
@@ -141,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(Args a) {
                 // published by the last arriving CTA of this GPU
                 __shared__ int s_last;
                 uint32_t* ctr = reinterpret_cast<uint32_t*>(own + L.ctr) + par;
-                unsigned long long* pm = reinterpret_cast<unsigned long long*>(own + L.pres) + (size_t)par * 8 * 8;
+                unsigned long long* pm = reinterpret_cast<unsigned long long*>(own + L.pacc) + (size_t)par * 8 * 4;
                 if (tid < a.G) {
                     uint32_t mask = 0;
                     for (int i = 0; i < a.tpc; ++i)
@@ -240,6 +238,7 @@ int main(int argc, char** argv) {
         cudaMalloc(&outs[g], 64);
         cudaStreamCreate(&streams[g]);
         cudaFuncSetAttribute(exchange_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(exchange_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
     }
     printf("G=%d B=%d C=%d tpc=%d cross=%.2f (%s)\n", G, B, C, tpc, cross,
            cudaGetErrorString(cudaGetLastError()));
@@ -269,7 +268,7 @@ int main(int argc, char** argv) {
                 a.cross = cross;
                 for (int h = 0; h < G; ++h) a.peers[h] = bufs[h];
                 a.out = outs[g];
-                exchange_kernel<<<kCtas, kThreads, 0, streams[g]>>>(a);
+                exchange_kernel<<<kCtas, kThreads, 150 * 1024, streams[g]>>>(a);  // one CTA per SM
             }
             long long worst = 0;
             for (int g = 0; g < G; ++g) {
