@@ -524,6 +524,7 @@ def measure_routing_kernels(hbm_peak, stream, T=1 << 21, L=24, iters=10):
     CPU: the reference's loops (C restatement, all host threads, integer sums)
     on the same trace. Algorithmic bytes: histogram 4*T*L (ids) + 8*(L-1)*E*(E+1)
     (counts + row totals); replay 4*T*L + 4*L*E (placement)."""
+    import numpy as np
     import torch
     from paper_2401_08383_b200 import _capi, placement as pl
     from oracle import oracle as orc

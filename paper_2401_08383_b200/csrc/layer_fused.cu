@@ -299,7 +299,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         ptx::tma_prefetch_desc(&tmA2);
         // before the PDL wait: issued mid-token-phase, the 160 KB bursts of the
         // token-owning CTAs delayed every flag poll behind them by ~4 us
-        prefetch_a();
+        if (DENSE || a.xpre >= 0) prefetch_a();
     }
 
     // ---------------- dependent part
@@ -309,6 +309,9 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // the i-cache, runs while the previous layer drains), the token/epilogue
     // warps at entry.
     if (!DENSE) ptx::pdl_wait();
+    // (diagnostics, EXF_XPRE=-1: weight prefetch only once the previous layer
+    // is complete, so its tail does not compete with the prefetch traffic)
+    if (!DENSE && a.xpre < 0 && warp == 0 && lane == 0) prefetch_a();
     ptx::pdl_trigger();
     mark3(1);
     if (tid == 0) tl_mark(a.tl, 1);
@@ -1020,7 +1023,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 if (ts2 && et == 0 && job == 1) ts2[11] = ptx::globaltimer();
                 ptx::mbar_wait(&tmem_full[buf], (job / NBUF) & 1, a.err, 110);
                 if (ts2 && et == 0 && job == 0) ts2[10] = ptx::globaltimer();
-                if (DENSE && ts4 && et == 0 && job < 8) ts4[2 * job] = ptx::globaltimer();
+                if (ts4 && et == 0 && job < (DENSE ? 8 : 4)) ts4[2 * job] = ptx::globaltimer();
                 ptx::tc_fence_after();
                 const uint32_t t_base = tmem + buf * NMAX + ((uint32_t)lane_base << 16);
                 auto tmem16 = [&](int col, float (&v)[16]) {
@@ -1055,6 +1058,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     }
                     release_tmem();
                     asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (!DENSE && ts4 && et == 0 && job < 4) ts4[8 + 2 * job] = ptx::globaltimer();
                     if (et == 0) {
                         // release this piece's partials; only the last arriver
                         // acquires (one load on the counter)
@@ -1064,8 +1068,9 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         if (s_flag) a.item_ctr[slot] = 0;  // next use is a later launch
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (!DENSE && ts4 && et == 0 && job < 4) ts4[9 + 2 * job] = ptx::globaltimer();
                     if (!s_flag) {
-                        if (DENSE && ts4 && et == 0 && job < 8) ts4[2 * job + 1] = ptx::globaltimer() | (1ull << 62);
+                        if (ts4 && et == 0 && job < (DENSE ? 8 : 4)) ts4[2 * job + 1] = ptx::globaltimer() | (1ull << 62);
                         continue;
                     }
                     from_ws = true;
@@ -1112,6 +1117,29 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         for (int i = 0; i < kG; ++i) v[i] = __uint_as_float(r[i]);
                     }
                 };
+                // split-K finisher: the k-ordered sum of all Sg partials for 16
+                // columns with up to 64 loads in flight (the 4-column rolled
+                // loop paid one L2 round trip per 4 columns: ~6 us for a
+                // 32-token tile at N=4, the layer's tail). Same addition order
+                // as final4, so the same bits.
+                auto fin16 = [&](int c0, float (&sv)[16]) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) sv[i] = 0.f;
+                    for (int k0 = 0; k0 < Sg; k0 += 4) {
+                        float pk[4][16];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                pk[k][i] = (k0 + k < Sg && c0 + i < nc)
+                                               ? __ldcg(w0 + (int64_t)(k0 + k) * NMAX * kBM + (c0 + i) * kBM) : 0.f;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (k0 + k < Sg) sv[i] += pk[k][i];
+                    }
+                };
                 if (g == 0) {
                     if (DENSE) {
                         // dense GEMM1 covered every resident token: keep the
@@ -1148,8 +1176,23 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     }
                     // dispatch path, or a split-K finisher: every column (dense
                     // keeps the routed ones), values from TMEM or the partials
+                    if (from_ws) {
 #pragma unroll 1
-                    for (int col = 0; col < (routed_only ? 0 : nc); col += kG) {
+                        for (int c0 = 0; c0 < nc; c0 += 16) {
+                            float sv[16];
+                            fin16(c0, sv);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) {
+                                const int j = cb + c0 + i;
+                                const int slot_j = DENSE ? s_exp[j < a.C ? j : 0] : e;
+                                const int pos_j = DENSE ? s_pos[j < a.C ? j : 0] : off_e + j;
+                                if (c0 + i < nc && slot_j == e)
+                                    a.H[(int64_t)pos_j * a.dff + m_glob] = __float2bfloat16(gelu_erf(sv[i] + bias));
+                            }
+                        }
+                    }
+#pragma unroll 1
+                    for (int col = 0; col < (routed_only || from_ws ? 0 : nc); col += kG) {
                         float v[kG];
                         final4(col, v);
                         // branch-free: independent GELUs and row lookups, then
@@ -1194,10 +1237,35 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     const __nv_bfloat16* xres = DENSE ? a.res_x_in : rx;
-                    // (16 columns per round with every load in flight measured
-                    // slower: 30.7 vs 28.0 us/layer)
+                    if (from_ws) {  // finisher: 16 columns per L2 round trip
+                        if (!DENSE && ts4 && et == 0 && job == 0) ts4[12] = ptx::globaltimer();
 #pragma unroll 1
-                    for (int col = 0; col < nc; col += kG) {
+                        for (int c0 = 0; c0 < nc; c0 += 16) {
+                            __nv_bfloat16 xin[16];  // residual loads in flight with the partials
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (c0 + i < nc) xin[i] = xres[s_rrow[c0 + i] * a.d + m_glob];
+                            float sv[16];
+                            fin16(c0, sv);
+                            if (!DENSE && ts4 && et == 0 && job == 0 && c0 == 0) {
+                                float z = 0.f;
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) z += sv[i];
+                                ts4[15] = ptx::globaltimer() | (z == 12345.f ? 1ull : 0ull);
+                            }
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (c0 + i < nc)
+                                    a.res_x_out[(int64_t)(off_e + cb + c0 + i) * a.d + m_glob] = __float2bfloat16(
+                                        __bfloat162float(xin[i]) + s_rprob[c0 + i] * (sv[i] + bias));
+                            if (!DENSE && ts4 && et == 0 && job == 0 && c0 == 0) ts4[13] = ptx::globaltimer();
+                        }
+                        if (!DENSE && ts4 && et == 0 && job == 0) ts4[14] = ptx::globaltimer();
+                    }
+                    // (16 columns per round with every load in flight measured
+                    // slower here, straight from TMEM: 30.7 vs 28.0 us/layer)
+#pragma unroll 1
+                    for (int col = 0; col < (from_ws ? 0 : nc); col += kG) {
                         __nv_bfloat16 xin[kG];  // residual loads in flight first
 #pragma unroll
                         for (int i = 0; i < kG; ++i)
@@ -1214,7 +1282,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     if (!DENSE && mt == 0 && et < nc)  // dense: the token's own CTA wrote it
                         a.res_meta_out[off_e + cb + et] = ResMeta{s_rtok[et], s_rexp[et]};
                 }
-                if (DENSE && ts4 && et == 0 && job < 8) ts4[2 * job + 1] = ptx::globaltimer() | ((uint64_t)from_ws << 63);
+                if (ts4 && et == 0 && job < (DENSE ? 8 : 4)) ts4[2 * job + 1] = ptx::globaltimer() | ((uint64_t)from_ws << 63);
             }
         }
         if (ts2 && et == 0) ts2[12] = ptx::globaltimer();
@@ -1310,6 +1378,10 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
     double kSw = kSwitch;
     if (const char* s = std::getenv("EXF_KSWITCH")) kSw = std::atof(s);
     std::vector<double> free_at(ctas, 0.0), done1(E_loc, 0.0);
+    // EXF_TIE_IDLE=1: ties on the start time go to the most idle CTA (measured
+    // no gain at N=4: 37.8 vs 38.5 us/layer, N=1 flat; off by default)
+    bool tie_idle = false;
+    if (const char* s = std::getenv("EXF_TIE_IDLE")) tie_idle = std::atoi(s) != 0;
     std::vector<std::vector<Piece>> per(ctas);
     // EXF_FILL2=1: GEMM2 as a stream-K fill (below); measured slower at
     // configs[1] (48.3 vs 45.8 us/layer): long GEMM2 runs stall on hdone
@@ -1337,7 +1409,12 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
                     double best_start = 1e300;
                     for (int c = 0; c < ctas; ++c) {
                         const double st = std::max(free_at[c], ready);
-                        if (st < best_start - 1e-9) {
+                        // (tie_idle: with E_loc <= 2 GEMM2's pieces then land on
+                        // CTAs of their own instead of behind the same CTA's
+                        // GEMM1 piece)
+                        const bool earlier = st < best_start - 1e-9;
+                        const bool idler = tie_idle && st < best_start + 1e-9 && free_at[c] < free_at[best] - 1e-9;
+                        if (earlier || idler) {
                             best_start = st;
                             best = c;
                         }

@@ -86,6 +86,34 @@ def main():
                     print(f"  epilogue job {j} {nm:8s} ctas {sel.sum():3d}: acc ready {np.median((st - mma_end)[sel]) / 1e3:5.2f} "
                           f"after last MMA, duration median {np.median((en - st)[sel]) / 1e3:5.2f} max "
                           f"{((en - st)[sel]).max() / 1e3:5.2f} us")
+    if G > 1:  # dispatch path: epilogue per job: acc ready, park done, counter done, done
+        t4 = buf[4]
+        for j in range(4):
+            st = t4[:, 2 * j].astype(np.int64)
+            en_raw = t4[:, 2 * j + 1]
+            ok = (st > 0) & (en_raw > 0)
+            if not ok.any():
+                break
+            kind = (en_raw >> np.uint64(62)).astype(np.int64)
+            en = (en_raw & np.uint64((1 << 62) - 1)).astype(np.int64)
+            pk = t4[:, 8 + 2 * j].astype(np.int64)
+            ct = t4[:, 9 + 2 * j].astype(np.int64)
+            for kd, nm in ((0, "direct"), (2, "finisher"), (1, "park")):
+                sel = ok & (kind == kd)
+                if sel.any():
+                    hasp = sel & (pk > 0)
+                    print(f"  epilogue job {j} {nm:8s} ctas {sel.sum():3d}: acc ready {np.median((st - t[:, 3 + 2 * j])[sel]) / 1e3:5.2f} "
+                          f"after last MMA, duration median {np.median((en - st)[sel]) / 1e3:5.2f} max "
+                          f"{((en - st)[sel]).max() / 1e3:5.2f} us" +
+                          (f"; park {np.median((pk - st)[hasp]) / 1e3:5.2f} counter {np.median((ct - pk)[hasp]) / 1e3:5.2f}"
+                           if hasp.any() else "") + f"; done rel first entry max {((en[sel] - t0) / 1e3).max():.2f}")
+                    if kd == 2 and j == 0:
+                        f12, f13, f14 = (t4[:, k].astype(np.int64) for k in (12, 13, 14))
+                        f15 = t4[:, 15].astype(np.int64)
+                        print(f"    finisher: partial sums of the first 16 columns ready {np.median((f15 - f12)[sel]) / 1e3:5.2f} us after loop start")
+                        print(f"    finisher: counter -> loop start {np.median((f12 - ct)[sel]) / 1e3:5.2f}, first 16 cols "
+                              f"{np.median((f13 - f12)[sel]) / 1e3:5.2f}, loop end {np.median((f14 - f12)[sel]) / 1e3:5.2f}, "
+                              f"-> done {np.median((en - f14)[sel]) / 1e3:5.2f} us; ncols? n/a")
     t5 = buf[5].astype(np.int64)
     print("  token-row stage issue (emptyB passed) rel. job 0 first MMA, median us, it 0..15:",
           [round(float(np.median((t5[:, i] - t[:, 2]) / 1e3)), 2) for i in range(16)])

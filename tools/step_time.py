@@ -22,9 +22,18 @@ def main():
     from paper_2401_08383_b200 import placement as pl
     from paper_2401_08383_b200.affinity import Topology
     from paper_2401_08383_b200.model import MoeModel, MoeModelConfig
+    G = int(os.environ.get("WORLD_SIZE", "1"))  # under torchrun: one process per GPU
+    rank = int(os.environ.get("RANK", "0"))
+    if G > 1:
+        import torch.distributed as dist
+        from paper_2401_08383_b200 import dist as xd
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+        dist.init_process_group("gloo")
     cfg = MoeModelConfig(num_experts=a.experts, num_layers=a.layers, d_model=a.d_model, d_ffn=a.d_ffn,
-                         tokens_per_gpu=a.batch, seed=1234, gate_affinity=0.8)
-    m = MoeModel(cfg, pl.contiguous_placement(a.experts, a.layers, Topology(1, 1)))
+                         tokens_per_gpu=a.batch, seed=1234, gate_affinity=0.8, world_size=G, rank=rank)
+    m = MoeModel(cfg, pl.contiguous_placement(a.experts, a.layers, Topology(1, G)))
+    if G > 1:
+        m.connect(xd.exchange_handles(m.ipc_handle()))
     x = torch.randn(a.batch, a.d_model).to(torch.bfloat16).cuda()
     s = torch.cuda.Stream()
     for _ in range(3):
@@ -41,9 +50,15 @@ def main():
     e1.synchronize()
     m.check()
     us = e0.elapsed_time(e1) * 1000.0 / a.reps
+    if G > 1:
+        t = torch.tensor([us], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        us = float(t.item())
+        if rank != 0:
+            return
     knobs = {k: v for k, v in os.environ.items() if k.startswith("EXF_")}
-    wbytes = a.experts * 2 * a.d_model * a.d_ffn * 2  # every expert active (weights dominate)
-    print(f"step {us:.1f} us  ({us / a.layers:.2f} us/layer, {a.batch / us * 1e6:.0f} tok/s, "
+    wbytes = a.experts // G * 2 * a.d_model * a.d_ffn * 2  # every local expert active (weights dominate)
+    print(f"G={G} step {us:.1f} us  ({us / a.layers:.2f} us/layer, {a.batch * G / us * 1e6:.0f} tok/s, "
           f"weights {wbytes / (us / a.layers * 1e-6) / 1e12:.2f} TB/s, {m.describe().get('path')}"
           f"{' dense' if m.describe().get('layer_kernel', {}).get('dense') else ''})  {knobs}")
 

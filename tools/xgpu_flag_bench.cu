@@ -214,6 +214,110 @@ __global__ void __launch_bounds__(kThreads, 1) exchange_kernel(Args a) {
     if (tid == 0 && blockIdx.x == 0) a.out[0] = (long long)(ptx::globaltimer() - t_start);
 }
 
+
+// ---------------------------------------------------------------------------
+// Protocol matrix (variant = 100 + rows*100 + pub*10 + poll):
+//   rows  0 none, 1 token rows stored first
+//   pub   0 per-slot st.release.sys by distinct threads after bar.sync
+//         1 per-slot st.relaxed.sys
+//         2 per-(CTA, dest) st.release.sys by thread 0..G-1 after bar.sync
+//         3 per-(CTA, dest) st.relaxed.sys
+//         4 per-slot st.release.sys by the warp that wrote the row (lane 0)
+//   poll  0 every thread: relaxed spin + ld.acquire.sys per flag
+//         1 every thread: relaxed spin only
+//         2 warp 0 of each CTA polls, bar.sync releases the rest
+//         3 CTA 0 polls everything, then a GPU-scope broadcast flag
+__global__ void __launch_bounds__(kThreads, 1) matrix_kernel(Args a, int rows_on, int pub, int poll,
+                                                             uint64_t* bcast) {
+    const Layout L = layout(a.G, a.C, a.d);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int t0 = blockIdx.x * a.tpc;
+    uint8_t* own = a.peers[a.me];
+    __shared__ int s_dest[32];
+    const bool per_cta = pub == 2 || pub == 3;
+    const int nflags = per_cta ? a.G * (int)gridDim.x : a.G * a.C;
+    const uint64_t t_start = ptx::globaltimer();
+    for (int r = 0; r < a.rounds; ++r) {
+        const int par = r & 1;
+        const uint64_t ep = (uint64_t)r + 1;
+        if (tid < a.tpc) s_dest[tid] = (t0 + tid < a.B) ? dest_of(a, t0 + tid, r) : -1;
+        __syncthreads();
+        for (int i = warp; i < a.tpc; i += kThreads / 32) {
+            const int g = s_dest[i];
+            if (rows_on && g >= 0) {
+                int4* dst = reinterpret_cast<int4*>(a.peers[g] + L.rows +
+                                                     (((size_t)par * a.G + a.me) * a.C + t0 + i) * a.d * 2);
+                const int4 v = make_int4(r, t0 + i, a.me, 7);
+                for (int u = lane; u < a.d / 8; u += 32) dst[u] = v;
+            }
+            if (pub == 4 && t0 + i < a.C) {
+                __syncwarp();
+                if (lane < a.G) {
+                    const uint64_t slotv = (g == lane) ? 1u : 0xFFu;
+                    uint64_t* f = reinterpret_cast<uint64_t*>(a.peers[lane] + L.sflag) +
+                                  ((size_t)par * a.G + a.me) * a.C + t0 + i;
+                    st_release_sys64(f, (ep << 40) | (slotv << 32));
+                }
+            }
+        }
+        __syncthreads();
+        if (pub == 0 || pub == 1) {
+            for (int q = kThreads - 1 - tid; q < a.tpc * a.G; q += kThreads) {
+                const int i = q / a.G, g = q - i * a.G;
+                if (t0 + i >= a.C) continue;
+                const uint64_t slotv = (s_dest[i] == g) ? 1u : 0xFFu;
+                uint64_t* f = reinterpret_cast<uint64_t*>(a.peers[g] + L.sflag) + ((size_t)par * a.G + a.me) * a.C + t0 + i;
+                if (pub == 0) st_release_sys64(f, (ep << 40) | (slotv << 32));
+                else st_relaxed_sys(f, (ep << 40) | (slotv << 32));
+            }
+        } else if (per_cta && tid < a.G) {
+            const int g = tid;
+            uint32_t mask = 0;
+            for (int i = 0; i < a.tpc; ++i)
+                if (s_dest[i] == g) mask |= 1u << i;
+            uint64_t* f = reinterpret_cast<uint64_t*>(a.peers[g] + L.cflag) + ((size_t)par * a.G + a.me) * kCtas + blockIdx.x;
+            if (pub == 2) st_release_sys64(f, (ep << 40) | mask);
+            else st_relaxed_sys(f, (ep << 40) | mask);
+        }
+        const uint64_t* f = reinterpret_cast<const uint64_t*>(own + (per_cta ? L.cflag : L.sflag)) +
+                            (size_t)par * (per_cta ? a.G * kCtas : a.G * a.C);
+        auto flag_at = [&](int k) {
+            return per_cta ? f + (k / (int)gridDim.x) * kCtas + (k % (int)gridDim.x) : f + k;
+        };
+        if (poll == 0 || poll == 1) {
+            for (int k = tid; k < nflags; k += kThreads) {
+                ptx::SpinGuard g;
+                while ((ptx::ld_relaxed_u64(flag_at(k), true) >> 40) != ep) g.step(nullptr, 0, 2000000000ull);
+                if (poll == 0) (void)ld_acquire_sys64(flag_at(k));
+            }
+        } else if (poll == 2) {
+            if (warp == 0) {
+                for (int k = lane; k < nflags; k += 32) {
+                    ptx::SpinGuard g;
+                    while ((ptx::ld_relaxed_u64(flag_at(k), true) >> 40) != ep) g.step(nullptr, 0, 2000000000ull);
+                    (void)ld_acquire_sys64(flag_at(k));
+                }
+            }
+        } else {
+            if (blockIdx.x == 0) {
+                for (int k = tid; k < nflags; k += kThreads) {
+                    ptx::SpinGuard g;
+                    while ((ptx::ld_relaxed_u64(flag_at(k), true) >> 40) != ep) g.step(nullptr, 0, 2000000000ull);
+                    (void)ld_acquire_sys64(flag_at(k));
+                }
+                __syncthreads();
+                if (tid == 0) asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(bcast), "l"(ep) : "memory");
+            } else if (tid == 0) {
+                ptx::SpinGuard g;
+                while (ptx::ld_relaxed_u64(bcast, false) < ep) g.step(nullptr, 0, 2000000000ull);
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0 && blockIdx.x == 0) a.out[0] = (long long)(ptx::globaltimer() - t_start);
+}
+
 int main(int argc, char** argv) {
     int ndev = 0;
     cudaGetDeviceCount(&ndev);
@@ -285,6 +389,49 @@ int main(int argc, char** argv) {
             if (rep == 1) printf("  v%d %-52s %.2f us per exchange round\n", variant, names[variant],
                                  worst / 1000.0 / rounds);
         }
+    }
+    // protocol matrix
+    std::vector<uint64_t*> bc(G);
+    for (int g = 0; g < G; ++g) {
+        cudaSetDevice(g);
+        cudaMalloc(&bc[g], 64);
+        cudaFuncSetAttribute(matrix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
+    }
+    const int combos[][3] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 0}, {1, 0, 1}, {1, 0, 2}, {1, 0, 3}, {1, 4, 0},
+                             {1, 4, 2}, {1, 2, 0}, {1, 2, 2}, {1, 2, 3}, {0, 3, 1}, {1, 3, 1}};
+    for (const auto& cb : combos) {
+        double per = 0;
+        for (int rep = 0; rep < 2; ++rep) {
+            const int rounds = rep == 0 ? 20 : 400;
+            for (int g = 0; g < G; ++g) {
+                cudaSetDevice(g);
+                cudaMemset(bufs[g], 0, L.total);
+                cudaMemset(bc[g], 0, 64);
+            }
+            for (int g = 0; g < G; ++g) cudaSetDevice(g), cudaDeviceSynchronize();
+            for (int g = 0; g < G; ++g) {
+                cudaSetDevice(g);
+                Args a{};
+                a.G = G; a.me = g; a.B = B; a.C = C; a.tpc = tpc; a.d = d; a.rounds = rounds; a.cross = cross;
+                for (int h = 0; h < G; ++h) a.peers[h] = bufs[h];
+                a.out = outs[g];
+                matrix_kernel<<<kCtas, kThreads, 150 * 1024, streams[g]>>>(a, cb[0], cb[1], cb[2], bc[g]);
+            }
+            long long worst = 0;
+            for (int g = 0; g < G; ++g) {
+                cudaSetDevice(g);
+                cudaError_t e = cudaStreamSynchronize(streams[g]);
+                if (e != cudaSuccess) {
+                    printf("matrix %d%d%d: %s\n", cb[0], cb[1], cb[2], cudaGetErrorString(e));
+                    return 1;
+                }
+                long long ns = 0;
+                cudaMemcpy(&ns, outs[g], 8, cudaMemcpyDeviceToHost);
+                worst = ns > worst ? ns : worst;
+            }
+            per = worst / 1000.0 / rounds;
+        }
+        printf("  rows=%d pub=%d poll=%d  %.2f us per round\n", cb[0], cb[1], cb[2], per);
     }
     return 0;
 }
