@@ -193,8 +193,10 @@ exf_status exf_generate_markov_trace(int32_t E, int32_t L, int64_t T, double alp
  * on tcgen05 (kernel 4); tokens stay on their expert's GPU (no combine).
  * Per step: context AllGather of the step's token states (kernel 3b).
  * Tokens: rank r owns home tokens r + G*i, i < tokens_per_gpu (round robin,
- * sim.cpp:111). x_in is this rank's [B][d] bf16 home tokens; the output is
- * the [G*B][d] bf16 final states of ALL tokens, indexed by token id.
+ * sim.cpp:111). x_in is this rank's [B][d] home tokens; the output is the
+ * [G*B][d] final states of ALL tokens, indexed by token id. Element type:
+ * bf16, or fp32 with dtype = EXF_DTYPE_F32 (every "bf16" buffer below --
+ * x_in, output, weights, resident rows -- is then fp32).
  * ---------------------------------------------------------------------- */
 typedef struct exf_model exf_model;
 
@@ -213,9 +215,13 @@ typedef struct { /* in the style of SynthConfig (proj/include/exflow/synth.hpp:1
     int32_t ep_mode;         /* EXF_EP_COHERENT (ExFlow: tokens stay on their expert's GPU,
                                 one exchange per layer) or EXF_EP_VANILLA (dispatch + combine
                                 back to the home GPU every layer, proj/src/sim.cpp:60-64) */
+    int32_t dtype;           /* EXF_DTYPE_BF16 (tcgen05 path) or EXF_DTYPE_F32 (fp32 mode:
+                                fp32 weights, token states, gate and FFN; SIMT FFN) */
 } exf_model_config;
 #define EXF_EP_COHERENT 0
 #define EXF_EP_VANILLA 1
+#define EXF_DTYPE_BF16 0
+#define EXF_DTYPE_F32 1
 
 /* assign: [L][E] placement table (exf_contiguous_placement = vanilla,
  * exf_solve_staged = affinity). Allocates weights (generated on device from

@@ -64,6 +64,50 @@ void orc_gate_logits(const uint16_t* x, const uint16_t* wg, int32_t d, int32_t E
     }
 }
 
+static double gelu_erf(double v) { return 0.5 * v * (1.0 + erf(v * 0.70710678118654752440)); }
+
+void orc_gate_logits_f32(const float* x, const float* wg, int32_t d, int32_t E, float* logits) {
+    /* same order as orc_gate_logits: lane l accumulates k = c*256 + l*8 + i
+     * (c-major, i-minor) with fmaf, then the xor butterfly 16..1 */
+    const int32_t chunks = d / 256;
+    for (int32_t e = 0; e < E; ++e) {
+        const float* w = wg + (int64_t)e * d;
+        float lane[32];
+        for (int32_t l = 0; l < 32; ++l) {
+            float acc = 0.0f;
+            for (int32_t c = 0; c < chunks; ++c)
+                for (int32_t i = 0; i < 8; ++i) {
+                    const int32_t k = c * 256 + l * 8 + i;
+                    acc = fmaf(x[k], w[k], acc);
+                }
+            lane[l] = acc;
+        }
+        for (int32_t off = 16; off >= 1; off >>= 1) {
+            float nxt[32];
+            for (int32_t l = 0; l < 32; ++l) nxt[l] = lane[l] + lane[l ^ off];
+            memcpy(lane, nxt, sizeof(lane));
+        }
+        logits[e] = lane[0];
+    }
+}
+
+void orc_expert_ffn_f32(const float* x, const float* w1, const float* b1, const float* w2,
+                        const float* b2, int32_t d, int32_t dff, float prob, double* out) {
+    static double h[65536];
+    for (int32_t m = 0; m < dff; ++m) {
+        const float* w = w1 + (int64_t)m * d;
+        double acc = 0.0;
+        for (int32_t k = 0; k < d; ++k) acc += (double)x[k] * (double)w[k];
+        h[m] = gelu_erf(acc + (double)b1[m]);
+    }
+    for (int32_t n = 0; n < d; ++n) {
+        const float* w = w2 + (int64_t)n * dff;
+        double acc = 0.0;
+        for (int32_t m = 0; m < dff; ++m) acc += h[m] * (double)w[m];
+        out[n] = (double)x[n] + (double)prob * (acc + (double)b2[n]);
+    }
+}
+
 int orc_gate_top1(const float* logits, int32_t E, float* prob) {
     int32_t best = 0;
     for (int32_t e = 1; e < E; ++e)
@@ -74,7 +118,6 @@ int orc_gate_top1(const float* logits, int32_t E, float* prob) {
     return best;
 }
 
-static double gelu_erf(double v) { return 0.5 * v * (1.0 + erf(v * 0.70710678118654752440)); }
 
 void orc_expert_ffn(const uint16_t* x, const uint16_t* w1, const uint16_t* b1,
                     const uint16_t* w2, const uint16_t* b2, int32_t d, int32_t dff,

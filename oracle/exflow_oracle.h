@@ -119,6 +119,13 @@ int orc_gate_top1(const float* logits, int32_t E, float* prob);
 void orc_expert_ffn(const uint16_t* x, const uint16_t* w1, const uint16_t* b1,
                     const uint16_t* w2, const uint16_t* b2, int32_t d, int32_t dff,
                     float prob, uint16_t* out, float* out_f32);
+/* fp32 mode: the same fixed-order fmaf gate on fp32 inputs (products are
+ * rounded inside the fused multiply-add exactly as on the device), and the
+ * expert FFN on fp32 inputs evaluated in fp64 with no intermediate rounding
+ * (the reference the 1e-5 fp32 bar is measured against). */
+void orc_gate_logits_f32(const float* x, const float* wg, int32_t d, int32_t E, float* logits);
+void orc_expert_ffn_f32(const float* x, const float* w1, const float* b1, const float* w2,
+                        const float* b2, int32_t d, int32_t dff, float prob, double* out);
 
 const char* orc_last_error(void);
 

@@ -108,6 +108,9 @@ def lib():
         L.orc_gate_top1.argtypes = [F32P, C.c_int32, C.c_void_p]
         L.orc_expert_ffn.argtypes = [U16P, U16P, U16P, U16P, U16P, C.c_int32, C.c_int32,
                                      C.c_float, C.c_void_p, C.c_void_p]
+        L.orc_gate_logits_f32.argtypes = [F32P, F32P, C.c_int32, C.c_int32, F32P]
+        L.orc_expert_ffn_f32.argtypes = [F32P, F32P, F32P, F32P, F32P, C.c_int32, C.c_int32,
+                                         C.c_float, C.c_void_p]
         _lib = L
     return _lib
 
@@ -332,6 +335,31 @@ def gate_logits(x_bits: np.ndarray, wg_bits: np.ndarray) -> np.ndarray:
     for t in range(n):
         lib().orc_gate_logits(np.ascontiguousarray(x_bits[t]), wg_bits, d, E, row)
         out[t] = row
+    return out
+
+
+def gate_logits_f32(x: np.ndarray, wg: np.ndarray) -> np.ndarray:
+    """fp32-mode gate logits: the fixed fmaf order on fp32 inputs. x [n][d], wg [E][d]."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    wg = np.ascontiguousarray(wg, dtype=np.float32)
+    n, d = x.shape
+    E = wg.shape[0]
+    out = np.empty((n, E), np.float32)
+    row = np.empty(E, np.float32)
+    for t in range(n):
+        lib().orc_gate_logits_f32(np.ascontiguousarray(x[t]), wg, d, E, row)
+        out[t] = row
+    return out
+
+
+def expert_ffn_f32(x, w1, b1, w2, b2, prob) -> np.ndarray:
+    """One fp32 token through one fp32 expert, evaluated in fp64: [d] float64."""
+    d = x.shape[0]
+    dff = w1.shape[0]
+    out = np.empty(d, np.float64)
+    f = lambda a: np.ascontiguousarray(a, dtype=np.float32)
+    lib().orc_expert_ffn_f32(f(x), f(w1), f(b1), f(w2), f(b2), d, dff, float(prob),
+                             out.ctypes.data_as(C.c_void_p))
     return out
 
 

@@ -132,7 +132,8 @@ class ModelConfigC(C.Structure):
     _fields_ = [("num_experts", C.c_int32), ("num_layers", C.c_int32), ("d_model", C.c_int32),
                 ("d_ffn", C.c_int32), ("top_k", C.c_int32), ("tokens_per_gpu", C.c_int32),
                 ("world_size", C.c_int32), ("rank", C.c_int32), ("seed", C.c_uint64),
-                ("init_std", C.c_float), ("gate_affinity", C.c_float), ("ep_mode", C.c_int32)]
+                ("init_std", C.c_float), ("gate_affinity", C.c_float), ("ep_mode", C.c_int32),
+                ("dtype", C.c_int32)]
 
 _lib = None
 

@@ -43,6 +43,17 @@ __device__ __forceinline__ void unpack8(const int4& v, float (&f)[8]) {
     }
 }
 
+// 8 consecutive elements as fp32 (bf16 rows: one 16-byte load; fp32 rows: two)
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
+    unpack8(*reinterpret_cast<const int4*>(p), f);
+}
+__device__ __forceinline__ void load8(const float* p, float (&f)[8]) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
+    f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w;
+    f[4] = b.x, f[5] = b.y, f[6] = b.z, f[7] = b.w;
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %lanemask_lt;" : "=r"(m));
@@ -82,9 +93,11 @@ constexpr int kGdThreads = 512;
 constexpr int kGdWarps = kGdThreads / 32;
 constexpr int kMaxKeys = 64;
 
-template <int EMAX>
+// T: element type of the token rows and the gate (bf16, or fp32 in the fp32
+// mode); the gate reduction order is the same for both (fixed-order fmaf)
+template <int EMAX, typename T>
 __global__ void __launch_bounds__(kGdThreads) gate_dispatch_kernel(LayerArgs a, int wg_in_smem) {
-    // dynamic smem: X [tpc][d] bf16 | meta [tpc] ResMeta | Wg [E][d] bf16 (when it fits)
+    // dynamic smem: X [tpc][d] T | meta [tpc] ResMeta | Wg [E][d] T (when it fits)
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int32_t s_exp[256];
     __shared__ float s_prob[256];
@@ -119,17 +132,17 @@ __global__ void __launch_bounds__(kGdThreads) gate_dispatch_kernel(LayerArgs a, 
 
     // ---- stage this CTA's token rows, their metadata and Wg in shared memory
     //      with one batch of independent 16-byte loads
-    const int vec = a.d >> 3;  // int4 per row
-    __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(smem);
-    ResMeta* smeta = reinterpret_cast<ResMeta*>(smem + (size_t)a.tpc * a.d * 2);
-    const __nv_bfloat16* wg = a.wg;
+    const int vec = a.d * (int)sizeof(T) / 16;  // int4 per row
+    T* sx = reinterpret_cast<T*>(smem);
+    ResMeta* smeta = reinterpret_cast<ResMeta*>(smem + (size_t)a.tpc * a.d * sizeof(T));
+    const T* wg = static_cast<const T*>(a.wg);
     {
-        const int4* xs = reinterpret_cast<const int4*>(a.res_x_in + (int64_t)t0 * a.d);
+        const int4* xs = reinterpret_cast<const int4*>(static_cast<const T*>(a.res_x_in) + (int64_t)t0 * a.d);
         int4* xd = reinterpret_cast<int4*>(sx);
         for (int i = tid; i < nt * vec; i += kGdThreads) xd[i] = xs[i];
         for (int i = tid; i < nt; i += kGdThreads) smeta[i] = a.res_meta_in[t0 + i];
         if (wg_in_smem && nt > 0) {
-            __nv_bfloat16* swg = reinterpret_cast<__nv_bfloat16*>(smem + (size_t)a.tpc * (a.d * 2 + 8));
+            T* swg = reinterpret_cast<T*>(smem + (size_t)a.tpc * (a.d * sizeof(T) + 8));
             const int4* src = reinterpret_cast<const int4*>(a.wg);
             int4* dst = reinterpret_cast<int4*>(swg);
             for (int i = tid; i < E * vec; i += kGdThreads) dst[i] = __ldg(src + i);
@@ -144,18 +157,18 @@ __global__ void __launch_bounds__(kGdThreads) gate_dispatch_kernel(LayerArgs a, 
     const int chunks = a.d >> 8;
     for (int i = warp; i < nt; i += kGdWarps) {
         const int t = t0 + i;
-        const __nv_bfloat16* x = sx + (int64_t)i * a.d;
+        const T* x = sx + (int64_t)i * a.d;
         float acc[EMAX];
 #pragma unroll
         for (int e = 0; e < EMAX; ++e) acc[e] = 0.f;
         for (int c = 0; c < chunks; ++c) {
             float xf[8];
-            unpack8(*reinterpret_cast<const int4*>(x + c * 256 + lane * 8), xf);
+            load8(x + c * 256 + lane * 8, xf);
 #pragma unroll
             for (int e = 0; e < EMAX; ++e) {
                 if (e < E) {
                     float wf[8];
-                    unpack8(*reinterpret_cast<const int4*>(wg + (int64_t)e * a.d + c * 256 + lane * 8), wf);
+                    load8(wg + (int64_t)e * a.d + c * 256 + lane * 8, wf);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) acc[e] = fmaf(xf[k], wf[k], acc[e]);
                 }
@@ -252,7 +265,7 @@ __global__ void __launch_bounds__(kGdThreads) gate_dispatch_kernel(LayerArgs a, 
 
     // ---- (3) rows straight from shared memory into the destination's
     //      receive region (P2P stores for remote destinations)
-    const int64_t row_bytes = (int64_t)a.d * 2;
+    const int64_t row_bytes = (int64_t)a.d * sizeof(T);
     for (int i = warp; i < nt; i += kGdWarps) {
         const int key = s_pos[i] >> 20;
         const int dest = key / a.E_loc;
@@ -311,12 +324,12 @@ __global__ void __launch_bounds__(kGdThreads) gate_dispatch_kernel(LayerArgs a, 
 // ------------------------------------------------------------------ step begin
 // Home tokens of this rank: global ids rank + G*i (round-robin homes, t % G;
 // proj/src/sim.cpp:111).
-__global__ void step_begin_kernel(const __nv_bfloat16* __restrict__ x_in, __nv_bfloat16* res_x,
-                                  ResMeta* res_meta, int32_t* n_res, int B, int d, int G,
+// (rows are copied as 16-byte vectors: vec = row bytes / 16, bf16 or fp32)
+__global__ void step_begin_kernel(const void* __restrict__ x_in, void* res_x,
+                                  ResMeta* res_meta, int32_t* n_res, int B, int vec, int G,
                                   int rank) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
-    const int vec = d >> 3;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)B * vec;
          i += (int64_t)gridDim.x * blockDim.x)
         reinterpret_cast<int4*>(res_x)[i] = reinterpret_cast<const int4*>(x_in)[i];
@@ -329,14 +342,13 @@ __global__ void step_begin_kernel(const __nv_bfloat16* __restrict__ x_in, __nv_b
 
 // ------------------------------------------------------------------ context AllGather
 __global__ void __launch_bounds__(512) gather_send_kernel(
-    const __nv_bfloat16* __restrict__ res_x, const ResMeta* __restrict__ res_meta,
-    const int32_t* n_res, uint8_t* const* peers, Symm sym, int G, int rank, int d, int C,
+    const void* __restrict__ res_x, const ResMeta* __restrict__ res_meta,
+    const int32_t* n_res, uint8_t* const* peers, Symm sym, int G, int rank, int vec, int C,
     const uint64_t* step, int32_t* done_ctr, int32_t* err) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
     const int n = *n_res;
-    const int vec = d >> 3;
     for (int64_t w = (int64_t)blockIdx.x * nwarp + warp; w < (int64_t)n * G;
          w += (int64_t)gridDim.x * nwarp) {
         const int r = (int)(w / G), p = (int)(w - (int64_t)r * G);
@@ -345,8 +357,8 @@ __global__ void __launch_bounds__(512) gather_send_kernel(
             if (lane == 0) atomicExch(err, ERR_CAPACITY);
             continue;
         }
-        int4* dst = reinterpret_cast<int4*>(peers[p] + sym.gather_x + (int64_t)tok * d * 2);
-        const int4* src = reinterpret_cast<const int4*>(res_x + (int64_t)r * d);
+        int4* dst = reinterpret_cast<int4*>(peers[p] + sym.gather_x) + (int64_t)tok * vec;
+        const int4* src = reinterpret_cast<const int4*>(res_x) + (int64_t)r * vec;
         for (int v = lane; v < vec; v += 32) dst[v] = src[v];
     }
     if (G > 1) __threadfence_system(); else __threadfence();
@@ -386,8 +398,8 @@ __global__ void gather_wait_kernel(uint8_t* own_sym, Symm sym, int G, uint64_t* 
 // by a per-slot release flag {epoch = step * L + layer + 1}: the home rank
 // needs no counts, it waits for its B slots.
 __global__ void __launch_bounds__(256) combine_send_kernel(
-    const __nv_bfloat16* __restrict__ res_x, const ResMeta* __restrict__ res_meta, const int32_t* n_res,
-    uint8_t* const* peers, Symm sym, int G, int B, int d, int L, int layer, const uint64_t* step,
+    const void* __restrict__ res_x, const ResMeta* __restrict__ res_meta, const int32_t* n_res,
+    uint8_t* const* peers, Symm sym, int G, int B, int vec, int L, int layer, const uint64_t* step,
     int32_t* err) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
@@ -395,7 +407,6 @@ __global__ void __launch_bounds__(256) combine_send_kernel(
     const int n = *n_res;
     const uint64_t epoch = *step * (uint64_t)L + (uint64_t)layer + 1;
     const int par = layer & 1;
-    const int vec = d >> 3;
     for (int r = blockIdx.x * nwarp + warp; r < n; r += gridDim.x * nwarp) {
         const ResMeta m = res_meta[r];
         if ((unsigned)m.token >= (unsigned)(B * G)) {
@@ -404,8 +415,8 @@ __global__ void __launch_bounds__(256) combine_send_kernel(
         }
         const int home = m.token % G, slot = m.token / G;
         uint8_t* base = peers[home];
-        int4* dst = reinterpret_cast<int4*>(base + sym.comb_x + ((int64_t)par * B + slot) * d * 2);
-        const int4* src = reinterpret_cast<const int4*>(res_x + (int64_t)r * d);
+        int4* dst = reinterpret_cast<int4*>(base + sym.comb_x) + ((int64_t)par * B + slot) * vec;
+        const int4* src = reinterpret_cast<const int4*>(res_x) + (int64_t)r * vec;
         for (int v = lane; v < vec; v += 32) dst[v] = src[v];
         if (lane == 0) reinterpret_cast<ResMeta*>(base + sym.comb_meta)[par * B + slot] = m;
         __syncwarp();  // the warp's row stores precede lane 0's release
@@ -419,14 +430,13 @@ __global__ void __launch_bounds__(256) combine_send_kernel(
 // Home side: wait for the B slots, then copy them (home order) into the
 // resident buffers the next layer reads.
 __global__ void __launch_bounds__(256) combine_wait_kernel(
-    const uint8_t* own_sym, Symm sym, int G, int B, int d, int L, int layer, const uint64_t* step,
-    __nv_bfloat16* res_x_next, ResMeta* res_meta_next, int32_t* n_res_next, int32_t* err) {
+    const uint8_t* own_sym, Symm sym, int G, int B, int vec, int L, int layer, const uint64_t* step,
+    void* res_x_next, ResMeta* res_meta_next, int32_t* n_res_next, int32_t* err) {
     ptx::pdl_wait();
     ptx::pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
     const uint64_t epoch = *step * (uint64_t)L + (uint64_t)layer + 1;
     const int par = layer & 1;
-    const int vec = d >> 3;
     for (int slot = blockIdx.x * nwarp + warp; slot < B; slot += gridDim.x * nwarp) {
         const uint64_t* f = reinterpret_cast<const uint64_t*>(own_sym + sym.comb_flags) + par * B + slot;
         if (lane == 0) {
@@ -435,8 +445,8 @@ __global__ void __launch_bounds__(256) combine_wait_kernel(
             (void)ptx::flag_read(f, G > 1);  // acquire on the flag itself
         }
         __syncwarp();
-        const int4* src = reinterpret_cast<const int4*>(own_sym + sym.comb_x + ((int64_t)par * B + slot) * d * 2);
-        int4* dst = reinterpret_cast<int4*>(res_x_next + (int64_t)slot * d);
+        const int4* src = reinterpret_cast<const int4*>(own_sym + sym.comb_x) + ((int64_t)par * B + slot) * vec;
+        int4* dst = reinterpret_cast<int4*>(res_x_next) + (int64_t)slot * vec;
         for (int v = lane; v < vec; v += 32) dst[v] = src[v];
         if (lane == 0) res_meta_next[slot] = reinterpret_cast<const ResMeta*>(own_sym + sym.comb_meta)[par * B + slot];
     }
@@ -456,24 +466,25 @@ int gate_dispatch_tpc(int C) {
     return std::max(16, std::min(tpc, 256));
 }
 
-exf_status launch_gate_dispatch(const LayerArgs& a, cudaStream_t s) {
+template <typename T>
+exf_status launch_gate_dispatch_t(const LayerArgs& a, cudaStream_t s) {
     if (a.E > kMaxKeys) return invalid("at most 64 experts");
     if (a.tpc < 16 || a.tpc > 256) return invalid("bad gate_dispatch tile");
     const int grid = (a.C + a.tpc - 1) / a.tpc;
     if (grid > 128) return invalid("G*B exceeds the gate_dispatch capacity (128 CTAs)");
-    const size_t x_bytes = (size_t)a.tpc * (2 * a.d + 8);
+    const size_t x_bytes = (size_t)a.tpc * (sizeof(T) * a.d + 8);
     if (x_bytes > kGdSmemBudget) return invalid("gate_dispatch token slice does not fit in shared memory");
-    const size_t wg_bytes = (size_t)a.E * a.d * 2;
+    const size_t wg_bytes = (size_t)a.E * a.d * sizeof(T);
     const int in_smem = x_bytes + wg_bytes <= kGdSmemBudget ? 1 : 0;
     const size_t smem = x_bytes + (in_smem ? wg_bytes : 0);
-    void (*k)(LayerArgs, int) = a.E <= 8    ? gate_dispatch_kernel<8>
-                                : a.E <= 16 ? gate_dispatch_kernel<16>
-                                : a.E <= 32 ? gate_dispatch_kernel<32>
-                                            : gate_dispatch_kernel<64>;
+    void (*k)(LayerArgs, int) = a.E <= 8    ? gate_dispatch_kernel<8, T>
+                                : a.E <= 16 ? gate_dispatch_kernel<16, T>
+                                : a.E <= 32 ? gate_dispatch_kernel<32, T>
+                                            : gate_dispatch_kernel<64, T>;
     static bool attr = false;
     if (!attr) {
-        for (auto kk : {gate_dispatch_kernel<8>, gate_dispatch_kernel<16>, gate_dispatch_kernel<32>,
-                        gate_dispatch_kernel<64>}) {
+        for (auto kk : {gate_dispatch_kernel<8, T>, gate_dispatch_kernel<16, T>, gate_dispatch_kernel<32, T>,
+                        gate_dispatch_kernel<64, T>}) {
             EXF_CUDA_TRY(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)kGdSmemBudget));
             max_carveout(kk);
@@ -487,36 +498,40 @@ exf_status launch_gate_dispatch(const LayerArgs& a, cudaStream_t s) {
     return EXF_OK;
 }
 
-exf_status launch_step_begin(const __nv_bfloat16* x_in, __nv_bfloat16* res_x, ResMeta* res_meta,
-                             int32_t* n_res, int B, int d, int G, int rank, cudaStream_t s) {
-    const int blocks = std::max(1, std::min(148, (int)(((int64_t)B * (d >> 3) + 255) / 256)));
+exf_status launch_gate_dispatch(const LayerArgs& a, cudaStream_t s) {
+    return a.esz == 4 ? launch_gate_dispatch_t<float>(a, s) : launch_gate_dispatch_t<__nv_bfloat16>(a, s);
+}
+
+exf_status launch_step_begin(const void* x_in, void* res_x, ResMeta* res_meta,
+                             int32_t* n_res, int B, int vec, int G, int rank, cudaStream_t s) {
+    const int blocks = std::max(1, std::min(148, (int)(((int64_t)B * vec + 255) / 256)));
     EXF_CUDA_TRY(launch_pdl(step_begin_kernel, dim3(blocks), dim3(256), 0, s, 0, x_in, res_x,
-                            res_meta, n_res, B, d, G, rank));
+                            res_meta, n_res, B, vec, G, rank));
     return EXF_OK;
 }
 
-exf_status launch_gather_send(const __nv_bfloat16* res_x, const ResMeta* res_meta,
+exf_status launch_gather_send(const void* res_x, const ResMeta* res_meta,
                               const int32_t* n_res, uint8_t* const* peers, const Symm& sym, int G,
-                              int rank, int d, int C, const uint64_t* step, int32_t* done_ctr,
+                              int rank, int vec, int C, const uint64_t* step, int32_t* done_ctr,
                               int32_t* err, cudaStream_t s) {
     const int blocks = std::max(1, std::min(132, (C * G + 15) / 16));
     EXF_CUDA_TRY(launch_pdl(gather_send_kernel, dim3(blocks), dim3(512), 0, s, 0, res_x, res_meta,
-                            n_res, peers, sym, G, rank, d, C, step, done_ctr, err));
+                            n_res, peers, sym, G, rank, vec, C, step, done_ctr, err));
     return EXF_OK;
 }
 
-exf_status launch_combine(const __nv_bfloat16* res_x_out, const ResMeta* res_meta_out, const int32_t* n_res_out,
-                          uint8_t* const* peers, uint8_t* own_sym, const Symm& sym, int G, int B, int d, int L,
-                          int layer, const uint64_t* step, __nv_bfloat16* res_x_next, ResMeta* res_meta_next,
+exf_status launch_combine(const void* res_x_out, const ResMeta* res_meta_out, const int32_t* n_res_out,
+                          uint8_t* const* peers, uint8_t* own_sym, const Symm& sym, int G, int B, int vec, int L,
+                          int layer, const uint64_t* step, void* res_x_next, ResMeta* res_meta_next,
                           int32_t* n_res_next, int32_t* err, int part, cudaStream_t s) {
     const int blocks = std::max(1, std::min(148, (B * G + 7) / 8));
     if (part == 0) {
         EXF_CUDA_TRY(launch_pdl(combine_send_kernel, dim3(blocks), dim3(256), 0, s, 0, res_x_out, res_meta_out,
-                                n_res_out, peers, sym, G, B, d, L, layer, step, err));
+                                n_res_out, peers, sym, G, B, vec, L, layer, step, err));
         return EXF_OK;
     }
     EXF_CUDA_TRY(launch_pdl(combine_wait_kernel, dim3(std::max(1, std::min(148, (B + 7) / 8))), dim3(256), 0, s, 0,
-                            (const uint8_t*)own_sym, sym, G, B, d, L, layer, step, res_x_next, res_meta_next,
+                            (const uint8_t*)own_sym, sym, G, B, vec, L, layer, step, res_x_next, res_meta_next,
                             n_res_next, err));
     return EXF_OK;
 }

@@ -23,16 +23,17 @@ namespace exf {
 
 exf_status launch_gate_dispatch(const LayerArgs& a, cudaStream_t s);
 int gate_dispatch_tpc(int C);
-exf_status launch_step_begin(const __nv_bfloat16* x_in, __nv_bfloat16* res_x, ResMeta* res_meta,
-                             int32_t* n_res, int B, int d, int G, int rank, cudaStream_t s);
-exf_status launch_gather_send(const __nv_bfloat16* res_x, const ResMeta* res_meta,
+exf_status launch_step_begin(const void* x_in, void* res_x, ResMeta* res_meta,
+                             int32_t* n_res, int B, int vec, int G, int rank, cudaStream_t s);
+exf_status launch_gather_send(const void* res_x, const ResMeta* res_meta,
                               const int32_t* n_res, uint8_t* const* peers, const Symm& sym, int G,
-                              int rank, int d, int C, const uint64_t* step, int32_t* done_ctr,
+                              int rank, int vec, int C, const uint64_t* step, int32_t* done_ctr,
                               int32_t* err, cudaStream_t s);
-exf_status launch_combine(const __nv_bfloat16* res_x_out, const ResMeta* res_meta_out, const int32_t* n_res_out,
-                          uint8_t* const* peers, uint8_t* own_sym, const Symm& sym, int G, int B, int d, int L,
-                          int layer, const uint64_t* step, __nv_bfloat16* res_x_next, ResMeta* res_meta_next,
+exf_status launch_combine(const void* res_x_out, const ResMeta* res_meta_out, const int32_t* n_res_out,
+                          uint8_t* const* peers, uint8_t* own_sym, const Symm& sym, int G, int B, int vec, int L,
+                          int layer, const uint64_t* step, void* res_x_next, ResMeta* res_meta_next,
                           int32_t* n_res_next, int32_t* err, int part, cudaStream_t s);
+exf_status launch_ffn_f32(const FfnF32Args& a, int mode, cudaStream_t s);
 exf_status launch_gather_wait(uint8_t* own_sym, const Symm& sym, int G, uint64_t* step,
                               int32_t* err, cudaStream_t s);
 exf_status make_weight_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols);
@@ -66,22 +67,29 @@ __device__ __forceinline__ float hnormal(uint64_t seed, uint64_t key, int64_t i)
     return (float)(sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2));
 }
 
-__global__ void init_normal_kernel(__nv_bfloat16* out, int64_t n, uint64_t seed, uint64_t key,
-                                   float stdv) {
+__device__ __forceinline__ void put(__nv_bfloat16* p, float v) { *p = __float2bfloat16(v); }
+__device__ __forceinline__ void put(float* p, float v) { *p = v; }
+__device__ __forceinline__ float get(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ float get(const float* p) { return *p; }
+
+// T = bf16 or fp32 (fp32 mode): the same N(0, std^2) draws, rounded to T
+template <typename T>
+__global__ void init_normal_kernel(T* out, int64_t n, uint64_t seed, uint64_t key, float stdv) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = __float2bfloat16(stdv * hnormal(seed, key, i));
+        put(out + i, stdv * hnormal(seed, key, i));
 }
 
 // planted inter-layer gate correlation: cur[perm[e]] = rho*prev[e] + sqrt(1-rho^2)*noise
-__global__ void gate_mix_kernel(const __nv_bfloat16* prev, __nv_bfloat16* cur, const int32_t* perm,
+template <typename T>
+__global__ void gate_mix_kernel(const T* prev, T* cur, const int32_t* perm,
                                 int E, int d, float rho, float stdv, uint64_t seed, uint64_t key) {
     const float beta = sqrtf(fmaxf(0.f, 1.f - rho * rho));
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)E * d;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int e = (int)(i / d), k = (int)(i - (int64_t)e * d);
         const int64_t dst = (int64_t)perm[e] * d + k;
-        cur[dst] = __float2bfloat16(rho * __bfloat162float(prev[i]) + beta * stdv * hnormal(seed, key, dst));
+        put(cur + dst, rho * get(prev + i) + beta * stdv * hnormal(seed, key, dst));
     }
 }
 
@@ -100,6 +108,7 @@ constexpr int kTimelineCtas = 4096;
 struct exf_model {
     exf_model_config cfg{};
     int E_loc = 0, C = 0;
+    int esz = 2;                            // element bytes: 2 (bf16) or 4 (fp32 mode)
     int device = 0;
     // placement
     std::vector<int32_t> assign;            // [L][E]
@@ -112,6 +121,8 @@ struct exf_model {
     __nv_bfloat16* b1 = nullptr;            // [L][E_loc][dff]
     __nv_bfloat16* w2 = nullptr;            // [L][E_loc][d][dff]
     __nv_bfloat16* b2 = nullptr;            // [L][E_loc][d]
+    // fp32 mode: the same tensors in fp32 (the bf16 ones are not allocated)
+    float *wg32 = nullptr, *w1_32 = nullptr, *b1_32 = nullptr, *w2_32 = nullptr, *b2_32 = nullptr;
     std::vector<CUtensorMap> tmap1, tmap2;  // per layer (weights, TMA tiles)
     CUtensorMap gmap_recv{}, gmap_h{};      // token rows for TMA gather4
     CUtensorMap tmap_x[2]{}, tmap_ht{};     // dense fused mode: resident rows / H as B tiles
@@ -190,9 +201,12 @@ exf_status validate_config(const exf_model_config& c) {
     if (!(c.gate_affinity >= 0.f && c.gate_affinity <= 1.f)) return invalid("gate_affinity must be in [0,1]");
     if (c.ep_mode != EXF_EP_COHERENT && c.ep_mode != EXF_EP_VANILLA)
         return invalid("ep_mode must be EXF_EP_COHERENT (0) or EXF_EP_VANILLA (1)");
+    if (c.dtype != EXF_DTYPE_BF16 && c.dtype != EXF_DTYPE_F32)
+        return invalid("dtype must be EXF_DTYPE_BF16 (0) or EXF_DTYPE_F32 (1)");
     {
         const int64_t C = (int64_t)c.tokens_per_gpu * c.world_size;
-        if (C > 128LL * 256 || (int64_t)gate_dispatch_tpc((int)C) * (2 * c.d_model + 8) > 200 * 1024)
+        const int64_t esz = c.dtype == EXF_DTYPE_F32 ? 4 : 2;
+        if (C > 128LL * 256 || (int64_t)gate_dispatch_tpc((int)C) * (esz * c.d_model + 8) > 200 * 1024)
             return invalid("G*B = " + std::to_string(C) + " tokens exceeds the dispatch capacity for d_model " +
                            std::to_string(c.d_model));
     }
@@ -208,15 +222,16 @@ exf_status build_layout(exf_model* m) {
         o += (bytes + 255) & ~int64_t(255);
         return at;
     };
-    m->sym.recv_x = take(2LL * G * C * d * 2);
+    const int64_t esz = m->esz;
+    m->sym.recv_x = take(2LL * G * C * d * esz);
     m->sym.recv_meta = take(2LL * G * C * (int64_t)sizeof(RecvMeta));
     m->sym.recv_cnt = take(2LL * G * m->E_loc * 4);
     m->sym.flags = take(2LL * G * 8);
-    m->sym.gather_x = take((int64_t)C * d * 2);
+    m->sym.gather_x = take((int64_t)C * d * esz);
     m->sym.gflags = take((int64_t)G * 8);
     m->sym.cflags = take(2LL * G * std::max<int64_t>(C, kMaxCtas) * 8);  // route flags [2][G][max(C, 256)]
     const int64_t B = c.tokens_per_gpu;
-    m->sym.comb_x = take(2LL * B * d * 2);
+    m->sym.comb_x = take(2LL * B * d * esz);
     m->sym.comb_meta = take(2LL * B * (int64_t)sizeof(ResMeta));
     m->sym.comb_flags = take(2LL * B * 8);
     m->sym.total = o;
@@ -260,7 +275,8 @@ exf_status set_placement(exf_model* m, const int32_t* h_assign) {
     return EXF_OK;
 }
 
-exf_status init_weights(exf_model* m) {
+template <typename T>
+exf_status init_weights_t(exf_model* m, T* wg, T* w1, T* b1, T* w2, T* b2) {
     const auto& c = m->cfg;
     const int L = c.num_layers, E = c.num_experts, d = c.d_model, f = c.d_ffn;
     const int blocks = 148 * 8;
@@ -268,15 +284,15 @@ exf_status init_weights(exf_model* m) {
         for (int s = 0; s < m->E_loc; ++s) {
             const int e = m->local[j][s];
             const int64_t ls = (int64_t)j * m->E_loc + s;
-            init_normal_kernel<<<blocks, 256>>>(m->w1 + ls * f * d, (int64_t)f * d, c.seed, weight_key(j, e, E, 0), c.init_std);
-            init_normal_kernel<<<blocks, 256>>>(m->b1 + ls * f, f, c.seed, weight_key(j, e, E, 1), c.init_std);
-            init_normal_kernel<<<blocks, 256>>>(m->w2 + ls * d * f, (int64_t)d * f, c.seed, weight_key(j, e, E, 2), c.init_std);
-            init_normal_kernel<<<blocks, 256>>>(m->b2 + ls * d, d, c.seed, weight_key(j, e, E, 3), c.init_std);
+            init_normal_kernel<<<blocks, 256>>>(w1 + ls * f * d, (int64_t)f * d, c.seed, weight_key(j, e, E, 0), c.init_std);
+            init_normal_kernel<<<blocks, 256>>>(b1 + ls * f, (int64_t)f, c.seed, weight_key(j, e, E, 1), c.init_std);
+            init_normal_kernel<<<blocks, 256>>>(w2 + ls * d * f, (int64_t)d * f, c.seed, weight_key(j, e, E, 2), c.init_std);
+            init_normal_kernel<<<blocks, 256>>>(b2 + ls * d, (int64_t)d, c.seed, weight_key(j, e, E, 3), c.init_std);
         }
     // gate: logits ~ N(0,1) for unit-variance inputs; planted affinity with a
     // hidden per-layer expert permutation
     const float gstd = 1.0f / std::sqrt((float)d);
-    init_normal_kernel<<<blocks, 256>>>(m->wg, (int64_t)E * d, c.seed, gate_key(0), gstd);
+    init_normal_kernel<<<blocks, 256>>>(wg, (int64_t)E * d, c.seed, gate_key(0), gstd);
     int32_t* d_perm = nullptr;
     EXF_CUDA_TRY(cudaMalloc(&d_perm, sizeof(int32_t) * E));
     for (int j = 1; j < L; ++j) {
@@ -285,12 +301,21 @@ exf_status init_weights(exf_model* m) {
         exflow::Rng rng(exflow::seed_stream(c.seed, 1000u + (uint64_t)j));
         exflow::shuffle(std::span<int>(perm), rng);
         EXF_CUDA_TRY(cudaMemcpy(d_perm, perm.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice));
-        gate_mix_kernel<<<blocks, 256>>>(m->wg + (int64_t)(j - 1) * E * d, m->wg + (int64_t)j * E * d,
+        gate_mix_kernel<<<blocks, 256>>>(wg + (int64_t)(j - 1) * E * d, wg + (int64_t)j * E * d,
                                          d_perm, E, d, c.gate_affinity, gstd, c.seed, gate_key(j));
     }
-    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    const cudaError_t se = cudaDeviceSynchronize();
     cudaFree(d_perm);
+    EXF_CUDA_TRY(se);
     EXF_LAUNCH_CHECK("init kernels");
+    return EXF_OK;
+}
+
+exf_status init_weights(exf_model* m) {
+    const auto& c = m->cfg;
+    const int L = c.num_layers, d = c.d_model, f = c.d_ffn;
+    if (m->esz == 4) return init_weights_t(m, m->wg32, m->w1_32, m->b1_32, m->w2_32, m->b2_32);
+    EXF_TRY(init_weights_t(m, m->wg, m->w1, m->b1, m->w2, m->b2));
     for (int j = 0; j < L; ++j) {
         EXF_TRY(make_weight_tmap(&m->tmap1[j], m->w1 + (int64_t)j * m->E_loc * f * d, (int64_t)m->E_loc * f, d));
         EXF_TRY(make_weight_tmap(&m->tmap2[j], m->w2 + (int64_t)j * m->E_loc * d * f, (int64_t)m->E_loc * d, f));
@@ -311,7 +336,9 @@ LayerArgs layer_args(exf_model* m, int j) {
     a.L = c.num_layers;
     a.layer = j;
     a.forced = m->forced_on ? 1 : 0;
-    a.wg = m->wg + (int64_t)j * c.num_experts * c.d_model;
+    a.esz = m->esz;
+    a.wg = m->esz == 4 ? static_cast<const void*>(m->wg32 + (int64_t)j * c.num_experts * c.d_model)
+                       : static_cast<const void*>(m->wg + (int64_t)j * c.num_experts * c.d_model);
     a.gpu_of = m->d_gpu_of + j * c.num_experts;
     a.slot_of = m->d_slot_of + j * c.num_experts;
     a.res_x_in = m->res_x[j & 1];
@@ -362,6 +389,31 @@ FfnArgs ffn_args(exf_model* m, int j, int mode) {
     a.err = m->err;
     a.tstamp = m->tstamp ? m->tstamp + (int64_t)mode * kTimelineCtas * 16 : nullptr;
     a.tl = m->tl ? m->tl + (int64_t)(j * 3 + 1 + mode) * 8 : nullptr;
+    return a;
+}
+
+FfnF32Args ffn_f32_args(exf_model* m, int j, int mode) {
+    const auto& c = m->cfg;
+    FfnF32Args a{};
+    a.G = c.world_size;
+    a.rank = c.rank;
+    a.E_loc = m->E_loc;
+    a.C = m->C;
+    a.d = c.d_model;
+    a.dff = c.d_ffn;
+    a.L = c.num_layers;
+    a.layer = j;
+    a.own_sym = m->sym_base;
+    a.sym = m->sym;
+    a.step = m->step;
+    const int64_t f = c.d_ffn, d = c.d_model;
+    a.w = mode == 0 ? m->w1_32 + (int64_t)j * m->E_loc * f * d : m->w2_32 + (int64_t)j * m->E_loc * d * f;
+    a.bias = mode == 0 ? m->b1_32 + (int64_t)j * m->E_loc * f : m->b2_32 + (int64_t)j * m->E_loc * d;
+    a.H = reinterpret_cast<float*>(m->H);
+    a.res_x_out = reinterpret_cast<float*>(m->res_x[(j + 1) & 1]);
+    a.res_meta_out = m->res_meta[(j + 1) & 1];
+    a.n_res_out = m->n_res + ((j + 1) & 1);
+    a.err = m->err;
     return a;
 }
 
@@ -434,8 +486,8 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
         }
         case 0:
             if (!x_in) return invalid("null input");
-            return launch_step_begin(static_cast<const __nv_bfloat16*>(x_in), m->res_x[0], m->res_meta[0],
-                                     m->n_res, c.tokens_per_gpu, c.d_model, c.world_size, c.rank, s);
+            return launch_step_begin(x_in, m->res_x[0], m->res_meta[0], m->n_res, c.tokens_per_gpu,
+                                     c.d_model * m->esz / 16, c.world_size, c.rank, s);
         case 1: {
             if (j < 0 || j >= c.num_layers) return invalid("layer out of range");
             const LayerArgs a = layer_args(m, j);
@@ -443,14 +495,18 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
         }
         case 2: {
             if (j < 0 || j >= c.num_layers) return invalid("layer out of range");
+            if (m->esz == 4) {
+                EXF_TRY(launch_ffn_f32(ffn_f32_args(m, j, 0), 0, s));
+                return launch_ffn_f32(ffn_f32_args(m, j, 1), 1, s);
+            }
             EXF_TRY(launch_ffn_gemm(m->tmap1[j], m->gmap_recv, ffn_args(m, j, 0), m->nmax, m->cl1, s));
             return launch_ffn_gemm(m->tmap2[j], m->gmap_h, ffn_args(m, j, 1), m->nmax, m->cl2, s);
         }
         case 3: {
             const int fin = c.num_layers & 1;
             return launch_gather_send(m->res_x[fin], m->res_meta[fin], m->n_res + fin, m->d_peers, m->sym,
-                                      c.world_size, c.rank, c.d_model, m->C, m->step, m->done_ctr + 1,
-                                      m->err, s);
+                                      c.world_size, c.rank, c.d_model * m->esz / 16, m->C, m->step,
+                                      m->done_ctr + 1, m->err, s);
         }
         case 4:
             return launch_gather_wait(m->sym_base, m->sym, c.world_size, m->step, m->err, s);
@@ -460,7 +516,7 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
             if (c.ep_mode != EXF_EP_VANILLA) return invalid("combine phases need ep_mode = EXF_EP_VANILLA");
             const int o = (j + 1) & 1;
             return launch_combine(m->res_x[o], m->res_meta[o], m->n_res + o, m->d_peers, m->sym_base, m->sym,
-                                  c.world_size, c.tokens_per_gpu, c.d_model, c.num_layers, j, m->step,
+                                  c.world_size, c.tokens_per_gpu, c.d_model * m->esz / 16, c.num_layers, j, m->step,
                                   m->res_x[o], m->res_meta[o], m->n_res + o, m->err, phase - 6, s);
         }
         default:
@@ -498,6 +554,8 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     const auto& c = m->cfg;
     m->E_loc = c.num_experts / c.world_size;
     m->C = c.tokens_per_gpu * c.world_size;
+    m->esz = c.dtype == EXF_DTYPE_F32 ? 4 : 2;
+    const size_t ew = (size_t)m->esz / 2;  // bf16-sized elements per stored element
     cudaGetDevice(&m->device);
     const int L = c.num_layers, E = c.num_experts, d = c.d_model, f = c.d_ffn, C = m->C;
     auto fail = [&](exf_status st) {
@@ -513,15 +571,23 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     EXF_M(dalloc(&m->d_gpu_of, (size_t)L * E));
     EXF_M(dalloc(&m->d_slot_of, (size_t)L * E));
     EXF_M(set_placement(m, h_assign));
-    EXF_M(dalloc(&m->wg, (size_t)L * E * d));
-    EXF_M(dalloc(&m->w1, (size_t)L * m->E_loc * f * d));
-    EXF_M(dalloc(&m->b1, (size_t)L * m->E_loc * f));
-    EXF_M(dalloc(&m->w2, (size_t)L * m->E_loc * d * f));
-    EXF_M(dalloc(&m->b2, (size_t)L * m->E_loc * d));
+    if (m->esz == 4) {
+        EXF_M(dalloc(&m->wg32, (size_t)L * E * d));
+        EXF_M(dalloc(&m->w1_32, (size_t)L * m->E_loc * f * d));
+        EXF_M(dalloc(&m->b1_32, (size_t)L * m->E_loc * f));
+        EXF_M(dalloc(&m->w2_32, (size_t)L * m->E_loc * d * f));
+        EXF_M(dalloc(&m->b2_32, (size_t)L * m->E_loc * d));
+    } else {
+        EXF_M(dalloc(&m->wg, (size_t)L * E * d));
+        EXF_M(dalloc(&m->w1, (size_t)L * m->E_loc * f * d));
+        EXF_M(dalloc(&m->b1, (size_t)L * m->E_loc * f));
+        EXF_M(dalloc(&m->w2, (size_t)L * m->E_loc * d * f));
+        EXF_M(dalloc(&m->b2, (size_t)L * m->E_loc * d));
+    }
     m->tmap1.resize(L);
     m->tmap2.resize(L);
     for (int i = 0; i < 2; ++i) {
-        EXF_M(dalloc(&m->res_x[i], (size_t)C * d));
+        EXF_M(dalloc(&m->res_x[i], (size_t)C * d * ew));
         EXF_M(dalloc(&m->res_meta[i], (size_t)C));
     }
     EXF_M(dalloc(&m->n_res, 2));
@@ -542,6 +608,7 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     if (const char* env = std::getenv("EXF_TOKEN_TILE")) m->nmax = std::atoi(env);
     {  // fused layer kernel plan and scratch
         if (const char* env = std::getenv("EXF_FUSED")) m->fused = std::atoi(env) != 0;
+        if (m->esz == 4) m->fused = false;  // fp32 mode: two-kernel path with the SIMT fp32 FFN
         m->f_ctas = fused_ctas();
         // one token per CTA while C <= #SMs: the gate's (token, expert) dot
         // products then spread over 8 warps of many CTAs
@@ -564,7 +631,7 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         const int tok = m->dense ? C : m->nmax;
         const int nmax_f = tok <= 32 ? 32 : (tok <= 64 ? 64 : 128);
         m->f_nmax = nmax_f;
-        EXF_M(dalloc(&m->H, (size_t)C * f));
+        EXF_M(dalloc(&m->H, (size_t)C * f * ew));
         std::vector<Piece> pieces;
         std::vector<int32_t> off;
         if (!build_fused_schedule(m->E_loc, d, f, m->f_ctas, pieces, off, &m->f_max_contrib,
@@ -591,8 +658,10 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     }
     EXF_M(dalloc(&m->d_peers, (size_t)c.world_size));
     EXF_M(build_layout(m));
-    EXF_M(make_gather_tmap(&m->gmap_recv, m->sym_base + m->sym.recv_x, 2LL * c.world_size * C, d));
-    EXF_M(make_gather_tmap(&m->gmap_h, m->H, C, f));
+    if (m->esz == 2) {
+        EXF_M(make_gather_tmap(&m->gmap_recv, m->sym_base + m->sym.recv_x, 2LL * c.world_size * C, d));
+        EXF_M(make_gather_tmap(&m->gmap_h, m->H, C, f));
+    }
     if (m->dense) {
         for (int i = 0; i < 2; ++i) EXF_M(make_tile_tmap(&m->tmap_x[i], m->res_x[i], C, d, m->f_nmax));
         EXF_M(make_tile_tmap(&m->tmap_ht, m->H, C, f, m->f_nmax));
@@ -600,8 +669,10 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     if (cudaMemset(m->trace, 0xff, sizeof(int32_t) * C * L) != cudaSuccess) return fail(EXF_CUDA);
     EXF_M(init_weights(m));
     // split-K / persistent-cluster plan of the two-kernel (phased) path
-    EXF_M(plan_ffn_gemm(m->nmax, 0, m->E_loc * (f / 128), d, &m->ks1, &m->cl1));
-    EXF_M(plan_ffn_gemm(m->nmax, 1, m->E_loc * (d / 128), f, &m->ks2, &m->cl2));
+    if (m->esz == 2) {
+        EXF_M(plan_ffn_gemm(m->nmax, 0, m->E_loc * (f / 128), d, &m->ks1, &m->cl1));
+        EXF_M(plan_ffn_gemm(m->nmax, 1, m->E_loc * (d / 128), f, &m->ks2, &m->cl2));
+    }
     if (c.world_size == 1) {  // a single rank is its own peer
         exf_model* self = m;
         EXF_M(exf_model_connect_local(&self, 1));
@@ -621,7 +692,8 @@ exf_status exf_model_destroy(exf_model* m) {
                     m->hist, m->crossed, m->trace, m->forced, m->step, m->err, m->done_ctr,
                     m->cta_cnt, m->gbar, m->tl, m->ws, m->item_ctr, m->hdone, m->fbar,
                     m->f_cta_cnt, m->f_pieces, m->f_piece_off,
-                    m->d_peers, m->sym_base, m->tstamp};
+                    m->d_peers, m->sym_base, m->tstamp, m->wg32, m->w1_32, m->b1_32, m->w2_32,
+                    m->b2_32};
     for (void* p : bufs)
         if (p) cudaFree(p);
     delete m;
@@ -771,12 +843,15 @@ exf_status exf_model_read_expert(exf_model* m, int32_t layer, int32_t expert, ui
     const auto it = std::find(loc.begin(), loc.end(), expert);
     if (it == loc.end()) return invalid("expert is not placed on this rank");
     const int64_t ls = (int64_t)layer * m->E_loc + (it - loc.begin());
-    const int64_t d = c.d_model, f = c.d_ffn;
+    void *w1, *b1, *w2, *b2;
+    EXF_TRY(exf_model_expert_storage(m, layer, (int32_t)(it - loc.begin()), &w1, &b1, &w2, &b2));
+    (void)ls;
+    const int64_t d = c.d_model, f = c.d_ffn, es = m->esz;
     EXF_CUDA_TRY(cudaDeviceSynchronize());
-    if (h_w1) EXF_CUDA_TRY(cudaMemcpy(h_w1, m->w1 + ls * f * d, f * d * 2, cudaMemcpyDeviceToHost));
-    if (h_b1) EXF_CUDA_TRY(cudaMemcpy(h_b1, m->b1 + ls * f, f * 2, cudaMemcpyDeviceToHost));
-    if (h_w2) EXF_CUDA_TRY(cudaMemcpy(h_w2, m->w2 + ls * d * f, f * d * 2, cudaMemcpyDeviceToHost));
-    if (h_b2) EXF_CUDA_TRY(cudaMemcpy(h_b2, m->b2 + ls * d, d * 2, cudaMemcpyDeviceToHost));
+    if (h_w1) EXF_CUDA_TRY(cudaMemcpy(h_w1, w1, f * d * es, cudaMemcpyDeviceToHost));
+    if (h_b1) EXF_CUDA_TRY(cudaMemcpy(h_b1, b1, f * es, cudaMemcpyDeviceToHost));
+    if (h_w2) EXF_CUDA_TRY(cudaMemcpy(h_w2, w2, f * d * es, cudaMemcpyDeviceToHost));
+    if (h_b2) EXF_CUDA_TRY(cudaMemcpy(h_b2, b2, d * es, cudaMemcpyDeviceToHost));
     return EXF_OK;
 }
 
@@ -788,6 +863,13 @@ exf_status exf_model_expert_storage(exf_model* m, int32_t layer, int32_t slot, v
         return invalid("layer/slot out of range");
     const int64_t ls = (int64_t)layer * m->E_loc + slot;
     const int64_t d = c.d_model, f = c.d_ffn;
+    if (m->esz == 4) {
+        *d_w1 = m->w1_32 + ls * f * d;
+        *d_b1 = m->b1_32 + ls * f;
+        *d_w2 = m->w2_32 + ls * d * f;
+        *d_b2 = m->b2_32 + ls * d;
+        return EXF_OK;
+    }
     *d_w1 = m->w1 + ls * f * d;
     *d_b1 = m->b1 + ls * f;
     *d_w2 = m->w2 + ls * d * f;
@@ -806,7 +888,9 @@ exf_status exf_model_read_gate(exf_model* m, int32_t layer, uint16_t* h_wg) {
     if (layer < 0 || layer >= m->cfg.num_layers) return invalid("layer out of range");
     const int64_t n = (int64_t)m->cfg.num_experts * m->cfg.d_model;
     EXF_CUDA_TRY(cudaDeviceSynchronize());
-    EXF_CUDA_TRY(cudaMemcpy(h_wg, m->wg + layer * n, n * 2, cudaMemcpyDeviceToHost));
+    const void* src = m->esz == 4 ? static_cast<const void*>(m->wg32 + layer * n)
+                                  : static_cast<const void*>(m->wg + layer * n);
+    EXF_CUDA_TRY(cudaMemcpy(h_wg, src, n * m->esz, cudaMemcpyDeviceToHost));
     return EXF_OK;
 }
 
@@ -817,7 +901,7 @@ exf_status exf_model_read_resident(exf_model* m, int32_t which, uint16_t* h_x, i
     int32_t n = 0;
     EXF_CUDA_TRY(cudaMemcpy(&n, m->n_res + which, 4, cudaMemcpyDeviceToHost));
     if (n < 0 || n > m->C) return runtime_err("resident count out of range");
-    if (h_x) EXF_CUDA_TRY(cudaMemcpy(h_x, m->res_x[which], (size_t)n * m->cfg.d_model * 2, cudaMemcpyDeviceToHost));
+    if (h_x) EXF_CUDA_TRY(cudaMemcpy(h_x, m->res_x[which], (size_t)n * m->cfg.d_model * m->esz, cudaMemcpyDeviceToHost));
     if (h_meta) EXF_CUDA_TRY(cudaMemcpy(h_meta, m->res_meta[which], (size_t)n * sizeof(ResMeta), cudaMemcpyDeviceToHost));
     *n_out = n;
     return EXF_OK;
@@ -888,7 +972,7 @@ exf_status exf_model_read_ffn_timeline(exf_model* m, uint64_t* h, int32_t ctas) 
 
 exf_status exf_model_describe(exf_model* m, char* buf, int32_t len) {
     if (!m || !buf || len < 1) return invalid("bad argument");
-    std::string s = "{\"token_tile\": " + std::to_string(m->nmax) +
+    std::string s = "{\"dtype\": \"" + std::string(m->esz == 4 ? "f32" : "bf16") + "\", \"token_tile\": " + std::to_string(m->nmax) +
                     ", \"experts_per_rank\": " + std::to_string(m->E_loc) +
                     ", \"capacity_tokens\": " + std::to_string(m->C) +
                     ", \"ep_mode\": \"" + std::string(m->cfg.ep_mode == EXF_EP_VANILLA ? "vanilla" : "coherent") + "\"";

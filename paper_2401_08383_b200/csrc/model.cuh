@@ -47,11 +47,12 @@ constexpr int kMaxCtas = 256;
 // Everything a kernel needs, passed by value.
 struct LayerArgs {
     int32_t G, rank, E, E_loc, d, dff, C, L, layer, forced;
+    int32_t esz;                    // bytes per element of rows and gate: 2 (bf16) or 4 (fp32 mode)
     // rank-local
-    const __nv_bfloat16* wg;        // [E][d] of this layer
+    const void* wg;                 // [E][d] of this layer
     const int32_t* gpu_of;          // [E] of this layer
     const int32_t* slot_of;         // [E] of this layer
-    __nv_bfloat16* res_x_in;        // [C][d]
+    const void* res_x_in;           // [C][d]
     const ResMeta* res_meta_in;     // [C]
     const int32_t* n_res_in;        // device scalar
     int32_t* expert;                // [C]
@@ -98,6 +99,21 @@ struct FfnArgs {
     int32_t* err;
     uint64_t* tstamp;            // optional per-CTA globaltimer stamps [grid][16] (diagnostics)
     unsigned long long* tl;      // optional step timeline [4] (diagnostics)
+};
+
+// Arguments of one fp32-mode FFN GEMM launch (ffn_f32.cu).
+struct FfnF32Args {
+    int32_t G, rank, E_loc, C, d, dff, L, layer;
+    uint8_t* own_sym;
+    Symm sym;
+    const uint64_t* step;
+    const float* w;        // [E_loc][M][K] of this layer (W1: M = dff, K = d; W2: M = d, K = dff)
+    const float* bias;     // [E_loc][M] of this layer
+    float* H;              // [C][dff] canonical token order
+    float* res_x_out;      // [C][d]  (GEMM2)
+    ResMeta* res_meta_out; //         (GEMM2)
+    int32_t* n_res_out;    //         (GEMM2)
+    int32_t* err;
 };
 
 // One piece of the fused kernel's static stream-K schedule: a contiguous run

@@ -73,6 +73,12 @@ def migrate_local(models: Sequence, new_assign: np.ndarray) -> int:
     return sum(1 for mv in moves if mv[2] != mv[4])
 
 
+def _wire(t):
+    """NCCL-transferable view of a weight slot (int16 bf16 bits -> bfloat16; fp32 as is)."""
+    import torch
+    return t.view(torch.bfloat16) if t.dtype == torch.int16 else t
+
+
 def migrate_nccl(model, new_assign: np.ndarray, group=None) -> int:
     """One process per GPU (every rank calls it with the same table): the old
     owner sends each moved expert's weights over NCCL, the new owner receives
@@ -95,11 +101,11 @@ def migrate_nccl(model, new_assign: np.ndarray, group=None) -> int:
         for (_, e, src, ss, dst, ds) in mvs:
             if src == rank and dst == rank:  # slot shuffle on this GPU
                 staged.append((ds, [t.clone() for t in model.expert_storage(j, ss)]))
-            elif src == rank:  # (bf16 views: NCCL has no int16 type)
+            elif src == rank:  # (bf16 views of int16 storage: NCCL has no int16 type)
                 for t in model.expert_storage(j, ss):
-                    ops.append(dist.P2POp(dist.isend, t.view(torch.bfloat16), dst, group=group))
+                    ops.append(dist.P2POp(dist.isend, _wire(t), dst, group=group))
             elif dst == rank:
-                bufs = [torch.empty_like(t).view(torch.bfloat16) for t in model.expert_storage(j, ds)]
+                bufs = [_wire(torch.empty_like(t)) for t in model.expert_storage(j, ds)]
                 for b in bufs:
                     ops.append(dist.P2POp(dist.irecv, b, src, group=group))
                 staged.append((ds, bufs))
@@ -109,7 +115,7 @@ def migrate_nccl(model, new_assign: np.ndarray, group=None) -> int:
         torch.cuda.synchronize()
         for ds, bufs in staged:
             for d_t, b in zip(model.expert_storage(j, ds), bufs):
-                d_t.copy_(b.view(torch.int16))
+                d_t.copy_(b.view(d_t.dtype))
     torch.cuda.synchronize()
     model.set_placement(new_assign)
     return sum(1 for mv in moves if mv[2] != mv[4])

@@ -18,6 +18,7 @@ from . import _capi
 PHASE_BEGIN, PHASE_DISPATCH, PHASE_FFN, PHASE_GATHER_SEND, PHASE_GATHER_WAIT, PHASE_FUSED, \
     PHASE_COMBINE_SEND, PHASE_COMBINE_WAIT = range(8)
 EP_COHERENT, EP_VANILLA = 0, 1  # include/exflow_c.h EXF_EP_*
+DTYPE_BF16, DTYPE_F32 = 0, 1    # include/exflow_c.h EXF_DTYPE_*
 
 
 @dataclass
@@ -37,10 +38,18 @@ class MoeModelConfig:
     # EP_COHERENT (ExFlow) or EP_VANILLA (dispatch + combine back home every
     # layer, proj/src/sim.cpp:60-64)
     ep_mode: int = 0
+    # DTYPE_BF16 (tcgen05 path) or DTYPE_F32 (fp32 mode: fp32 weights, states,
+    # gate and SIMT FFN; the north star's 1e-5 bar)
+    dtype: int = 0
 
     @property
     def capacity(self) -> int:
         return self.tokens_per_gpu * self.world_size
+
+    @property
+    def np_dtype(self):
+        """Host element type of rows/weights: uint16 bf16 bits or float32."""
+        return np.float32 if self.dtype == DTYPE_F32 else np.uint16
 
     def home_tokens(self, rank: Optional[int] = None) -> np.ndarray:
         r = self.rank if rank is None else rank
@@ -49,7 +58,8 @@ class MoeModelConfig:
     def _c(self) -> _capi.ModelConfigC:
         return _capi.ModelConfigC(self.num_experts, self.num_layers, self.d_model, self.d_ffn,
                                   self.top_k, self.tokens_per_gpu, self.world_size, self.rank,
-                                  self.seed, self.init_std, self.gate_affinity, self.ep_mode)
+                                  self.seed, self.init_std, self.gate_affinity, self.ep_mode,
+                                  self.dtype)
 
 
 def _stream_ptr(stream) -> Optional[int]:
@@ -113,14 +123,16 @@ class MoeModel:
         return p.value
 
     def output(self):
-        """torch bf16 [G*B][d] view of the context-AllGather output (token-id order)."""
+        """torch [G*B][d] view (bf16, or fp32 in fp32 mode) of the context-AllGather
+        output (token-id order)."""
         import torch
         cfg = self.config
         n = cfg.capacity * cfg.d_model
-        holder = _CudaArray(self.output_ptr(), (cfg.capacity, cfg.d_model))
+        f32 = cfg.dtype == DTYPE_F32
+        holder = _CudaArray(self.output_ptr(), (cfg.capacity, cfg.d_model), "<f4" if f32 else "<i2")
         t = torch.as_tensor(holder, device="cuda")
         assert t.numel() == n
-        return t.view(torch.bfloat16)
+        return t if f32 else t.view(torch.bfloat16)
 
     def check(self) -> None:
         _capi.call("exf_model_check", self._h)
@@ -164,7 +176,7 @@ class MoeModel:
 
     def resident(self, which: int):
         cfg = self.config
-        x = np.empty((cfg.capacity, cfg.d_model), np.uint16)
+        x = np.empty((cfg.capacity, cfg.d_model), cfg.np_dtype)
         meta = np.empty((cfg.capacity, 2), np.int32)
         n = C.c_int32()
         _capi.call("exf_model_read_resident", self._h, which, x.ctypes.data, meta.ctypes.data,
@@ -173,16 +185,17 @@ class MoeModel:
 
     def expert_weights(self, layer: int, expert: int):
         cfg = self.config
-        w1 = np.empty((cfg.d_ffn, cfg.d_model), np.uint16)
-        b1 = np.empty(cfg.d_ffn, np.uint16)
-        w2 = np.empty((cfg.d_model, cfg.d_ffn), np.uint16)
-        b2 = np.empty(cfg.d_model, np.uint16)
+        dt = cfg.np_dtype
+        w1 = np.empty((cfg.d_ffn, cfg.d_model), dt)
+        b1 = np.empty(cfg.d_ffn, dt)
+        w2 = np.empty((cfg.d_model, cfg.d_ffn), dt)
+        b2 = np.empty(cfg.d_model, dt)
         _capi.call("exf_model_read_expert", self._h, layer, expert, w1.ctypes.data,
                    b1.ctypes.data, w2.ctypes.data, b2.ctypes.data)
         return w1, b1, w2, b2
 
     def expert_storage(self, layer: int, slot: int):
-        """torch int16 (bf16 bits) views of local weight slot `slot` of `layer`:
+        """torch int16 (bf16 bits; float32 in fp32 mode) views of local weight slot `slot` of `layer`:
         (W1 [d_ffn][d], b1 [d_ffn], W2 [d][d_ffn], b2 [d]) -- device memory of
         this model, for expert migration (migrate.py)."""
         import torch
@@ -190,7 +203,8 @@ class MoeModel:
         ptrs = [C.c_void_p() for _ in range(4)]
         _capi.call("exf_model_expert_storage", self._h, layer, slot, *[C.byref(p) for p in ptrs])
         shapes = [(cfg.d_ffn, cfg.d_model), (cfg.d_ffn,), (cfg.d_model, cfg.d_ffn), (cfg.d_model,)]
-        return tuple(torch.as_tensor(_CudaArray(p.value, sh), device="cuda") for p, sh in zip(ptrs, shapes))
+        ts = "<f4" if cfg.dtype == DTYPE_F32 else "<i2"
+        return tuple(torch.as_tensor(_CudaArray(p.value, sh, ts), device="cuda") for p, sh in zip(ptrs, shapes))
 
     def set_placement(self, assign: np.ndarray) -> None:
         """Install a new [L][E] placement (same table on every rank, weights
@@ -203,7 +217,7 @@ class MoeModel:
 
     def gate_weights(self, layer: int) -> np.ndarray:
         cfg = self.config
-        wg = np.empty((cfg.num_experts, cfg.d_model), np.uint16)
+        wg = np.empty((cfg.num_experts, cfg.d_model), cfg.np_dtype)
         _capi.call("exf_model_read_gate", self._h, layer, wg.ctypes.data)
         return wg
 
@@ -231,6 +245,6 @@ class MoeModel:
 class _CudaArray:
     """__cuda_array_interface__ over a raw device pointer (int16 view of bf16)."""
 
-    def __init__(self, ptr: int, shape):
+    def __init__(self, ptr: int, shape, typestr: str = "<i2"):
         self.__cuda_array_interface__ = {"data": (ptr, False), "shape": tuple(shape),
-                                         "typestr": "<i2", "version": 3, "strides": None}
+                                         "typestr": typestr, "version": 3, "strides": None}
