@@ -1,0 +1,49 @@
+"""Real multi-GPU parity at the BASELINE.json shapes (needs >= G visible
+B200s; skipped otherwise). One process per GPU (torchrun), the ranks'
+kernels exchanging tokens over NVLink peer memory; every rank checks its own
+part of one full decode step against the CPU oracle (tests/step_check.py):
+  configs[1]  E=8,  d=1024, d_ffn=4096, B=64     at G=2 and G=4 (fused path)
+  configs[2]  E=16, d=1024, d_ffn=4096, B=64     at G=2 and G=4
+  configs[3]  E=32, d=2048, d_ffn=8192, B=64/256 at G=4
+  fp32 mode   configs[1] shape                   at G=2 (<= 1e-5)
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+CASES = [
+    # (G, experts, d, dff, batch, dtype, port)
+    (2, 8, 1024, 4096, 64, "bf16", 29711),
+    (4, 8, 1024, 4096, 64, "bf16", 29712),
+    (2, 16, 1024, 4096, 64, "bf16", 29713),
+    (4, 16, 1024, 4096, 64, "bf16", 29714),
+    (4, 32, 2048, 8192, 64, "bf16", 29715),
+    (4, 32, 2048, 8192, 256, "bf16", 29716),
+    (2, 8, 1024, 4096, 64, "f32", 29717),
+]
+
+
+def _gpus():
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("G,E,d,dff,B,dtype,port", CASES,
+                         ids=[f"G{c[0]}-E{c[1]}-d{c[2]}-B{c[4]}-{c[5]}" for c in CASES])
+def test_baseline_shape_parity(G, E, d, dff, B, dtype, port):
+    if _gpus() < G:
+        pytest.skip(f"needs {G} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(G),
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(HERE, "mgpu_step_worker.py"), "--experts", str(E), "--d-model", str(d),
+           "--d-ffn", str(dff), "--batch", str(B), "--dtype", dtype]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert " OK" in r.stdout, r.stdout[-2000:]
+    print(r.stdout.strip().splitlines()[-1])
