@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--gate-affinity", type=float, default=0.8)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-parity", action="store_true", help="skip the per-placement checked step")
+    p.add_argument("--no-fp32", action="store_true", help="skip the fp32-mode sub-measurement")
     p.add_argument("--no-routing-kernels", action="store_true",
                    help="skip the histogram / replay kernel measurements")
     return p.parse_args()
@@ -211,10 +212,10 @@ def main():
         dist.all_reduce(t)
         return t.cpu().numpy()
 
-    def make_model(assign, ep_mode=0):
+    def make_model(assign, ep_mode=0, dtype=0):
         cfg = MoeModelConfig(num_experts=a.experts, num_layers=a.layers, d_model=a.d_model,
                              d_ffn=a.d_ffn, tokens_per_gpu=a.batch, world_size=n, rank=rank,
-                             seed=1234, gate_affinity=a.gate_affinity, ep_mode=ep_mode)
+                             seed=1234, gate_affinity=a.gate_affinity, ep_mode=ep_mode, dtype=dtype)
         m = MoeModel(cfg, assign)
         if n > 1:
             hs = [None] * n
@@ -243,7 +244,9 @@ def main():
             stream.synchronize()
     model.check()
     counts = allsum_i64(model.affinity_counts())
+    t_solve = time.perf_counter()
     aff_assign, solve = pl.solve_staged(counts, topo, pl.AnnealParams(seed=7))
+    solve_ms = (time.perf_counter() - t_solve) * 1e3
     prof_routes = model.routes()
     if n > 1:
         allr = [None] * n
@@ -257,10 +260,28 @@ def main():
 
     results = {}
     clocks = None
+    migration = None
     for name, assign in (("vanilla", vanilla), ("affinity", aff_assign)):
         if name == "affinity":
-            model.close()
-            model = make_model(assign)
+            if n > 1:
+                # online placement change: move every
+                # expert whose (GPU, slot) changes over NCCL, timed
+                from paper_2401_08383_b200 import migrate
+                barrier()
+                torch.cuda.synchronize()
+                t_mig = time.perf_counter()
+                moved = migrate.migrate_nccl(model, assign)
+                torch.cuda.synchronize()
+                mig_s = allmax(time.perf_counter() - t_mig)
+                per_expert = 2 * a.d_model * a.d_ffn * 2 + (a.d_model + a.d_ffn) * 2
+                migration = {"experts_moved": moved, "bytes": moved * per_expert, "wall_ms": mig_s * 1e3,
+                             "gbs": moved * per_expert / mig_s / 1e9 if mig_s > 0 else None,
+                             "how": "migrate_nccl: per layer batch_isend_irecv of W1/b1/W2/b2 over NCCL "
+                                    "(NVLink), then exf_model_set_placement on every rank; host wall "
+                                    "clock, max over ranks"}
+            else:
+                model.close()
+                model = make_model(assign)
         model.capture(x_dev, stream)
         for _ in range(a.warmup):
             model.replay(stream)
@@ -429,6 +450,26 @@ def main():
         traffic, traffic_src = summ.get("traffic_bytes_per_launch"), "profiles/r01_fused_ncu_summary.json"
     launches = model.launches_per_step()
 
+    # ---- fp32 mode (north_star: 1e-5 in fp32 mode): the same workload with
+    # fp32 weights/states/gate and the SIMT fp32 expert FFN, affinity placement
+    fp32 = None
+    if not a.no_fp32:
+        fp32 = measure_fp32(a, n, rank, aff_assign, make_model, stream, barrier, allmax, check_step,
+                            hbm_peak)
+        log(f"[bench] fp32 mode: {fp32.get('ms_per_step')} ms/step parity {fp32.get('parity')}")
+    # ---- solver at BASELINE configs[4] scale (E=64, L=24, 8 GPUs) on a
+    # synthetic Markov histogram (host, all restarts on host threads)
+    solve4 = None
+    if rank == 0:
+        paths4 = pl.generate_markov_trace(64, 24, 1 << 16, 0.8, 8, 5)
+        c4 = affinity.count_transitions(paths4, 64).matrices
+        t0 = time.perf_counter()
+        _, rep4 = pl.solve_staged(c4, affinity.Topology(1, 8), pl.AnnealParams(seed=7))
+        solve4 = {"E": 64, "L": 24, "G": 8, "wall_ms": (time.perf_counter() - t0) * 1e3,
+                  "solver": rep4.solver, "iterations": rep4.iterations, "restarts": rep4.restarts,
+                  "host_threads": os.cpu_count(), "objective": rep4.objective}
+    barrier()
+
     # ---- CPU baseline (rank 0, at every N; the other ranks wait): whole
     # decode steps of the same G*B tokens on the host cores, nothing
     # extrapolated; the reference's own CPU routing bookkeeping included
@@ -482,7 +523,10 @@ def main():
                                       "note": "p_star of the timed batch's routes replayed on a 1x8 "
                                               "topology (GPU replay kernel); the affinity placement "
                                               "is solved from the held-out profiling batches"},
-        "affinity_solve": {"solver": solve.solver, "objective": solve.objective},
+        "affinity_solve": {"solver": solve.solver, "objective": solve.objective, "wall_ms": solve_ms,
+                           "configs4_scale": solve4},
+        "expert_migration": migration,
+        "fp32_mode": fp32,
         "e2e": {"value": a.batch * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "roofline": {"kernel": ("layer_fused_kernel (gate+dispatch+GEMM1+GEMM2 per layer, tcgen05)"
@@ -512,6 +556,56 @@ def main():
     model.close()
     if n > 1:
         dist.destroy_process_group()
+
+
+def measure_fp32(a, n, rank, assign, make_model, stream, barrier, allmax, check_step, hbm_peak):
+    """fp32 mode at the bench config: graph-replayed steps timed with CUDA
+    events (max over ranks), one checked step (<= 1e-5 vs the fp64 oracle),
+    HBM roofline of the step over its weight bytes (fp32 weights of the active
+    local experts, every layer)."""
+    import torch
+    from paper_2401_08383_b200.model import DTYPE_F32
+    dev = torch.device("cuda", torch.cuda.current_device())
+    try:
+        m = make_model(assign, dtype=DTYPE_F32)
+    except Exception as e:  # e.g. fp32 weights do not fit
+        return {"error": f"{type(e).__name__}: {e}"}
+    g = torch.Generator(device="cpu").manual_seed(100 + rank)
+    x = torch.randn(a.batch, a.d_model, generator=g).to(dev)
+    m.capture(x, stream)
+    for _ in range(max(3, a.warmup)):
+        m.replay(stream)
+    stream.synchronize()
+    m.check()
+    barrier()
+    torch.cuda.synchronize()
+    steps = max(3, a.steps // 2)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        m.replay(stream)
+    e1.record(stream)
+    stream.synchronize()
+    m.check()
+    ms = allmax(e0.elapsed_time(e1)) / steps
+    barrier()
+    r = m.routes()
+    d, f = a.d_model, a.d_ffn
+    active = 0
+    for j in range(a.layers):
+        toks = r[:, j][r[:, j] >= 0]
+        active += len(set(toks[assign[j][toks] == rank].tolist()))
+    wbytes = active * (2 * d * f + d + f) * 4
+    gbs = allmax(wbytes / (ms * 1e-3) / 1e9)
+    chk = check_step(m, x, assign)
+    m.close()
+    torch.cuda.empty_cache()
+    return {"value": a.batch * n / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms, "steps": steps,
+            "dtype": "f32", "path": "two-kernel: fp32 gate+dispatch, SIMT fp32 expert FFN (ffn_f32.cu)",
+            "parity": chk["parity"], "max_rel_err_sampled": chk["max_rel_err_sampled"],
+            "tolerance": 1e-5, "failures": chk["failures"],
+            "roofline": {"bound": "hbm", "achieved_gbs": gbs, "peak": hbm_peak, "frac": gbs / hbm_peak,
+                         "bytes_model": "fp32 weights of the active local experts, all layers, per step"}}
 
 
 def measure_routing_kernels(hbm_peak, stream, T=1 << 21, L=24, iters=10):
