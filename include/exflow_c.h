@@ -56,7 +56,8 @@ int32_t exf_device_ok(void);
  * proj/src/trace.cpp:191-215): counts[j][a][b] = #{t : paths[t][j] == a and
  * paths[t][j+gap] == b}, row_totals[j][a] = sum_b counts[j][a][b].
  * Bit-exact (integer). Validation errors match trace.cpp:53-70 / :193-196.
- * d_workspace must hold exf_count_transitions_workspace_bytes(...) bytes.
+ * d_workspace: exf_count_transitions_workspace_bytes(...) bytes (currently 0:
+ * per-CTA privatised counters flush with exact 64-bit atomics; may be NULL).
  * ---------------------------------------------------------------------- */
 int64_t exf_count_transitions_workspace_bytes(int64_t T, int32_t L, int32_t E, int32_t gap);
 exf_status exf_count_transitions(const int32_t* d_paths, int64_t T, int32_t L, int32_t E,
@@ -217,6 +218,12 @@ typedef struct { /* in the style of SynthConfig (proj/include/exflow/synth.hpp:1
                                 back to the home GPU every layer, proj/src/sim.cpp:60-64) */
     int32_t dtype;           /* EXF_DTYPE_BF16 (tcgen05 path) or EXF_DTYPE_F32 (fp32 mode:
                                 fp32 weights, token states, gate and FFN; SIMT FFN) */
+    int32_t attn_heads;      /* H > 0: every layer starts with the coherent attention block
+                                (QKV projection, K/V append into every replica, attention over
+                                the token's sequence in the local replica, output projection +
+                                residual; bf16 only); 0: MoE layers only */
+    int32_t context_len;     /* replicated context capacity per sequence (keys) */
+    int32_t context_prefix;  /* prompt length written by exf_model_context_setup */
 } exf_model_config;
 #define EXF_EP_COHERENT 0
 #define EXF_EP_VANILLA 1
@@ -244,9 +251,26 @@ exf_status exf_model_step(exf_model* model, const void* d_x_in, exf_stream_t str
  * concurrently, i.e. one process or GPU per rank) |
  * 3 gather send | 4 gather wait |
  * 6 combine send(layer) | 7 combine wait(layer) (ep_mode EXF_EP_VANILLA, after
- * each layer: outputs back to the tokens' home ranks). */
+ * each layer: outputs back to the tokens' home ranks) |
+ * 8 attention block(layer) (attn_heads > 0: runs before the layer's MoE). */
 exf_status exf_model_step_phase(exf_model* model, int32_t phase, int32_t layer,
                                 const void* d_x_in, exf_stream_t stream);
+/* Setup AllGather of the replicated context (attention block; once before
+ * decoding, proj/src/sim.cpp:162): every rank writes the prompt's K/V
+ * (context_prefix positions, synthetic and seeded) of its home sequences
+ * into EVERY rank's replica over NVLink, sets the lengths, then flags every
+ * peer and waits for all of them on `stream`. All ranks must call it. */
+exf_status exf_model_context_setup(exf_model* model, exf_stream_t stream);
+/* Replicated context rows of this rank's replica (synchronous, diagnostics /
+ * tests): K and V of (layer, seq) at positions [pos0, pos0+count), each
+ * [count][H][Dh] bf16 bits; lengths [S] int32 of a layer. */
+exf_status exf_model_read_kv(exf_model* model, int32_t layer, int32_t seq, int32_t pos0,
+                             int32_t count, uint16_t* h_k, uint16_t* h_v);
+exf_status exf_model_read_kv_len(exf_model* model, int32_t layer, int32_t* h_len);
+/* Attention-block weights of a layer (bf16 bits): Wqkv [3d][d], bqkv [3d],
+ * Wo [d][d], bo [d] (replicated on every rank). */
+exf_status exf_model_read_attn(exf_model* model, int32_t layer, uint16_t* h_wqkv, uint16_t* h_bqkv,
+                               uint16_t* h_wo, uint16_t* h_bo);
 /* Device pointer to the [G*B][d] bf16 step output (token-id order). */
 exf_status exf_model_output(exf_model* model, void** d_out);
 /* Forced routing (routes from a trace, e.g. generate_markov_trace): h_routes

@@ -99,6 +99,10 @@ SIGNATURES = {
     "exf_model_step": (C.c_int, [_VP, _VP, _VP]),
     "exf_model_step_phase": (C.c_int, [_VP, _I32, _I32, _VP, _VP]),
     "exf_model_output": (C.c_int, [_VP, _VP]),
+    "exf_model_context_setup": (C.c_int, [_VP, _VP]),
+    "exf_model_read_kv": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _VP, _VP]),
+    "exf_model_read_kv_len": (C.c_int, [_VP, _I32, _VP]),
+    "exf_model_read_attn": (C.c_int, [_VP, _I32, _VP, _VP, _VP, _VP]),
     "exf_model_set_forced_routes": (C.c_int, [_VP, _VP]),
     "exf_model_read_routes": (C.c_int, [_VP, _VP]),
     "exf_model_read_crossed": (C.c_int, [_VP, _VP]),
@@ -133,7 +137,8 @@ class ModelConfigC(C.Structure):
                 ("d_ffn", C.c_int32), ("top_k", C.c_int32), ("tokens_per_gpu", C.c_int32),
                 ("world_size", C.c_int32), ("rank", C.c_int32), ("seed", C.c_uint64),
                 ("init_std", C.c_float), ("gate_affinity", C.c_float), ("ep_mode", C.c_int32),
-                ("dtype", C.c_int32)]
+                ("dtype", C.c_int32), ("attn_heads", C.c_int32), ("context_len", C.c_int32),
+                ("context_prefix", C.c_int32)]
 
 _lib = None
 

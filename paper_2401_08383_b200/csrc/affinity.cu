@@ -4,19 +4,25 @@
 // Replaces exflow::count_transitions (proj/src/trace.cpp:191-215; hot loop
 // :205-209 does counts[j](p(t,j), p(t,j+gap)) += 1 with scattered int64 RMW).
 //
-// Design (HBM-bound integer scatter):
-//  * grid = splits x 1: each CTA owns a contiguous token range (<= 65535
-//    tokens) and privatises the WHOLE (pairs x E x E) histogram in shared
-//    memory as packed u16 counters (two bins per 32-bit word; a per-CTA count
-//    never exceeds 65535, so a 32-bit atomicAdd of 1<<16 never carries).
-//  * token rows are staged through shared memory with coalesced 16-byte loads
-//    (a token range of the row-major [T][L] trace is one contiguous chunk);
-//    work items are flattened (token, pair) so consecutive lanes touch
-//    consecutive columns (conflict-free reads) and different pair matrices
-//    (low atomic contention).
-//  * global merge is atomic-free and deterministic: each CTA streams its u16
-//    partials to a workspace; a second kernel sums the splits per bin into the
-//    int64 result and forms row totals (trace.cpp:210-213).
+// Design (HBM-bound integer scatter; v2 after the round-1
+// ncu capture: 212 us for 201 MB of ids = 0.15 of HBM, of which 70 us was a
+// serial split reduction):
+//  * persistent CTAs, each owning a contiguous token range (<= 65535 tokens)
+//    and privatising the (pairs x E x E) histogram in shared memory as packed
+//    u16 counters (two bins per 32-bit word; a per-CTA count never exceeds
+//    65535, so a 32-bit atomicAdd of 1<<16 never carries). Each pair's block
+//    of words has an odd stride, so lanes counting the same (a, b) transition
+//    of different layer pairs hit different banks;
+//  * the trace streams through a software pipeline: the next tile's rows
+//    (a contiguous chunk of the row-major [T][L] trace) are loaded into
+//    registers with 16-byte non-allocating loads while the current tile is
+//    counted from shared memory;
+//  * work items are (token, pair) with the pair fixed per thread (no integer
+//    division in the loop);
+//  * the merge is a flush of the CTA's non-zero bins with 64-bit global
+//    atomics into zeroed counts: integer sums are exact in any order, so the
+//    result is bit-identical to the reference loop and
+//    there is no second pass over split partials.
 // Algorithmic bytes per launch: 4*T*L (ids) + 8*(L-gap)*E*E (+8*(L-gap)*E).
 #include "common.cuh"
 
@@ -30,6 +36,7 @@ constexpr int kHistThreads = 512;
 constexpr int kTileTokens = 256;
 constexpr int kMaxTokensPerCta = 65535;
 constexpr int64_t kCounterSmemBudget = 190 * 1024;
+constexpr int kPrefetchVec = 4;  // int4 per thread per tile in registers (tile <= 512*4*4 ints)
 
 int g_num_sms = 0;
 
@@ -45,10 +52,11 @@ int num_sms() {
 
 struct HistPlan {
     int32_t pairs;
-    int32_t pair_group;  // pairs per CTA pass (all pairs when they fit)
+    int32_t pair_group;   // pairs per CTA pass (all pairs when they fit)
     int32_t groups;
-    int64_t splits;
-    int64_t counter_words;  // u32 words of packed u16 counters per CTA
+    int64_t splits;       // token ranges
+    int32_t pair_words;   // odd stride of one pair's packed counters (u32 words)
+    int32_t tile_tokens;  // tokens per pipeline tile
     size_t smem_bytes;
     int64_t workspace_bytes;
 };
@@ -57,107 +65,112 @@ HistPlan plan_hist(int64_t T, int32_t L, int32_t E, int32_t gap) {
     HistPlan p{};
     p.pairs = L - gap;
     const int64_t bins_per_pair = (int64_t)E * E;
+    p.pair_words = (int32_t)(((bins_per_pair + 1) / 2) | 1);
+    // the tile must fit the register prefetch (kPrefetchVec int4 per thread)
+    p.tile_tokens = (int32_t)std::min<int64_t>(kTileTokens, (int64_t)kHistThreads * kPrefetchVec * 4 / L);
+    p.tile_tokens = std::max(1, p.tile_tokens & ~3);
+    const int64_t tile_bytes = (int64_t)p.tile_tokens * L * 4;
     p.pair_group = (int32_t)std::max<int64_t>(
-        1, std::min<int64_t>(p.pairs, kCounterSmemBudget / (bins_per_pair * 2)));
+        1, std::min<int64_t>(p.pairs, (kCounterSmemBudget + 32 * 1024 - tile_bytes) / ((int64_t)p.pair_words * 4)));
     p.groups = (p.pairs + p.pair_group - 1) / p.pair_group;
-    const int64_t group_bins = bins_per_pair * p.pair_group;
-    p.counter_words = (group_bins + 1) / 2;
-    // splits: enough CTAs to fill the machine, few enough that the flush of
-    // private histograms (splits * bins * 2 B) stays well below the id bytes.
-    const int64_t total_bins = bins_per_pair * p.pairs;
+    // token ranges: about two CTAs per SM over all groups, <= 65535 tokens each
     const int64_t min_splits = (T + kMaxTokensPerCta - 1) / kMaxTokensPerCta;
-    const int64_t by_traffic = std::max<int64_t>(1, (4 * T * L) / (total_bins * 2 * 4));
     const int64_t target = std::max<int64_t>(1, 2 * (int64_t)num_sms() / p.groups);
-    int64_t splits = std::min(target, by_traffic);
-    splits = std::max(splits, min_splits);
-    splits = std::min<int64_t>(splits, std::max<int64_t>(1, (T + 31) / 32));
-    p.splits = std::max<int64_t>(splits, 1);
-    p.smem_bytes = (size_t)p.counter_words * 4 + (size_t)kTileTokens * L * 4 + 16;
-    p.workspace_bytes = p.splits * total_bins * 2;
+    int64_t splits = std::max(target, min_splits);
+    splits = std::min<int64_t>(splits, std::max<int64_t>(1, (T + 63) / 64));
+    p.splits = std::max<int64_t>(std::max(splits, min_splits), 1);
+    p.smem_bytes = (size_t)p.pair_group * p.pair_words * 4 + (size_t)tile_bytes + 16;
+    p.workspace_bytes = 0;  // the flush is atomic into the result: no split partials
     return p;
 }
 
-// Each CTA: one token range x one pair group. Writes packed u16 partials to
-// ws[split][pair][E][E] (u16 view).
+// One CTA: one token range x one pair group.
 __global__ void __launch_bounds__(kHistThreads)
-hist_partial_kernel(const int32_t* __restrict__ paths, int64_t T, int32_t L, int32_t E,
-                    int32_t gap, int32_t pairs, int32_t pair_group, int64_t splits,
-                    int64_t counter_words, uint16_t* __restrict__ ws) {
+hist_kernel(const int32_t* __restrict__ paths, int64_t T, int32_t L, int32_t E, int32_t gap,
+            int32_t pairs, int32_t pair_group, int32_t pair_words, int32_t tile_tokens, int64_t splits,
+            unsigned long long* __restrict__ counts, unsigned long long* __restrict__ row_totals) {
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);
-    int32_t* tile = reinterpret_cast<int32_t*>(smem + ((counter_words * 4 + 15) & ~15ll));
-
     const int32_t group = blockIdx.x;
-    const int64_t split = blockIdx.y;
     const int32_t j0 = group * pair_group;
     const int32_t pg = min(pair_group, pairs - j0);
+    int32_t* tile = reinterpret_cast<int32_t*>(smem + (((int64_t)pair_group * pair_words * 4 + 15) & ~15ll));
+    const int64_t split = blockIdx.y;
     const int64_t t_begin = T * split / splits;
     const int64_t t_end = T * (split + 1) / splits;
     const int32_t EE = E * E;
+    const int32_t tid = threadIdx.x;
 
-    for (int64_t w = threadIdx.x; w < counter_words; w += blockDim.x) cnt[w] = 0u;
+    for (int32_t w = tid; w < pg * pair_words; w += kHistThreads) cnt[w] = 0u;
+    // pair handled by this thread, token stride
+    const int32_t lanes = (kHistThreads / pg) * pg;  // threads in use
+    const int32_t jj = tid % pg, tstep = kHistThreads / pg, tfirst = tid / pg;
+    const bool counting = tid < lanes;
+    uint32_t* my_cnt = cnt + jj * pair_words;
+    const int32_t ja = j0 + jj, jb = ja + gap;
 
-    for (int64_t t0 = t_begin; t0 < t_end; t0 += kTileTokens) {
-        const int32_t nt = (int32_t)imin64(kTileTokens, t_end - t0);
-        const int32_t nints = nt * L;
-        const int32_t* src = paths + t0 * L;
-        __syncthreads();  // previous tile fully consumed
-        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-            const int32_t nvec = nints >> 2;
-            const int4* s4 = reinterpret_cast<const int4*>(src);
-            int4* d4 = reinterpret_cast<int4*>(tile);
-            for (int32_t i = threadIdx.x; i < nvec; i += blockDim.x) d4[i] = ld_nc_v4(s4 + i);
-            for (int32_t i = (nvec << 2) + threadIdx.x; i < nints; i += blockDim.x) tile[i] = src[i];
-        } else {
-            for (int32_t i = threadIdx.x; i < nints; i += blockDim.x) tile[i] = __ldg(src + i);
+    const bool aligned = ((reinterpret_cast<uintptr_t>(paths) | (uintptr_t)(L * 4)) & 15) == 0;
+    int4 pre[kPrefetchVec];
+    auto fetch = [&](int64_t t0) {  // tile starting at token t0 into registers
+        const int32_t nt = (int32_t)imin64(tile_tokens, t_end - t0);
+        if (aligned) {
+            const int32_t nvec = nt * L / 4;
+            const int4* s4 = reinterpret_cast<const int4*>(paths + t0 * L);
+#pragma unroll
+            for (int u = 0; u < kPrefetchVec; ++u) {
+                const int32_t i = tid + u * kHistThreads;
+                if (i < nvec) pre[u] = ld_nc_v4(s4 + i);
+            }
         }
+    };
+    auto stage = [&](int64_t t0) {  // registers (or global, unaligned) -> shared tile
+        const int32_t nt = (int32_t)imin64(tile_tokens, t_end - t0);
+        if (aligned) {
+            const int32_t nvec = nt * L / 4;
+            int4* d4 = reinterpret_cast<int4*>(tile);
+#pragma unroll
+            for (int u = 0; u < kPrefetchVec; ++u) {
+                const int32_t i = tid + u * kHistThreads;
+                if (i < nvec) d4[i] = pre[u];
+            }
+        } else {
+            for (int32_t i = tid; i < nt * L; i += kHistThreads) tile[i] = __ldg(paths + t0 * L + i);
+        }
+    };
+    if (t_begin < t_end) fetch(t_begin);
+    for (int64_t t0 = t_begin; t0 < t_end; t0 += tile_tokens) {
+        const int32_t nt = (int32_t)imin64(tile_tokens, t_end - t0);
+        __syncthreads();  // previous tile fully counted (and the zeroing done)
+        stage(t0);
+        if (t0 + tile_tokens < t_end) fetch(t0 + tile_tokens);  // in flight while counting
         __syncthreads();
-        const int32_t items = nt * pg;
-        for (int32_t w = threadIdx.x; w < items; w += blockDim.x) {
-            const int32_t t = w / pg;
-            const int32_t jj = w - t * pg;
-            const int32_t j = j0 + jj;
-            const int32_t a = tile[t * L + j];
-            const int32_t b = tile[t * L + j + gap];
-            if ((unsigned)a < (unsigned)E && (unsigned)b < (unsigned)E) {
-                const int32_t bin = jj * EE + a * E + b;
-                atomicAdd(&cnt[bin >> 1], 1u << ((bin & 1) * 16));
+        if (counting) {
+            for (int32_t t = tfirst; t < nt; t += tstep) {
+                const int32_t a = tile[t * L + ja];
+                const int32_t b = tile[t * L + jb];
+                if ((unsigned)a < (unsigned)E && (unsigned)b < (unsigned)E) {
+                    const int32_t bin = a * E + b;
+                    atomicAdd(&my_cnt[bin >> 1], 1u << ((bin & 1) * 16));
+                }
             }
         }
     }
     __syncthreads();
-    // stream the packed partial histogram of this group to the workspace
-    const int64_t total_bins = (int64_t)pairs * EE;
-    uint16_t* dst = ws + split * total_bins + (int64_t)j0 * EE;
+    // flush: non-zero bins into the exact 64-bit result; row totals per (pair, a)
     const uint16_t* c16 = reinterpret_cast<const uint16_t*>(cnt);
-    const int64_t nb = (int64_t)pg * EE;
-    for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) dst[i] = c16[i];
-}
-
-// One CTA per (pair j, source expert a): sums the splits of each bin (fixed
-// order, exact) and forms the row total.
-__global__ void hist_reduce_kernel(const uint16_t* __restrict__ ws, int64_t splits,
-                                   int32_t pairs, int32_t E, int64_t* __restrict__ counts,
-                                   int64_t* __restrict__ row_totals) {
-    const int32_t row = blockIdx.x;  // j*E + a
-    const int64_t total_bins = (int64_t)pairs * E * E;
-    __shared__ int64_t warp_tot[32];
-    int64_t mine = 0;
-    for (int32_t b = threadIdx.x; b < E; b += blockDim.x) {
-        const int64_t bin = (int64_t)row * E + b;
-        int64_t s = 0;
-        for (int64_t sp = 0; sp < splits; ++sp) s += ws[sp * total_bins + bin];
-        counts[bin] = s;
-        mine += s;
+    for (int32_t i = tid; i < pg * EE; i += kHistThreads) {
+        const int32_t q = i / EE, bin = i - q * EE;
+        const uint32_t c = c16[(int64_t)q * pair_words * 2 + bin];
+        if (c) atomicAdd(&counts[(int64_t)(j0 + q) * EE + bin], (unsigned long long)c);
     }
-    mine = warp_sum(mine);
-    if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = mine;
-    __syncthreads();
-    if (threadIdx.x == 0 && row_totals) {
-        int64_t t = 0;
-        for (int w = 0; w < (int)((blockDim.x + 31) >> 5); ++w) t += warp_tot[w];
-        row_totals[row] = t;
-    }
+    if (row_totals)
+        for (int32_t r = tid; r < pg * E; r += kHistThreads) {
+            const int32_t q = r / E, a = r - q * E;
+            const uint16_t* row = c16 + (int64_t)q * pair_words * 2 + (int64_t)a * E;
+            uint32_t sum = 0;
+            for (int32_t b = 0; b < E; ++b) sum += row[b];
+            if (sum) atomicAdd(&row_totals[(int64_t)(j0 + q) * E + a], (unsigned long long)sum);
+        }
 }
 
 exf_status check_hist_args(int64_t T, int32_t L, int32_t E, int32_t gap) {
@@ -168,9 +181,9 @@ exf_status check_hist_args(int64_t T, int32_t L, int32_t E, int32_t gap) {
     if (gap < 1 || gap > L - 1)
         return invalid("gap " + std::to_string(gap) + " out of range [1," + std::to_string(L - 1) +
                        "]");
-    if ((int64_t)E * E * 2 > kCounterSmemBudget)
+    if ((((int64_t)E * E + 1) / 2 | 1) * 4 > kCounterSmemBudget)
         return invalid("num_experts " + std::to_string(E) + " exceeds the histogram kernel limit");
-    if ((int64_t)kTileTokens * L * 4 > 32 * 1024) return invalid("num_layers too large");
+    if ((int64_t)L * 4 > (int64_t)kHistThreads * kPrefetchVec * 16) return invalid("num_layers too large");
     return EXF_OK;
 }
 
@@ -190,22 +203,24 @@ extern "C" exf_status exf_count_transitions(const int32_t* d_paths, int64_t T, i
                                             int64_t* d_row_totals, void* d_workspace,
                                             exf_stream_t stream) {
     EXF_TRY(check_hist_args(T, L, E, gap));
-    if (!d_paths || !d_counts || !d_workspace) return invalid("null device pointer");
+    if (!d_paths || !d_counts) return invalid("null device pointer");
+    (void)d_workspace;  // no split partials in v2 (workspace_bytes == 0; may be NULL)
     const HistPlan p = plan_hist(T, L, E, gap);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    EXF_CUDA_TRY(cudaFuncSetAttribute(hist_partial_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)p.smem_bytes));
+    static size_t attr_bytes = 0;
+    if (p.smem_bytes > attr_bytes) {
+        EXF_CUDA_TRY(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)std::max<size_t>(p.smem_bytes, 48 * 1024)));
+        attr_bytes = std::max<size_t>(p.smem_bytes, 48 * 1024);
+    }
+    const int64_t pairs_bins = (int64_t)p.pairs * E * E;
+    EXF_CUDA_TRY(cudaMemsetAsync(d_counts, 0, (size_t)pairs_bins * 8, s));
+    if (d_row_totals) EXF_CUDA_TRY(cudaMemsetAsync(d_row_totals, 0, (size_t)p.pairs * E * 8, s));
     dim3 grid(p.groups, (unsigned)p.splits);
-    hist_partial_kernel<<<grid, kHistThreads, p.smem_bytes, s>>>(
-        d_paths, T, L, E, gap, p.pairs, p.pair_group, p.splits, p.counter_words,
-        static_cast<uint16_t*>(d_workspace));
-    EXF_LAUNCH_CHECK("hist_partial_kernel");
-    const int threads = std::max(32, std::min(256, ((E + 31) / 32) * 32));
-    hist_reduce_kernel<<<p.pairs * E, threads, 0, s>>>(static_cast<uint16_t*>(d_workspace),
-                                                       p.splits, p.pairs, E, d_counts,
-                                                       d_row_totals);
-    EXF_LAUNCH_CHECK("hist_reduce_kernel");
+    hist_kernel<<<grid, kHistThreads, p.smem_bytes, s>>>(
+        d_paths, T, L, E, gap, p.pairs, p.pair_group, p.pair_words, p.tile_tokens, p.splits,
+        reinterpret_cast<unsigned long long*>(d_counts), reinterpret_cast<unsigned long long*>(d_row_totals));
+    EXF_LAUNCH_CHECK("hist_kernel");
     return EXF_OK;
 }
 

@@ -63,11 +63,15 @@ __global__ void __launch_bounds__(kThreads) coherent_attn_kernel(
     const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ seq,
     const int32_t* __restrict__ ctx, const __nv_bfloat16* __restrict__ k,
     const __nv_bfloat16* __restrict__ v, int32_t H, int32_t C, int32_t chunk, float scale_log2,
-    float* __restrict__ ws, __nv_bfloat16* __restrict__ out) {
+    float* __restrict__ ws, __nv_bfloat16* __restrict__ out, int32_t seq_stride,
+    const int32_t* __restrict__ n_dev) {
     constexpr int LPK = Dh / 8;                  // lanes per key
     constexpr int GROUPS = kThreads / LPK;       // keys in flight per CTA step
     const int h = blockIdx.x, n = blockIdx.y, split = blockIdx.z, splits = gridDim.z;
-    const int s = seq[n];
+    // decode-step form: the grid covers the capacity, the resident count is
+    // on the device (uniform per CTA: every split of token n leaves together)
+    if (n_dev && n >= *n_dev) return;
+    const int s = seq[(size_t)n * seq_stride];
     const int len = ctx[s];
     const int lane_in = threadIdx.x % LPK, grp = threadIdx.x / LPK;
     const int k_begin = split * chunk;
@@ -224,6 +228,42 @@ int attn_splits(int64_t N, int32_t H, int32_t Dh, int32_t C) {
 }
 
 }  // namespace
+
+int64_t attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh, int32_t C) {
+    const int splits = attn_splits(N, H, Dh, C);
+    cudaGetLastError();
+    if (splits <= 1) return 0;
+    return (int64_t)ws_partials_off(N, H) * (int64_t)sizeof(float) +
+           N * (int64_t)H * (int64_t)splits * (Dh + 2) * (int64_t)sizeof(float);
+}
+
+exf_status launch_attention_model(const void* q, const int32_t* seq, int32_t seq_stride,
+                                  const int32_t* n_dev, int64_t n_max, const int32_t* ctx,
+                                  const void* k, const void* v, int32_t H, int32_t Dh, int32_t C,
+                                  float scale, void* ws, void* out, cudaStream_t st) {
+    if (n_max <= 0) return EXF_OK;
+    if (Dh != 64 && Dh != 128) return invalid("attention: head dim must be 64 or 128");
+    const int splits = attn_splits(n_max, H, Dh, C);
+    if (splits > 1 && !ws) return invalid("attention: workspace required");
+    const int chunk = ((C + splits - 1) / splits + 63) / 64 * 64;
+    const float scale_log2 = scale * 1.4426950408889634f;
+    const dim3 grid(H, (unsigned)n_max, splits);
+    if (splits > 1) EXF_CUDA_TRY(cudaMemsetAsync(ws, 0, (size_t)n_max * H * sizeof(unsigned int), st));
+    auto qq = static_cast<const __nv_bfloat16*>(q);
+    auto kk = static_cast<const __nv_bfloat16*>(k);
+    auto vv = static_cast<const __nv_bfloat16*>(v);
+    auto oo = static_cast<__nv_bfloat16*>(out);
+    auto w = static_cast<float*>(ws);
+    if (Dh == 64)
+        coherent_attn_kernel<64><<<grid, kThreads, 0, st>>>(qq, seq, ctx, kk, vv, H, C, chunk, scale_log2, w, oo,
+                                                            seq_stride, n_dev);
+    else
+        coherent_attn_kernel<128><<<grid, kThreads, 0, st>>>(qq, seq, ctx, kk, vv, H, C, chunk, scale_log2, w,
+                                                             oo, seq_stride, n_dev);
+    EXF_LAUNCH_CHECK("attention_model");
+    return EXF_OK;
+}
+
 }  // namespace exf
 
 extern "C" int64_t exf_coherent_attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh,
@@ -280,10 +320,10 @@ extern "C" exf_status exf_coherent_attention(const void* d_q, const int32_t* d_s
     }
     if (Dh == 64) {
         coherent_attn_kernel<64><<<grid, kThreads, 0, st>>>(q, d_seq, d_ctx_len, k, v, H, C, chunk,
-                                                            scale_log2, ws, o);
+                                                            scale_log2, ws, o, 1, nullptr);
     } else {
         coherent_attn_kernel<128><<<grid, kThreads, 0, st>>>(q, d_seq, d_ctx_len, k, v, H, C,
-                                                             chunk, scale_log2, ws, o);
+                                                             chunk, scale_log2, ws, o, 1, nullptr);
     }
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_status(err, "coherent_attention launch");
@@ -313,9 +353,12 @@ __global__ void __launch_bounds__(128) kv_append_kernel(const uint4* __restrict_
                                                         const int32_t* __restrict__ seq,
                                                         int32_t H, int32_t Dh, int32_t C,
                                                         int32_t replicas, KvReplicas rep,
-                                                        int32_t* overflow) {
+                                                        int32_t* overflow, int32_t seq_stride,
+                                                        const int32_t* __restrict__ n_dev,
+                                                        int64_t new_stride) {
     const int n = blockIdx.x;
-    const int s = seq[n];
+    if (n_dev && n >= *n_dev) return;
+    const int s = seq[(size_t)n * seq_stride];
     const int pos = rep.ctx[0][s];
     if (pos >= C) {
         if (threadIdx.x == 0 && overflow) atomicAdd(overflow, 1);
@@ -325,8 +368,8 @@ __global__ void __launch_bounds__(128) kv_append_kernel(const uint4* __restrict_
     const int vecs = H * vec_per_head;
     for (int i = threadIdx.x; i < vecs; i += blockDim.x) {
         const int h = i / vec_per_head, c = i % vec_per_head;
-        const uint4 kv = k_new[(size_t)n * vecs + i];
-        const uint4 vv = v_new[(size_t)n * vecs + i];
+        const uint4 kv = k_new[(size_t)n * new_stride + i];
+        const uint4 vv = v_new[(size_t)n * new_stride + i];
         const size_t off = (((size_t)s * H + h) * C + pos) * vec_per_head + c;
         for (int r = 0; r < replicas; ++r) {
             reinterpret_cast<uint4*>(rep.k[r])[off] = kv;
@@ -340,6 +383,32 @@ __global__ void __launch_bounds__(128) kv_append_kernel(const uint4* __restrict_
 }
 
 }  // namespace
+
+// Decode-step forms used by the model (attn_block.cu): token count on the
+// device (grid over the capacity), sequence id = the token id of each
+// resident row (ResMeta stride 2), rows of the projection buffers with their
+// own stride (int4 units).
+exf_status launch_kv_append_model(const void* k_new, const void* v_new, int64_t new_stride_vec,
+                                  const int32_t* seq, int32_t seq_stride, const int32_t* n_dev,
+                                  int64_t n_max, int32_t H, int32_t Dh, int32_t C, int32_t replicas,
+                                  void* const* k_caches, void* const* v_caches,
+                                  int32_t* const* lens, int32_t* overflow, cudaStream_t st) {
+    if (replicas < 1 || replicas > kMaxReplicas) return invalid("kv_append: replicas must be in [1, 8]");
+    KvReplicas rep{};
+    for (int r = 0; r < replicas; ++r) {
+        rep.k[r] = static_cast<__nv_bfloat16*>(k_caches[r]);
+        rep.v[r] = static_cast<__nv_bfloat16*>(v_caches[r]);
+        rep.ctx[r] = lens[r];
+    }
+    if (n_max <= 0) return EXF_OK;
+    kv_append_kernel<<<(unsigned)n_max, 128, 0, st>>>(static_cast<const uint4*>(k_new),
+                                                      static_cast<const uint4*>(v_new), seq, H, Dh, C,
+                                                      replicas, rep, overflow, seq_stride, n_dev,
+                                                      new_stride_vec);
+    EXF_LAUNCH_CHECK("kv_append_model");
+    return EXF_OK;
+}
+
 }  // namespace exf
 
 extern "C" exf_status exf_kv_append(const void* d_k_new, const void* d_v_new,
@@ -382,7 +451,7 @@ extern "C" exf_status exf_kv_append(const void* d_k_new, const void* d_v_new,
     }
     kv_append_kernel<<<(unsigned)N, 128, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint4*>(d_k_new), static_cast<const uint4*>(d_v_new), d_seq, H, Dh, C,
-        replicas, rep, d_overflow);
+        replicas, rep, d_overflow, 1, nullptr, (int64_t)H * Dh / 8);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_status(err, "kv_append launch");
     return EXF_OK;

@@ -34,6 +34,21 @@ exf_status launch_combine(const void* res_x_out, const ResMeta* res_meta_out, co
                           int layer, const uint64_t* step, void* res_x_next, ResMeta* res_meta_next,
                           int32_t* n_res_next, int32_t* err, int part, cudaStream_t s);
 exf_status launch_ffn_f32(const FfnF32Args& a, int mode, cudaStream_t s);
+exf_status launch_dense_gemm(const CUtensorMap& w, const CUtensorMap& x, const DenseArgs& a, int nt, int mode,
+                             cudaStream_t s);
+int dense_gemm_ksplit(int M, int K);
+exf_status launch_context_setup(const ContextSetupArgs& a, int64_t flag_off, uint64_t epoch, int32_t* err,
+                                cudaStream_t s);
+exf_status launch_kv_append_model(const void* k_new, const void* v_new, int64_t new_stride_vec,
+                                  const int32_t* seq, int32_t seq_stride, const int32_t* n_dev,
+                                  int64_t n_max, int32_t H, int32_t Dh, int32_t C, int32_t replicas,
+                                  void* const* k_caches, void* const* v_caches,
+                                  int32_t* const* lens, int32_t* overflow, cudaStream_t st);
+exf_status launch_attention_model(const void* q, const int32_t* seq, int32_t seq_stride,
+                                  const int32_t* n_dev, int64_t n_max, const int32_t* ctx,
+                                  const void* k, const void* v, int32_t H, int32_t Dh, int32_t C,
+                                  float scale, void* ws, void* out, cudaStream_t st);
+int64_t attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh, int32_t C);
 exf_status launch_gather_wait(uint8_t* own_sym, const Symm& sym, int G, uint64_t* step,
                               int32_t* err, cudaStream_t s);
 exf_status make_weight_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols);
@@ -97,6 +112,7 @@ uint64_t weight_key(int layer, int expert, int E, int which) {
     return ((uint64_t)layer * (uint64_t)E + (uint64_t)expert) * 8u + (uint64_t)which + 1u;
 }
 uint64_t gate_key(int layer) { return 0x6A7E000000000000ULL + (uint64_t)layer; }
+uint64_t attn_key(int layer, int which) { return 0xA770000000000000ULL + (uint64_t)layer * 8u + (uint64_t)which; }
 
 }  // namespace
 }  // namespace exf
@@ -123,6 +139,16 @@ struct exf_model {
     __nv_bfloat16* b2 = nullptr;            // [L][E_loc][d]
     // fp32 mode: the same tensors in fp32 (the bf16 ones are not allocated)
     float *wg32 = nullptr, *w1_32 = nullptr, *b1_32 = nullptr, *w2_32 = nullptr, *b2_32 = nullptr;
+    // attention block (attn_heads > 0): replicated dense weights, projection
+    // buffers, TMA maps, the attention workspace
+    int nh = 0, Dh = 0, Cctx = 0, at_nt = 64, ks_qkv = 1, ks_o = 1;
+    __nv_bfloat16 *wqkv = nullptr, *bqkv = nullptr, *wo = nullptr, *bo = nullptr;  // [L][3d][d] [L][3d] [L][d][d] [L][d]
+    __nv_bfloat16 *qb = nullptr, *kb = nullptr, *vb = nullptr, *ab = nullptr;      // [C][d] each
+    std::vector<CUtensorMap> tm_qkv, tm_o;                                       // per layer weights
+    CUtensorMap tm_res[2]{}, tm_attn{};                                          // token rows as B tiles
+    void* attn_ws = nullptr;
+    int32_t* kv_overflow = nullptr;
+    uint64_t setup_epoch = 0;
     std::vector<CUtensorMap> tmap1, tmap2;  // per layer (weights, TMA tiles)
     CUtensorMap gmap_recv{}, gmap_h{};      // token rows for TMA gather4
     CUtensorMap tmap_x[2]{}, tmap_ht{};     // dense fused mode: resident rows / H as B tiles
@@ -203,6 +229,15 @@ exf_status validate_config(const exf_model_config& c) {
         return invalid("ep_mode must be EXF_EP_COHERENT (0) or EXF_EP_VANILLA (1)");
     if (c.dtype != EXF_DTYPE_BF16 && c.dtype != EXF_DTYPE_F32)
         return invalid("dtype must be EXF_DTYPE_BF16 (0) or EXF_DTYPE_F32 (1)");
+    if (c.attn_heads < 0) return invalid("attn_heads must be >= 0");
+    if (c.attn_heads > 0) {
+        if (c.dtype != EXF_DTYPE_BF16) return invalid("the attention block runs in bf16 only");
+        if (c.d_model % c.attn_heads != 0 || (c.d_model / c.attn_heads != 64 && c.d_model / c.attn_heads != 128))
+            return invalid("d_model / attn_heads (head dim) must be 64 or 128");
+        if (c.context_len < 1) return invalid("context_len must be >= 1 with attention");
+        if (c.context_prefix < 0 || c.context_prefix >= c.context_len)
+            return invalid("context_prefix must be in [0, context_len)");
+    }
     {
         const int64_t C = (int64_t)c.tokens_per_gpu * c.world_size;
         const int64_t esz = c.dtype == EXF_DTYPE_F32 ? 4 : 2;
@@ -234,6 +269,13 @@ exf_status build_layout(exf_model* m) {
     m->sym.comb_x = take(2LL * B * d * esz);
     m->sym.comb_meta = take(2LL * B * (int64_t)sizeof(ResMeta));
     m->sym.comb_flags = take(2LL * B * 8);
+    if (m->nh > 0) {  // replicated context: S = C sequences (token id = sequence id)
+        const int64_t kv = (int64_t)c.num_layers * C * m->nh * m->Cctx * m->Dh * 2;
+        m->sym.kv_k = take(kv);
+        m->sym.kv_v = take(kv);
+        m->sym.kv_len = take((int64_t)c.num_layers * C * 4);
+        m->sym.sflags = take((int64_t)G * 8);
+    }
     m->sym.total = o;
     EXF_CUDA_TRY(cudaMalloc(&m->sym_base, (size_t)o));
     EXF_CUDA_TRY(cudaMemset(m->sym_base, 0, (size_t)o));
@@ -316,6 +358,19 @@ exf_status init_weights(exf_model* m) {
     const int L = c.num_layers, d = c.d_model, f = c.d_ffn;
     if (m->esz == 4) return init_weights_t(m, m->wg32, m->w1_32, m->b1_32, m->w2_32, m->b2_32);
     EXF_TRY(init_weights_t(m, m->wg, m->w1, m->b1, m->w2, m->b2));
+    if (m->nh > 0) {  // attention block: replicated, identical on every rank
+        const int blocks = 148 * 8;
+        for (int j = 0; j < L; ++j) {
+            init_normal_kernel<<<blocks, 256>>>(m->wqkv + (int64_t)j * 3 * d * d, 3LL * d * d, c.seed, attn_key(j, 0), c.init_std);
+            init_normal_kernel<<<blocks, 256>>>(m->bqkv + (int64_t)j * 3 * d, 3LL * d, c.seed, attn_key(j, 1), c.init_std);
+            init_normal_kernel<<<blocks, 256>>>(m->wo + (int64_t)j * d * d, (int64_t)d * d, c.seed, attn_key(j, 2), c.init_std);
+            init_normal_kernel<<<blocks, 256>>>(m->bo + (int64_t)j * d, (int64_t)d, c.seed, attn_key(j, 3), c.init_std);
+            EXF_TRY(make_weight_tmap(&m->tm_qkv[j], m->wqkv + (int64_t)j * 3 * d * d, 3LL * d, d));
+            EXF_TRY(make_weight_tmap(&m->tm_o[j], m->wo + (int64_t)j * d * d, d, d));
+        }
+        EXF_CUDA_TRY(cudaDeviceSynchronize());
+        EXF_LAUNCH_CHECK("attention init");
+    }
     for (int j = 0; j < L; ++j) {
         EXF_TRY(make_weight_tmap(&m->tmap1[j], m->w1 + (int64_t)j * m->E_loc * f * d, (int64_t)m->E_loc * f, d));
         EXF_TRY(make_weight_tmap(&m->tmap2[j], m->w2 + (int64_t)j * m->E_loc * d * f, (int64_t)m->E_loc * d, f));
@@ -471,6 +526,53 @@ FusedArgs fused_args(exf_model* m, int j) {
     return a;
 }
 
+// q, k, v = x Wqkv^T + b -> K/V rows into every replica -> attention over the
+// local replica -> x += attn Wo^T + b (in place in the layer's input rows)
+exf_status run_attention(exf_model* m, int j, cudaStream_t s) {
+    const auto& c = m->cfg;
+    const int d = c.d_model, G = c.world_size, L = c.num_layers, C = m->C;
+    const int32_t* n_dev = m->n_res + (j & 1);
+    DenseArgs qa{};
+    qa.M = 3 * d;
+    qa.K = d;
+    qa.d = d;
+    qa.ksplit = m->ks_qkv;
+    qa.n_dev = n_dev;
+    qa.bias = m->bqkv + (int64_t)j * 3 * d;
+    qa.out[0] = m->qb;
+    qa.out[1] = m->kb;
+    qa.out[2] = m->vb;
+    qa.err = m->err;
+    EXF_TRY(launch_dense_gemm(m->tm_qkv[j], m->tm_res[j & 1], qa, m->at_nt, 0, s));
+    const int64_t layer_off = (int64_t)j * C * m->nh * m->Cctx * m->Dh * 2;
+    void* kc[8];
+    void* vc[8];
+    int32_t* lc[8];
+    for (int r = 0; r < G; ++r) {  // replica 0 = the local one
+        const int peer = (c.rank + r) % G;
+        uint8_t* base = m->peer_ptrs[peer];
+        kc[r] = base + m->sym.kv_k + layer_off;
+        vc[r] = base + m->sym.kv_v + layer_off;
+        lc[r] = reinterpret_cast<int32_t*>(base + m->sym.kv_len) + (int64_t)j * C;
+    }
+    const int32_t* seq = reinterpret_cast<const int32_t*>(m->res_meta[j & 1]);  // ResMeta.token
+    EXF_TRY(launch_kv_append_model(m->kb, m->vb, (int64_t)d / 8, seq, 2, n_dev, C, m->nh, m->Dh, m->Cctx, G, kc,
+                                   vc, lc, m->kv_overflow, s));
+    EXF_TRY(launch_attention_model(m->qb, seq, 2, n_dev, C, lc[0], kc[0], vc[0], m->nh, m->Dh, m->Cctx,
+                                   1.0f / std::sqrt((float)m->Dh), m->attn_ws, m->ab, s));
+    DenseArgs oa{};
+    oa.M = d;
+    oa.K = d;
+    oa.d = d;
+    oa.ksplit = m->ks_o;
+    oa.n_dev = n_dev;
+    oa.bias = m->bo + (int64_t)j * d;
+    oa.out[0] = m->res_x[j & 1];
+    oa.err = m->err;
+    (void)L;
+    return launch_dense_gemm(m->tm_o[j], m->tm_attn, oa, m->at_nt, 1, s);
+}
+
 exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStream_t s) {
     const auto& c = m->cfg;
     if (!m->connected) return invalid("model is not connected to its peers (exf_model_connect)");
@@ -519,6 +621,11 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
                                   c.world_size, c.tokens_per_gpu, c.d_model * m->esz / 16, c.num_layers, j, m->step,
                                   m->res_x[o], m->res_meta[o], m->n_res + o, m->err, phase - 6, s);
         }
+        case 8: {  // attention block of layer j (before its MoE)
+            if (j < 0 || j >= c.num_layers) return invalid("layer out of range");
+            if (m->nh <= 0) return invalid("attention block disabled (attn_heads = 0)");
+            return run_attention(m, j, s);
+        }
         default:
             return invalid("unknown phase");
     }
@@ -527,6 +634,7 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
 exf_status run_step(exf_model* m, const void* x_in, cudaStream_t s) {
     EXF_TRY(run_phase(m, 0, 0, x_in, s));
     for (int j = 0; j < m->cfg.num_layers; ++j) {
+        if (m->nh > 0) EXF_TRY(run_phase(m, 8, j, nullptr, s));
         if (m->fused) {
             EXF_TRY(run_phase(m, 5, j, nullptr, s));
         } else {
@@ -555,6 +663,11 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     m->E_loc = c.num_experts / c.world_size;
     m->C = c.tokens_per_gpu * c.world_size;
     m->esz = c.dtype == EXF_DTYPE_F32 ? 4 : 2;
+    if (c.attn_heads > 0) {
+        m->nh = c.attn_heads;
+        m->Dh = c.d_model / c.attn_heads;
+        m->Cctx = c.context_len;
+    }
     const size_t ew = (size_t)m->esz / 2;  // bf16-sized elements per stored element
     cudaGetDevice(&m->device);
     const int L = c.num_layers, E = c.num_experts, d = c.d_model, f = c.d_ffn, C = m->C;
@@ -656,6 +769,26 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         EXF_M(dalloc(&m->tstamp, (size_t)6 * kTimelineCtas * 16));
         EXF_M(dalloc(&m->tl, (size_t)L * 3 * 8));
     }
+    if (m->nh > 0) {
+        EXF_M(dalloc(&m->wqkv, (size_t)L * 3 * d * d));
+        EXF_M(dalloc(&m->bqkv, (size_t)L * 3 * d));
+        EXF_M(dalloc(&m->wo, (size_t)L * d * d));
+        EXF_M(dalloc(&m->bo, (size_t)L * d));
+        EXF_M(dalloc(&m->qb, (size_t)C * d));
+        EXF_M(dalloc(&m->kb, (size_t)C * d));
+        EXF_M(dalloc(&m->vb, (size_t)C * d));
+        EXF_M(dalloc(&m->ab, (size_t)C * d));
+        EXF_M(dalloc(&m->kv_overflow, 1));
+        m->tm_qkv.resize(L);
+        m->tm_o.resize(L);
+        m->at_nt = C <= 64 ? 64 : 128;
+        m->ks_qkv = dense_gemm_ksplit(3 * d, d);
+        m->ks_o = dense_gemm_ksplit(d, d);
+        const int64_t wsb = attention_workspace_bytes(C, m->nh, m->Dh, m->Cctx);
+        if (wsb > 0) EXF_M(cuda_status_ok(cudaMalloc(&m->attn_ws, (size_t)wsb), "attention workspace"));
+        for (int i = 0; i < 2; ++i) EXF_M(make_tile_tmap(&m->tm_res[i], m->res_x[i], C, d, m->at_nt));
+        EXF_M(make_tile_tmap(&m->tm_attn, m->ab, C, d, m->at_nt));
+    }
     EXF_M(dalloc(&m->d_peers, (size_t)c.world_size));
     EXF_M(build_layout(m));
     if (m->esz == 2) {
@@ -693,7 +826,8 @@ exf_status exf_model_destroy(exf_model* m) {
                     m->cta_cnt, m->gbar, m->tl, m->ws, m->item_ctr, m->hdone, m->fbar,
                     m->f_cta_cnt, m->f_pieces, m->f_piece_off,
                     m->d_peers, m->sym_base, m->tstamp, m->wg32, m->w1_32, m->b1_32, m->w2_32,
-                    m->b2_32};
+                    m->b2_32, m->wqkv, m->bqkv, m->wo, m->bo, m->qb, m->kb, m->vb, m->ab,
+                    m->attn_ws, m->kv_overflow};
     for (void* p : bufs)
         if (p) cudaFree(p);
     delete m;
@@ -883,6 +1017,76 @@ exf_status exf_model_set_placement(exf_model* m, const int32_t* h_assign) {
     return set_placement(m, h_assign);
 }
 
+exf_status exf_model_context_setup(exf_model* m, exf_stream_t stream) {
+    if (!m) return invalid("null model");
+    if (m->nh <= 0) return invalid("attention block disabled (attn_heads = 0)");
+    if (!m->connected) return invalid("model is not connected to its peers (exf_model_connect)");
+    const auto& c = m->cfg;
+    ContextSetupArgs a{};
+    a.G = c.world_size;
+    a.rank = c.rank;
+    a.L = c.num_layers;
+    a.S = m->C;
+    a.H = m->nh;
+    a.Dh = m->Dh;
+    a.Cctx = m->Cctx;
+    a.prefix = c.context_prefix;
+    a.seed = c.seed ^ 0xC0FFEEULL;
+    a.peers = m->d_peers;
+    a.kv_k = m->sym.kv_k;
+    a.kv_v = m->sym.kv_v;
+    a.kv_len = m->sym.kv_len;
+    ++m->setup_epoch;
+    return launch_context_setup(a, m->sym.sflags, m->setup_epoch, m->err, static_cast<cudaStream_t>(stream));
+}
+
+exf_status exf_model_read_kv(exf_model* m, int32_t layer, int32_t seq, int32_t pos0, int32_t count,
+                             uint16_t* h_k, uint16_t* h_v) {
+    if (!m) return invalid("null model");
+    if (m->nh <= 0) return invalid("attention block disabled (attn_heads = 0)");
+    if (layer < 0 || layer >= m->cfg.num_layers || seq < 0 || seq >= m->C || pos0 < 0 || count < 0 ||
+        pos0 + count > m->Cctx)
+        return invalid("kv read out of range");
+    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    const int64_t per_head = (int64_t)m->Cctx * m->Dh;
+    for (int which = 0; which < 2; ++which) {
+        uint16_t* dst = which == 0 ? h_k : h_v;
+        if (!dst) continue;
+        const uint8_t* base = m->sym_base + (which == 0 ? m->sym.kv_k : m->sym.kv_v);
+        for (int h = 0; h < m->nh; ++h) {
+            const int64_t off = ((((int64_t)layer * m->C + seq) * m->nh + h) * per_head + (int64_t)pos0 * m->Dh) * 2;
+            // [count][H][Dh] on the host: strided copy of the head's rows
+            EXF_CUDA_TRY(cudaMemcpy2D(dst + (int64_t)h * m->Dh, (size_t)m->nh * m->Dh * 2, base + off,
+                                      (size_t)m->Dh * 2, (size_t)m->Dh * 2, (size_t)count, cudaMemcpyDeviceToHost));
+        }
+    }
+    return EXF_OK;
+}
+
+exf_status exf_model_read_kv_len(exf_model* m, int32_t layer, int32_t* h_len) {
+    if (!m || !h_len) return invalid("null argument");
+    if (m->nh <= 0) return invalid("attention block disabled (attn_heads = 0)");
+    if (layer < 0 || layer >= m->cfg.num_layers) return invalid("layer out of range");
+    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    EXF_CUDA_TRY(cudaMemcpy(h_len, m->sym_base + m->sym.kv_len + (int64_t)layer * m->C * 4, (size_t)m->C * 4,
+                            cudaMemcpyDeviceToHost));
+    return EXF_OK;
+}
+
+exf_status exf_model_read_attn(exf_model* m, int32_t layer, uint16_t* h_wqkv, uint16_t* h_bqkv, uint16_t* h_wo,
+                               uint16_t* h_bo) {
+    if (!m) return invalid("null model");
+    if (m->nh <= 0) return invalid("attention block disabled (attn_heads = 0)");
+    if (layer < 0 || layer >= m->cfg.num_layers) return invalid("layer out of range");
+    const int64_t d = m->cfg.d_model;
+    EXF_CUDA_TRY(cudaDeviceSynchronize());
+    if (h_wqkv) EXF_CUDA_TRY(cudaMemcpy(h_wqkv, m->wqkv + layer * 3 * d * d, 3 * d * d * 2, cudaMemcpyDeviceToHost));
+    if (h_bqkv) EXF_CUDA_TRY(cudaMemcpy(h_bqkv, m->bqkv + layer * 3 * d, 3 * d * 2, cudaMemcpyDeviceToHost));
+    if (h_wo) EXF_CUDA_TRY(cudaMemcpy(h_wo, m->wo + layer * d * d, d * d * 2, cudaMemcpyDeviceToHost));
+    if (h_bo) EXF_CUDA_TRY(cudaMemcpy(h_bo, m->bo + layer * d, d * 2, cudaMemcpyDeviceToHost));
+    return EXF_OK;
+}
+
 exf_status exf_model_read_gate(exf_model* m, int32_t layer, uint16_t* h_wg) {
     if (!m || !h_wg) return invalid("null argument");
     if (layer < 0 || layer >= m->cfg.num_layers) return invalid("layer out of range");
@@ -941,8 +1145,9 @@ exf_status exf_model_replay(exf_model* m, exf_stream_t stream) {
 
 int32_t exf_model_launches_per_step(exf_model* m) {
     if (!m) return 0;
-    // begin, L x (fused layer | gate_dispatch + GEMM1 + GEMM2) [+ combine send + wait], gather send + wait
-    const int per_layer = (m->fused ? 1 : 3) + (m->cfg.ep_mode == EXF_EP_VANILLA ? 2 : 0);
+    // begin, L x ([qkv + kv append + attention + o-proj] + fused layer | gate_dispatch + GEMM1 +
+    // GEMM2) [+ combine send + wait], gather send + wait
+    const int per_layer = (m->nh > 0 ? 4 : 0) + (m->fused ? 1 : 3) + (m->cfg.ep_mode == EXF_EP_VANILLA ? 2 : 0);
     return 1 + per_layer * m->cfg.num_layers + 2;
 }
 
@@ -972,7 +1177,13 @@ exf_status exf_model_read_ffn_timeline(exf_model* m, uint64_t* h, int32_t ctas) 
 
 exf_status exf_model_describe(exf_model* m, char* buf, int32_t len) {
     if (!m || !buf || len < 1) return invalid("bad argument");
-    std::string s = "{\"dtype\": \"" + std::string(m->esz == 4 ? "f32" : "bf16") + "\", \"token_tile\": " + std::to_string(m->nmax) +
+    std::string s = "{\"dtype\": \"" + std::string(m->esz == 4 ? "f32" : "bf16") + "\", " +
+                    (m->nh > 0 ? "\"attention\": {\"heads\": " + std::to_string(m->nh) + ", \"head_dim\": " +
+                                    std::to_string(m->Dh) + ", \"context_len\": " + std::to_string(m->Cctx) +
+                                    ", \"ksplit_qkv\": " + std::to_string(m->ks_qkv) + ", \"ksplit_o\": " +
+                                    std::to_string(m->ks_o) + "}, "
+                              : std::string()) +
+                    "\"token_tile\": " + std::to_string(m->nmax) +
                     ", \"experts_per_rank\": " + std::to_string(m->E_loc) +
                     ", \"capacity_tokens\": " + std::to_string(m->C) +
                     ", \"ep_mode\": \"" + std::string(m->cfg.ep_mode == EXF_EP_VANILLA ? "vanilla" : "coherent") + "\"";

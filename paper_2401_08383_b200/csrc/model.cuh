@@ -39,6 +39,9 @@ struct ResMeta {
 struct Symm {  // byte offsets inside the symmetric region
     int64_t recv_x, recv_meta, recv_cnt, flags, gather_x, gflags, cflags;
     int64_t comb_x, comb_meta, comb_flags;  // vanilla-EP combine: [2 layer parity][B] home slots
+    // replicated context (attention block): K, V [L][S][H][Cctx][Dh] bf16,
+    // lengths [L][S] int32, setup-AllGather flags [G] u64 (0 when disabled)
+    int64_t kv_k, kv_v, kv_len, sflags;
     int64_t total;
 };
 // fused layer kernel: per-(parity, src rank, src CTA) dispatch-complete flags
@@ -99,6 +102,23 @@ struct FfnArgs {
     int32_t* err;
     uint64_t* tstamp;            // optional per-CTA globaltimer stamps [grid][16] (diagnostics)
     unsigned long long* tl;      // optional step timeline [4] (diagnostics)
+};
+
+// Arguments of one dense decode GEMM of the attention block (attn_block.cu).
+struct DenseArgs {
+    int32_t M, K, d, ksplit;
+    const int32_t* n_dev;          // resident tokens (device scalar)
+    const __nv_bfloat16* bias;     // [M]
+    __nv_bfloat16* out[3];         // MODE 0: q, k, v [C][d]; MODE 1: out[0] = x [C][d] (in place)
+    int32_t* err;
+};
+
+// Arguments of the setup AllGather of the replicated context (attn_block.cu).
+struct ContextSetupArgs {
+    int32_t G, rank, L, S, H, Dh, Cctx, prefix;
+    uint64_t seed;
+    uint8_t* const* peers;  // device array [G] of symmetric-region bases
+    int64_t kv_k, kv_v, kv_len;
 };
 
 // Arguments of one fp32-mode FFN GEMM launch (ffn_f32.cu).

@@ -2,11 +2,15 @@
 // exflow::simulate (proj/src/sim.cpp:110-145), as exact integer counters.
 //
 // One thread follows one token through the L layers (the coherent location is
-// a sequential dependency), token rows are staged through shared memory with
-// coalesced loads (row stride padded to L|1 so per-thread column reads are
-// bank-conflict free), the placement table [L][E] lives in shared memory, and
-// counters are reduced warp -> CTA -> one 64-bit atomic per counter per CTA
-// (integer sums: order-independent, bit-exact).
+// a sequential dependency). v2 after the round-1 capture (239 us for 201 MB
+// of ids, 0.13 of HBM): persistent CTAs stream the trace through a software
+// pipeline (the next tile's rows in flight as 16-byte non-allocating loads
+// while the current tile is replayed from shared memory, rows padded to L|1
+// words so per-thread column reads are bank-conflict free); the placement
+// table lives in shared memory with each entry packed as {gpu, node} so the
+// loop does no integer division; counters are reduced warp -> CTA -> one
+// 64-bit atomic per counter per CTA (integer sums: order-independent,
+// bit-exact).
 // Algorithmic bytes per launch: 4*T*L (+4*T homes when given).
 #include "common.cuh"
 
@@ -18,6 +22,7 @@ namespace exf {
 namespace {
 
 constexpr int kReplayThreads = 256;
+constexpr int kReplayPrefetch = 8;  // int4 per thread per tile (tile <= 256 tokens x 32 layers)
 
 __global__ void __launch_bounds__(kReplayThreads)
 route_replay_kernel(const int32_t* __restrict__ paths, const int32_t* __restrict__ homes,
@@ -26,59 +31,94 @@ route_replay_kernel(const int32_t* __restrict__ paths, const int32_t* __restrict
                     unsigned long long* __restrict__ out) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int32_t stride = L | 1;
-    int32_t* s_assign = reinterpret_cast<int32_t*>(smem);
-    int32_t* tile = s_assign + ((L * E + 3) & ~3);
+    int32_t* s_tab = reinterpret_cast<int32_t*>(smem);  // [L][E] gpu | node << 16
+    int32_t* tile = s_tab + ((L * E + 3) & ~3);
     __shared__ unsigned long long s_cnt[6];
+    const int tid = threadIdx.x;
+    for (int32_t i = tid; i < L * E; i += blockDim.x) {
+        const int32_t g = assign[i];
+        s_tab[i] = g | ((g / gpus_per_node) << 16);
+    }
+    if (tid < 6) s_cnt[tid] = 0ull;
 
-    for (int32_t i = threadIdx.x; i < L * E; i += blockDim.x) s_assign[i] = assign[i];
-    if (threadIdx.x < 6) s_cnt[threadIdx.x] = 0ull;
-
-    int64_t gl = 0, nl = 0, away = 0, moves = 0, hi = 0, he = 0;
+    const bool vec = ((reinterpret_cast<uintptr_t>(paths) | (uintptr_t)(L * 4)) & 15) == 0 &&
+                     L * kReplayThreads <= kReplayPrefetch * 4 * kReplayThreads;
     const int64_t tiles = (T + kReplayThreads - 1) / kReplayThreads;
+    int4 pre[kReplayPrefetch];
+    auto fetch = [&](int64_t tile_id) {
+        const int64_t t0 = tile_id * kReplayThreads;
+        const int32_t nvec = (int32_t)imin64(kReplayThreads, T - t0) * L / 4;
+        const int4* s4 = reinterpret_cast<const int4*>(paths + t0 * L);
+#pragma unroll
+        for (int u = 0; u < kReplayPrefetch; ++u) {
+            const int32_t i = tid + u * kReplayThreads;
+            if (i < nvec) pre[u] = ld_nc_v4(s4 + i);
+        }
+    };
+    int64_t gl = 0, nl = 0, away = 0, moves = 0, hi = 0, he = 0;
+    if (vec && blockIdx.x < tiles) fetch(blockIdx.x);
     for (int64_t tile_id = blockIdx.x; tile_id < tiles; tile_id += gridDim.x) {
         const int64_t t0 = tile_id * kReplayThreads;
         const int32_t nt = (int32_t)imin64(kReplayThreads, T - t0);
-        const int32_t nints = nt * L;
-        const int32_t* src = paths + t0 * L;
-        __syncthreads();
-        for (int32_t i = threadIdx.x; i < nints; i += blockDim.x) {
-            const int32_t r = i / L;
-            tile[r * stride + (i - r * L)] = __ldg(src + i);
+        __syncthreads();  // previous tile replayed (and the table built)
+        if (vec) {
+            const int32_t nvec = nt * L / 4;
+#pragma unroll
+            for (int u = 0; u < kReplayPrefetch; ++u) {
+                const int32_t i = tid + u * kReplayThreads;
+                if (i < nvec) {
+                    const int32_t e0 = 4 * i, r = e0 / L, c = e0 - r * L;  // L % 4 == 0: no row straddle
+                    int32_t* d = tile + r * stride + c;
+                    d[0] = pre[u].x;
+                    d[1] = pre[u].y;
+                    d[2] = pre[u].z;
+                    d[3] = pre[u].w;
+                }
+            }
+            if (tile_id + gridDim.x < tiles) fetch(tile_id + gridDim.x);  // in flight during the replay
+        } else {
+            const int32_t* src = paths + t0 * L;
+            for (int32_t i = tid; i < nt * L; i += blockDim.x) {
+                const int32_t r = i / L;
+                tile[r * stride + (i - r * L)] = __ldg(src + i);
+            }
         }
         __syncthreads();
-        if ((int32_t)threadIdx.x < nt) {
-            const int64_t t = t0 + threadIdx.x;
+        if (tid < nt) {
+            const int64_t t = t0 + tid;
             const int32_t home = homes ? __ldg(homes + t) : (int32_t)(t % gpus);
-            int32_t location = home;
-            const int32_t* p = tile + threadIdx.x * stride;
+            const int32_t home_node = home / gpus_per_node;
+            int32_t loc = home, loc_node = home_node;
+            const int32_t* p = tile + tid * stride;
             for (int32_t j = 0; j < L; ++j) {
                 const int32_t e = p[j];
-                const int32_t eg = ((unsigned)e < (unsigned)E) ? s_assign[j * E + e] : location;
-                gl += (eg == location);
-                nl += (eg / gpus_per_node == location / gpus_per_node);
+                const int32_t ent = ((unsigned)e < (unsigned)E) ? s_tab[j * E + e] : (loc | (loc_node << 16));
+                const int32_t eg = ent & 0xFFFF, en = ent >> 16;
+                gl += (eg == loc);
+                nl += (en == loc_node);
                 away += (eg != home);
-                if (eg != location) {
+                if (eg != loc) {
                     ++moves;
                     if (mode == 1) {
-                        if (eg / gpus_per_node != location / gpus_per_node) ++he; else ++hi;
+                        if (en != loc_node) ++he; else ++hi;
                     }
                 }
                 if (mode == 0 && eg != home) {
-                    if (eg / gpus_per_node != home / gpus_per_node) he += 2; else hi += 2;
+                    if (en != home_node) he += 2; else hi += 2;
                 }
-                location = eg;
+                loc = eg;
+                loc_node = en;
             }
         }
     }
     int64_t v[6] = {gl, nl, away, moves, hi, he};
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
-        const int64_t s = warp_sum(v[k]);
-        if ((threadIdx.x & 31) == 0 && s) atomicAdd(&s_cnt[k], (unsigned long long)s);
+        const int64_t sm = warp_sum(v[k]);
+        if ((tid & 31) == 0 && sm) atomicAdd(&s_cnt[k], (unsigned long long)sm);
     }
     __syncthreads();
-    if (threadIdx.x < 6 && s_cnt[threadIdx.x])
-        atomicAdd(&out[threadIdx.x], s_cnt[threadIdx.x]);
+    if (tid < 6 && s_cnt[tid]) atomicAdd(&out[tid], s_cnt[tid]);
 }
 
 }  // namespace
@@ -96,6 +136,7 @@ extern "C" exf_status exf_route_replay(const int32_t* d_paths, const int32_t* d_
     if (mode != 0 && mode != 1) return invalid("mode must be 0 (vanilla) or 1 (coherent)");
     if ((int64_t)L * E * 4 + (int64_t)kReplayThreads * (L | 1) * 4 > 200 * 1024)
         return invalid("placement table too large for the replay kernel");
+    if (num_nodes * gpus_per_node > 0x7FFF) return invalid("too many GPUs for the replay kernel");
     if (!d_paths || !d_assign || !d_out) return invalid("null device pointer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t smem = (size_t)((L * E + 3) & ~3) * 4 + (size_t)kReplayThreads * (L | 1) * 4;
@@ -106,7 +147,7 @@ extern "C" exf_status exf_route_replay(const int32_t* d_paths, const int32_t* d_
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t tiles = (T + kReplayThreads - 1) / kReplayThreads;
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 4LL * sms));
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 3LL * sms));
     route_replay_kernel<<<blocks, kReplayThreads, smem, s>>>(
         d_paths, d_homes, d_assign, T, L, E, gpus_per_node, num_nodes * gpus_per_node, mode,
         reinterpret_cast<unsigned long long*>(d_out));

@@ -16,7 +16,7 @@ import numpy as np
 from . import _capi
 
 PHASE_BEGIN, PHASE_DISPATCH, PHASE_FFN, PHASE_GATHER_SEND, PHASE_GATHER_WAIT, PHASE_FUSED, \
-    PHASE_COMBINE_SEND, PHASE_COMBINE_WAIT = range(8)
+    PHASE_COMBINE_SEND, PHASE_COMBINE_WAIT, PHASE_ATTN = range(9)
 EP_COHERENT, EP_VANILLA = 0, 1  # include/exflow_c.h EXF_EP_*
 DTYPE_BF16, DTYPE_F32 = 0, 1    # include/exflow_c.h EXF_DTYPE_*
 
@@ -41,6 +41,12 @@ class MoeModelConfig:
     # DTYPE_BF16 (tcgen05 path) or DTYPE_F32 (fp32 mode: fp32 weights, states,
     # gate and SIMT FFN; the north star's 1e-5 bar)
     dtype: int = 0
+    # coherent attention block before every MoE layer (bf16): heads (0 = off),
+    # replicated context capacity per sequence, prompt length written by
+    # context_setup() (the setup AllGather)
+    attn_heads: int = 0
+    context_len: int = 0
+    context_prefix: int = 0
 
     @property
     def capacity(self) -> int:
@@ -59,7 +65,7 @@ class MoeModelConfig:
         return _capi.ModelConfigC(self.num_experts, self.num_layers, self.d_model, self.d_ffn,
                                   self.top_k, self.tokens_per_gpu, self.world_size, self.rank,
                                   self.seed, self.init_std, self.gate_affinity, self.ep_mode,
-                                  self.dtype)
+                                  self.dtype, self.attn_heads, self.context_len, self.context_prefix)
 
 
 def _stream_ptr(stream) -> Optional[int]:
@@ -214,6 +220,36 @@ class MoeModel:
             raise _capi.ExflowInvalidArgument("placement must be [L][E]")
         _capi.call("exf_model_set_placement", self._h, a.ctypes.data)
         self.assign = a
+
+    # ------------------------------------------------------------ attention block
+    def context_setup(self, stream=None) -> None:
+        """Setup AllGather of the replicated context (every rank must call it)."""
+        _capi.call("exf_model_context_setup", self._h, _stream_ptr(stream))
+
+    def kv_rows(self, layer: int, seq: int, pos0: int, count: int):
+        """(K, V) rows of this rank's replica: [count][H][Dh] bf16 bits each."""
+        cfg = self.config
+        H, Dh = cfg.attn_heads, cfg.d_model // max(cfg.attn_heads, 1)
+        k = np.empty((count, H, Dh), np.uint16)
+        v = np.empty((count, H, Dh), np.uint16)
+        _capi.call("exf_model_read_kv", self._h, layer, seq, pos0, count, k.ctypes.data, v.ctypes.data)
+        return k, v
+
+    def kv_len(self, layer: int) -> np.ndarray:
+        out = np.empty(self.config.capacity, np.int32)
+        _capi.call("exf_model_read_kv_len", self._h, layer, out.ctypes.data)
+        return out
+
+    def attn_weights(self, layer: int):
+        """(Wqkv [3d][d], bqkv [3d], Wo [d][d], bo [d]) bf16 bits."""
+        d = self.config.d_model
+        wqkv = np.empty((3 * d, d), np.uint16)
+        bqkv = np.empty(3 * d, np.uint16)
+        wo = np.empty((d, d), np.uint16)
+        bo = np.empty(d, np.uint16)
+        _capi.call("exf_model_read_attn", self._h, layer, wqkv.ctypes.data, bqkv.ctypes.data,
+                   wo.ctypes.data, bo.ctypes.data)
+        return wqkv, bqkv, wo, bo
 
     def gate_weights(self, layer: int) -> np.ndarray:
         cfg = self.config

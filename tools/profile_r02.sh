@@ -7,7 +7,7 @@ CS=/usr/local/cuda/bin/compute-sanitizer
 # --- ncu: full set of the dominant kernel (one launch mid-step), the routing kernels, the fp32 FFN
 timeout 600 $NCU --set full --import-source on --clock-control none -k regex:layer_fused --launch-skip 30 --launch-count 1 \
   -o gpurun_out/r2p/fused_full python tools/ncu_targets.py step > gpurun_out/r2p/ncu_fused.log 2>&1
-timeout 600 $NCU --set full --clock-control none -k regex:"hist_partial|hist_reduce|route_replay" --launch-count 6 \
+timeout 600 $NCU --set full --clock-control none -k regex:"hist_kernel|route_replay" --launch-count 4 \
   -o gpurun_out/r2p/routing_full python tools/ncu_targets.py routing > gpurun_out/r2p/ncu_routing.log 2>&1
 timeout 600 $NCU --set full --clock-control none -k regex:"ffn_f32|gate_dispatch" --launch-skip 6 --launch-count 3 \
   -o gpurun_out/r2p/fp32_full python tools/ncu_targets.py fp32 > gpurun_out/r2p/ncu_fp32.log 2>&1
