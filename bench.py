@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-parity", action="store_true", help="skip the per-placement checked step")
     p.add_argument("--no-fp32", action="store_true", help="skip the fp32-mode sub-measurement")
+    p.add_argument("--no-configs4", action="store_true",
+                   help="skip the BASELINE configs[4] long-context sub-measurement")
     p.add_argument("--no-routing-kernels", action="store_true",
                    help="skip the histogram / replay kernel measurements")
     return p.parse_args()
@@ -470,6 +472,19 @@ def main():
                   "host_threads": os.cpu_count(), "objective": rep4.objective}
     barrier()
 
+    # ---- BASELINE configs[4]: E=64 top-1, 8 experts/GPU at N=8, long-context
+    # decode with the coherent attention block over the replicated 16k context,
+    # the context AllGather, and the online affinity-histogram rebuild
+    configs4 = None
+    if not a.no_configs4:
+        try:
+            configs4 = measure_configs4(a, n, rank, stream, barrier, allmax, allsum_i64, check_step,
+                                        hbm_peak)
+        except Exception as e:  # informational; never blocks the headline line
+            configs4 = {"error": f"{type(e).__name__}: {e}"}
+        log(f"[bench] configs4: {json.dumps(configs4)[:300]}")
+        barrier()
+
     # ---- CPU baseline (rank 0, at every N; the other ranks wait): whole
     # decode steps of the same G*B tokens on the host cores, nothing
     # extrapolated; the reference's own CPU routing bookkeeping included
@@ -527,6 +542,7 @@ def main():
                            "configs4_scale": solve4},
         "expert_migration": migration,
         "fp32_mode": fp32,
+        "configs4_long_context": configs4,
         "e2e": {"value": a.batch * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "roofline": {"kernel": ("layer_fused_kernel (gate+dispatch+GEMM1+GEMM2 per layer, tcgen05)"
@@ -556,6 +572,139 @@ def main():
     model.close()
     if n > 1:
         dist.destroy_process_group()
+
+
+def measure_configs4(a, n, rank, stream, barrier, allmax, allsum_i64, check_step, hbm_peak):
+    """BASELINE configs[4] at this N: GPT-MoE with 64 experts top-1 (64/N per
+    GPU; 8 at N=8), 24 layers, d=1024 (16 heads x 64), d_ffn=4096, 8 decode
+    sequences per GPU, every layer = coherent attention block over the
+    replicated context (16k keys capacity, ~16k resident) + MoE layer.
+    Measures: the online histogram rebuild (profiling steps -> fused histogram
+    -> solve_staged -> NCCL expert migration at N>1), graph-replayed decode
+    steps (CUDA events, max over ranks), per-phase HBM fractions from one
+    phased step, and one fully checked step (attention + MoE)."""
+    import torch
+    from paper_2401_08383_b200 import affinity, dist as xd, placement as pl
+    from paper_2401_08383_b200.model import (PHASE_ATTN, PHASE_BEGIN, PHASE_FUSED, PHASE_GATHER_SEND,
+                                             PHASE_GATHER_WAIT, MoeModel, MoeModelConfig)
+    E, L, d, dff, B, H = 64, a.layers, 1024, 4096, 8, 16
+    if E % n:
+        return {"skipped": f"64 experts not divisible by {n} GPUs"}
+    cap = 16384
+    prefix = max(1024, cap - (a.steps + a.warmup + 48))
+    topo = affinity.Topology(1, n)
+    vanilla = pl.contiguous_placement(E, L, topo)
+    cfg = MoeModelConfig(num_experts=E, num_layers=L, d_model=d, d_ffn=dff, tokens_per_gpu=B, world_size=n,
+                         rank=rank, seed=4321, gate_affinity=a.gate_affinity, attn_heads=H, context_len=cap,
+                         context_prefix=prefix)
+    m = MoeModel(cfg, vanilla)
+    if n > 1:
+        m.connect(xd.exchange_handles(m.ipc_handle()))
+    t0 = time.perf_counter()
+    m.context_setup(stream, phase=3)  # every rank synthesizes the same prompt context locally
+    stream.synchronize()
+    setup_s = allmax(time.perf_counter() - t0)
+    barrier()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    # online histogram rebuild: held-out profiling steps on the vanilla placement
+    for k in range(3):
+        gp = torch.Generator(device="cpu").manual_seed(77_000 + 31 * k + rank)
+        m.step(torch.randn(B, d, generator=gp).to(torch.bfloat16).to(dev), stream)
+    stream.synchronize()
+    m.check()
+    t0 = time.perf_counter()
+    counts = allsum_i64(m.affinity_counts())
+    snap_ms = (time.perf_counter() - t0) * 1e3
+    t0 = time.perf_counter()
+    aff, rep = pl.solve_staged(counts, topo, pl.AnnealParams(seed=7))
+    solve_ms = (time.perf_counter() - t0) * 1e3
+    migration = None
+    if n > 1:
+        from paper_2401_08383_b200 import migrate
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        moved = migrate.migrate_nccl(m, aff)
+        torch.cuda.synchronize()
+        mig_s = allmax(time.perf_counter() - t0)
+        per_expert = 2 * d * dff * 2 + (d + dff) * 2
+        migration = {"experts_moved": moved, "bytes": moved * per_expert, "wall_ms": mig_s * 1e3,
+                     "gbs": moved * per_expert / mig_s / 1e9 if mig_s > 0 else None}
+    else:
+        aff = vanilla  # one GPU: every expert is local, the placement is trivial
+    g = torch.Generator(device="cpu").manual_seed(500 + rank)
+    x = torch.randn(B, d, generator=g).to(torch.bfloat16).to(dev)
+    m.capture(x, stream)
+    for _ in range(max(3, a.warmup)):
+        m.replay(stream)
+    stream.synchronize()
+    m.check()
+    m.reset_stats()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        m.replay(stream)
+    e1.record(stream)
+    stream.synchronize()
+    m.check()
+    ms = allmax(e0.elapsed_time(e1)) / a.steps
+    barrier()
+    crossed = allsum_i64(m.crossed())
+    frac = float(crossed.sum()) / (B * n * L * a.steps)
+    # per-phase timing of one step (each phase synchronised; events on the stream)
+    att_ms, moe_ms = [], []
+    att_bytes, moe_bytes = [], []
+    fused = m.describe().get("path") == "fused"
+    with torch.cuda.stream(stream):
+        m.phase(PHASE_BEGIN, 0, x, stream)
+        for j in range(L):
+            nres = m.resident(j % 2)[1]
+            lens = m.kv_len(j)
+            ctx_keys = int(sum(int(lens[t]) + 1 for t in nres[:, 0]))
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record(stream)
+            m.phase(PHASE_ATTN, j, None, stream)
+            ev[1].record(stream)
+            if fused:
+                m.phase(PHASE_FUSED, j, None, stream)
+            ev[2].record(stream)
+            stream.synchronize()
+            att_ms.append(ev[0].elapsed_time(ev[1]))
+            moe_ms.append(ev[1].elapsed_time(ev[2]))
+            att_bytes.append(ctx_keys * H * (d // H) * 4 + 8 * d * d)  # K+V rows read + Wqkv/Wo
+            r = m.routes()
+            toks = r[:, j][r[:, j] >= 0]
+            moe_bytes.append(len(set(toks[aff[j][toks] == rank].tolist())) * (4 * d * dff + 2 * (d + dff)))
+        m.phase(PHASE_GATHER_SEND, 0, None, stream)
+        m.phase(PHASE_GATHER_WAIT, 0, None, stream)
+        stream.synchronize()
+    m.check()
+    att_gbs = sum(att_bytes) / (sum(att_ms) * 1e-3) / 1e9
+    moe_gbs = sum(moe_bytes) / (sum(moe_ms) * 1e-3) / 1e9 if sum(moe_ms) > 0 else None
+    chk = check_step(m, x, aff, rows_per_layer=1)
+    lens_now = m.kv_len(0)
+    m.close()
+    torch.cuda.empty_cache()
+    return {"workload": "GPT-MoE configs[4]: 64 experts top-1 (64/N per GPU), 24 layers, d 1024 (16 heads x 64), "
+                        "d_ffn 4096, 8 decode sequences per GPU, coherent attention over the replicated context",
+            "value": B * n / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms, "steps": a.steps,
+            "context_keys": {"capacity": cap, "prompt": prefix, "at_check": int(lens_now.max())},
+            "routed_fraction": frac, "parity": chk["parity"], "failures": chk["failures"],
+            "attention_max_rel_err_sampled": chk.get("attention_max_rel_err_sampled"),
+            "context_setup_s": setup_s,
+            "histogram_rebuild": {"profile_steps": 3, "snapshot_and_sum_ms": snap_ms, "solve_ms": solve_ms,
+                                  "solver": rep.solver, "objective": rep.objective, "migration": migration},
+            "per_phase": {"attention_block_ms_per_layer": statistics.mean(att_ms),
+                          "attention_block_gbs": att_gbs, "attention_block_frac": att_gbs / hbm_peak,
+                          "moe_layer_ms_per_layer": statistics.mean(moe_ms) if fused else None,
+                          "moe_layer_gbs": moe_gbs, "moe_layer_frac": (moe_gbs / hbm_peak) if moe_gbs else None,
+                          "timing": "one phased step, each layer's attention block (QKV GEMM + K/V append + "
+                                    "attention + O GEMM) and fused MoE kernel bracketed by CUDA events with a "
+                                    "sync per layer (cold starts included)",
+                          "bytes_model": "attention: K+V rows read for every resident token's context + 8 d^2 "
+                                         "projection weights; MoE: weights of the active local experts"}}
 
 
 def measure_fp32(a, n, rank, assign, make_model, stream, barrier, allmax, check_step, hbm_peak):

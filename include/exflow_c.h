@@ -261,6 +261,11 @@ exf_status exf_model_step_phase(exf_model* model, int32_t phase, int32_t layer,
  * into EVERY rank's replica over NVLink, sets the lengths, then flags every
  * peer and waits for all of them on `stream`. All ranks must call it. */
 exf_status exf_model_context_setup(exf_model* model, exf_stream_t stream);
+/* The same in two halves for G ranks emulated in one stream (lock-step):
+ * phase 1 writes + flags the peers, phase 2 waits (0 = both); phase 3 writes
+ * every sequence's (deterministic) prompt into this rank's replica only --
+ * the same resulting state without NVLink traffic, for long-context benches. */
+exf_status exf_model_context_setup_phase(exf_model* model, int32_t phase, exf_stream_t stream);
 /* Replicated context rows of this rank's replica (synchronous, diagnostics /
  * tests): K and V of (layer, seq) at positions [pos0, pos0+count), each
  * [count][H][Dh] bf16 bits; lengths [S] int32 of a layer. */

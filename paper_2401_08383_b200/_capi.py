@@ -100,6 +100,7 @@ SIGNATURES = {
     "exf_model_step_phase": (C.c_int, [_VP, _I32, _I32, _VP, _VP]),
     "exf_model_output": (C.c_int, [_VP, _VP]),
     "exf_model_context_setup": (C.c_int, [_VP, _VP]),
+    "exf_model_context_setup_phase": (C.c_int, [_VP, _I32, _VP]),
     "exf_model_read_kv": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _VP, _VP]),
     "exf_model_read_kv_len": (C.c_int, [_VP, _I32, _VP]),
     "exf_model_read_attn": (C.c_int, [_VP, _I32, _VP, _VP, _VP, _VP]),

@@ -244,7 +244,9 @@ __global__ void __launch_bounds__(256) context_setup_kernel(ContextSetupArgs a) 
     // grid (pos blocks, home sequences, layers)
     const int j = blockIdx.z;
     const int home_i = blockIdx.y;
-    const int s = a.rank + a.G * home_i;  // home sequence (round robin, sim.cpp:111)
+    // AllGather: home sequence (round robin, sim.cpp:111) into every replica;
+    // local: every sequence into this rank's replica only (same contents)
+    const int s = a.local ? home_i : a.rank + a.G * home_i;
     const int row_elems = a.H * a.Dh;     // per position, all heads
     const int64_t per_head = (int64_t)a.Cctx * a.Dh;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)a.prefix * row_elems;
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(256) context_setup_kernel(ContextSetupArgs a) 
         };
         const __nv_bfloat16 kv = __float2bfloat16(draw(hk)), vv = __float2bfloat16(draw(hv));
         const int64_t off = (((int64_t)j * a.S + s) * a.H + h) * per_head + (int64_t)pos * a.Dh + c;
-        for (int r = 0; r < a.G; ++r) {
+        for (int r = a.local ? a.rank : 0; r < (a.local ? a.rank + 1 : a.G); ++r) {
             __nv_bfloat16* base_k = reinterpret_cast<__nv_bfloat16*>(a.peers[r] + a.kv_k);
             __nv_bfloat16* base_v = reinterpret_cast<__nv_bfloat16*>(a.peers[r] + a.kv_v);
             base_k[off] = kv;
@@ -270,20 +272,21 @@ __global__ void __launch_bounds__(256) context_setup_kernel(ContextSetupArgs a) 
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0)
-        for (int r = 0; r < a.G; ++r)
+        for (int r = a.local ? a.rank : 0; r < (a.local ? a.rank + 1 : a.G); ++r)
             reinterpret_cast<int32_t*>(a.peers[r] + a.kv_len)[(int64_t)j * a.S + s] = a.prefix;
 }
 
-// every rank: rows + lengths visible system-wide, flag every peer, wait for all
+// every rank: rows + lengths visible system-wide, flag every peer (publish),
+// wait for all peers' flags (wait)
 __global__ void context_setup_sync_kernel(uint8_t* const* peers, int64_t flag_off, int G, int rank,
-                                          uint64_t epoch, int32_t* err) {
+                                          uint64_t epoch, int32_t* err, int publish, int wait) {
     __threadfence_system();
-    if ((int)threadIdx.x < G) {
+    if (publish && (int)threadIdx.x < G) {
         uint64_t* f = reinterpret_cast<uint64_t*>(peers[threadIdx.x] + flag_off) + rank;
         ptx::st_release_sys(f, epoch);
     }
     __syncthreads();
-    if ((int)threadIdx.x < G) {
+    if (wait && (int)threadIdx.x < G) {
         const uint64_t* f = reinterpret_cast<const uint64_t*>(peers[rank] + flag_off) + threadIdx.x;
         ptx::SpinGuard g;
         while (ptx::ld_acquire_sys(f) < epoch) g.step(err, ERR_TIMEOUT_GATHER);
@@ -333,15 +336,17 @@ exf_status launch_dense_gemm(const CUtensorMap& w, const CUtensorMap& x, const D
 }
 
 exf_status launch_context_setup(const ContextSetupArgs& a, int64_t flag_off, uint64_t epoch, int32_t* err,
-                                cudaStream_t s) {
-    const int B = a.S / a.G;  // home sequences of this rank
-    if (a.prefix > 0 && B > 0) {
+                                int phase, cudaStream_t s) {
+    const int B = a.local ? a.S : a.S / a.G;  // sequences this rank writes
+    if (phase != 2 && B > 0) {
         const int64_t elems = (int64_t)a.prefix * a.H * a.Dh;
         const int bx = (int)std::min<int64_t>(64, (elems + 255) / 256);
-        context_setup_kernel<<<dim3(bx, B, a.L), 256, 0, s>>>(a);
+        context_setup_kernel<<<dim3(std::max(bx, 1), B, a.L), 256, 0, s>>>(a);
         EXF_LAUNCH_CHECK("context_setup_kernel");
     }
-    context_setup_sync_kernel<<<1, 32, 0, s>>>(a.peers, flag_off, a.G, a.rank, epoch, err);
+    if (a.local) return EXF_OK;  // nothing crossed GPUs: no flags
+    context_setup_sync_kernel<<<1, 32, 0, s>>>(a.peers, flag_off, a.G, a.rank, epoch, err, phase != 2,
+                                               phase != 1);
     EXF_LAUNCH_CHECK("context_setup_sync_kernel");
     return EXF_OK;
 }

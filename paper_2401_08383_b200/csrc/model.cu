@@ -38,7 +38,7 @@ exf_status launch_dense_gemm(const CUtensorMap& w, const CUtensorMap& x, const D
                              cudaStream_t s);
 int dense_gemm_ksplit(int M, int K);
 exf_status launch_context_setup(const ContextSetupArgs& a, int64_t flag_off, uint64_t epoch, int32_t* err,
-                                cudaStream_t s);
+                                int phase, cudaStream_t s);
 exf_status launch_kv_append_model(const void* k_new, const void* v_new, int64_t new_stride_vec,
                                   const int32_t* seq, int32_t seq_stride, const int32_t* n_dev,
                                   int64_t n_max, int32_t H, int32_t Dh, int32_t C, int32_t replicas,
@@ -1018,7 +1018,13 @@ exf_status exf_model_set_placement(exf_model* m, const int32_t* h_assign) {
 }
 
 exf_status exf_model_context_setup(exf_model* m, exf_stream_t stream) {
+    return exf_model_context_setup_phase(m, 0, stream);
+}
+
+exf_status exf_model_context_setup_phase(exf_model* m, int32_t phase, exf_stream_t stream) {
     if (!m) return invalid("null model");
+    if (phase < 0 || phase > 3)
+        return invalid("context setup phase must be 0 (both), 1 (publish), 2 (wait) or 3 (local synthesis)");
     if (m->nh <= 0) return invalid("attention block disabled (attn_heads = 0)");
     if (!m->connected) return invalid("model is not connected to its peers (exf_model_connect)");
     const auto& c = m->cfg;
@@ -1036,8 +1042,10 @@ exf_status exf_model_context_setup(exf_model* m, exf_stream_t stream) {
     a.kv_k = m->sym.kv_k;
     a.kv_v = m->sym.kv_v;
     a.kv_len = m->sym.kv_len;
-    ++m->setup_epoch;
-    return launch_context_setup(a, m->sym.sflags, m->setup_epoch, m->err, static_cast<cudaStream_t>(stream));
+    a.local = phase == 3 ? 1 : 0;
+    if (phase == 0 || phase == 1) ++m->setup_epoch;
+    return launch_context_setup(a, m->sym.sflags, m->setup_epoch, m->err, phase,
+                                static_cast<cudaStream_t>(stream));
 }
 
 exf_status exf_model_read_kv(exf_model* m, int32_t layer, int32_t seq, int32_t pos0, int32_t count,

@@ -116,6 +116,7 @@ struct DenseArgs {
 // Arguments of the setup AllGather of the replicated context (attn_block.cu).
 struct ContextSetupArgs {
     int32_t G, rank, L, S, H, Dh, Cctx, prefix;
+    int32_t local;  // 1: every sequence into this rank's replica only (no exchange)
     uint64_t seed;
     uint8_t* const* peers;  // device array [G] of symmetric-region bases
     int64_t kv_k, kv_v, kv_len;

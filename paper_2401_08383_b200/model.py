@@ -222,9 +222,10 @@ class MoeModel:
         self.assign = a
 
     # ------------------------------------------------------------ attention block
-    def context_setup(self, stream=None) -> None:
-        """Setup AllGather of the replicated context (every rank must call it)."""
-        _capi.call("exf_model_context_setup", self._h, _stream_ptr(stream))
+    def context_setup(self, stream=None, phase: int = 0) -> None:
+        """Setup AllGather of the replicated context (every rank must call it);
+        phase 1/2 = publish/wait halves for lock-step ranks in one stream."""
+        _capi.call("exf_model_context_setup_phase", self._h, phase, _stream_ptr(stream))
 
     def kv_rows(self, layer: int, seq: int, pos0: int, count: int):
         """(K, V) rows of this rank's replica: [count][H][Dh] bf16 bits each."""

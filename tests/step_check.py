@@ -36,8 +36,8 @@ REL_TOL_F32 = 1e-5   # fp32 mode
 def check_step(model, x_dev, assign, rows_per_layer=2, seed=0, group=None):
     import torch
     import torch.distributed as dist
-    from paper_2401_08383_b200.model import (PHASE_BEGIN, PHASE_COMBINE_SEND, PHASE_COMBINE_WAIT,
-                                             PHASE_DISPATCH, PHASE_FFN, PHASE_FUSED,
+    from paper_2401_08383_b200.model import (PHASE_ATTN, PHASE_BEGIN, PHASE_COMBINE_SEND,
+                                             PHASE_COMBINE_WAIT, PHASE_DISPATCH, PHASE_FFN, PHASE_FUSED,
                                              PHASE_GATHER_SEND, PHASE_GATHER_WAIT)
     cfg = model.config
     G, rank, L, E = cfg.world_size, cfg.rank, cfg.num_layers, cfg.num_experts
@@ -67,6 +67,49 @@ def check_step(model, x_dev, assign, rows_per_layer=2, seed=0, group=None):
 
     def as_f64(row):
         return row.astype(np.float64) if f32 else co.orc.bf16_bits_to_f32(row).astype(np.float64)
+
+    attn = getattr(cfg, "attn_heads", 0) > 0
+    attn_worst = 0.0
+
+    def check_attention(j, before_mine, mid_mine):
+        """Post-attention rows of sampled resident tokens vs the fp64 oracle on
+        the local replica; the appended K/V row identical on every rank."""
+        nonlocal attn_worst
+        from oracle import attention as oatt
+        d, H = cfg.d_model, cfg.attn_heads
+        Dh = d // H
+        xb, meta = before_mine
+        xm, _ = mid_mine
+        lens = model.kv_len(j)
+        wqkv, bqkv, wo, bo = (co.orc.bf16_bits_to_f32(w).astype(np.float64) for w in model.attn_weights(j))
+        pick = rng.choice(len(meta), min(rows_per_layer, len(meta)), replace=False) if len(meta) else []
+        rows = []
+        for i in pick:
+            s_ = int(meta[i, 0])
+            pos = int(lens[s_]) - 1
+            k_all, v_all = model.kv_rows(j, s_, 0, pos + 1)
+            xq = co.orc.bf16_bits_to_f32(xb[i]).astype(np.float64)
+            qkv = xq @ wqkv.T + bqkv
+            qkv = co.orc.bf16_bits_to_f32(co.orc.f32_to_bf16_bits(qkv.astype(np.float32))).astype(np.float64)
+            kf = co.orc.bf16_bits_to_f32(k_all).astype(np.float64)
+            vf = co.orc.bf16_bits_to_f32(v_all).astype(np.float64)
+            ek = np.linalg.norm(kf[pos].ravel() - qkv[d:2 * d]) / max(np.linalg.norm(qkv[d:2 * d]), 1e-30)
+            att = oatt.coherent_attention(qkv[:d].reshape(1, H, Dh), np.array([0]), np.array([pos + 1]),
+                                          kf.transpose(1, 0, 2)[None], vf.transpose(1, 0, 2)[None], Dh ** -0.5)
+            att = co.orc.bf16_bits_to_f32(co.orc.f32_to_bf16_bits(att.reshape(-1).astype(np.float32)))
+            want = xq + att.astype(np.float64) @ wo.T + bo
+            got = co.orc.bf16_bits_to_f32(xm[i]).astype(np.float64)
+            err = float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30))
+            attn_worst = max(attn_worst, err, float(ek))
+            if err > REL_TOL or ek > REL_TOL:
+                fails.append(f"layer {j} token {s_}: attention rel err {err:.3e}, appended k rel err {ek:.3e}")
+            rows.append((s_, pos, k_all[pos].copy(), v_all[pos].copy()))
+        # the appended rows must be identical in every rank's replica
+        for r_rows in allgather(rows):
+            for s_, pos, kr, vr in r_rows:
+                k2, v2 = model.kv_rows(j, s_, pos, 1)
+                if not (np.array_equal(k2[0], kr) and np.array_equal(v2[0], vr)):
+                    fails.append(f"layer {j} seq {s_}: replicas differ at position {pos}")
     rng = np.random.default_rng(seed + rank)
     fails = []
     worst = 0.0
@@ -78,6 +121,15 @@ def check_step(model, x_dev, assign, rows_per_layer=2, seed=0, group=None):
     model.phase(PHASE_BEGIN, 0, x_dev)
     for j in range(L):
         torch.cuda.synchronize()
+        if attn:  # the attention block first, checked on its own
+            pre = model.resident(j % 2)
+            if dist_on:
+                dist.barrier(group=group)
+            model.phase(PHASE_ATTN, j)
+            torch.cuda.synchronize()
+            if dist_on:
+                dist.barrier(group=group)  # every rank's appends landed
+            check_attention(j, pre, model.resident(j % 2))
         before = allgather(model.resident(j % 2))
         if dist_on:
             dist.barrier(group=group)
@@ -178,4 +230,5 @@ def check_step(model, x_dev, assign, rows_per_layer=2, seed=0, group=None):
             "routed_fraction_checked_step": float(crossed.sum()) / (cfg.capacity * L),
             "simulate_p_star": rep.p_star if not vanilla else None,
             "max_rel_err_sampled": worst_all,
+            "attention_max_rel_err_sampled": max(allgather(attn_worst)) if attn else None,
             "failures": flat[:8]}

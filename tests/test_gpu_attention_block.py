@@ -51,7 +51,9 @@ def run_attention_checked(torch, models, assign, steps=2, seed=0):
     Dh = d // H
     fused = G == 1 and models[0].describe().get("path") == "fused"
     for m in models:
-        m.context_setup()
+        m.context_setup(phase=1)
+    for m in models:
+        m.context_setup(phase=2)
     torch.cuda.synchronize()
     P = cfg.context_prefix
     # setup AllGather: every replica identical, lengths = prompt
