@@ -9,16 +9,18 @@
 // expert) with ~2 x tokens flops per weight -- far below the fp32 FMA ridge.
 //
 // One launch per GEMM (MODE 0: H = gelu(X W1^T + b1); MODE 1:
-// out = x + prob * (H W2^T + b2)), grid (M / RB, E_loc):
-//   * a CTA owns RB output features (weight rows) of one local expert; S
-//     threads share a row, each streaming K/S consecutive weights with 32 B
-//     loads (4 in flight per thread), L1-bypassing;
+// out = x + prob * (H W2^T + b2)), grid (M / kRowsPerCta, E_loc):
+//   * each warp owns whole weight rows (output features); its 32 lanes read
+//     one row as consecutive 16-byte vectors (512 B per warp instruction,
+//     fully coalesced, L1-bypassing), a 1024-float chunk in flight at a time
+//     with the next chunk prefetched;
 //   * the expert's tokens are staged per tile of <= 16 in shared memory
 //     (canonical (slot, source, order) rows of the receive region for GEMM1,
-//     H rows for GEMM2) and read as broadcasts;
-//   * each thread accumulates its k-range in order with fmaf; the S partials
-//     of a row are summed in k order through shared memory: deterministic,
-//     fp32 accumulation (the fp64 oracle sits within ~1e-6 relative).
+//     H rows for GEMM2); lane l reads token columns k = 4l + 128c (conflict-
+//     free vectors);
+//   * per token, each lane accumulates its columns in order with fmaf, then a
+//     fixed xor butterfly sums the 32 lanes: deterministic fp32 accumulation
+//     (the fp64 oracle sits within ~1e-6 relative).
 // Tokens of expert e come from the dispatch exactly as on the bf16 two-kernel
 // path: per-(source, slot) counts in recv_cnt, rows of source s for slot e at
 // [seg_start, +cnt) of s's receive region, flags per source (GEMM1 waits).
@@ -48,13 +50,15 @@ __device__ __forceinline__ float gelu_exact(float v) { return 0.5f * v * (1.0f +
 
 }  // namespace
 
-template <int MODE, int S>
-__global__ void __launch_bounds__(kF32Threads) ffn_f32_kernel(FfnF32Args a) {
-    constexpr int RB = kF32Threads / S;  // weight rows per CTA
+constexpr int kRowsPerWarp = 8;
+constexpr int kRowsPerCta = kRowsPerWarp * (kF32Threads / 32);  // 64
+
+template <int MODE>
+__global__ void __launch_bounds__(kF32Threads, 1) ffn_f32_kernel(FfnF32Args a) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int32_t s_prefix[9], s_start[8];
     __shared__ int32_t s_ne, s_off;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int e = blockIdx.y;
     const int M = MODE == 0 ? a.dff : a.d;
     const int K = MODE == 0 ? a.d : a.dff;
@@ -101,16 +105,11 @@ __global__ void __launch_bounds__(kF32Threads) ffn_f32_kernel(FfnF32Args a) {
         return ((int64_t)parity * a.G + s) * a.C + s_start[s] + (i - s_prefix[s]);
     };
     const int tile = min(kF32TokTile, (int)(kF32SmemBudget / ((size_t)K * 4)));
-    float* sx = reinterpret_cast<float*>(smem);                           // [tile][K]
-    float* red = reinterpret_cast<float*>(smem + (size_t)tile * K * 4);  // [RB][S][tile]
-    const int row_l = tid / S, ks = tid - row_l * S;
-    const int r = blockIdx.x * RB + row_l;  // weight row == output feature
-    const int kn = K / S, k0 = ks * kn;
-    const float* wr = a.w + ((int64_t)e * M + r) * K + k0;
-    const float bias = a.bias[(int64_t)e * M + r];
+    float* sx = reinterpret_cast<float*>(smem);  // [tile][K]
+    const int nv = K / 128;                      // float4 per lane per row
+    const int kchunks = (nv + 7) / 8;            // 32 lanes x 8 float4 per chunk
     for (int t0 = 0; t0 < n_e; t0 += tile) {
         const int nt = min(tile, n_e - t0);
-        // ---- stage the tile's token rows (float4 copies)
         const int vec = K / 4;
         for (int i = tid; i < nt * vec; i += kF32Threads) {
             const int t = i / vec, v = i - t * vec;
@@ -119,21 +118,33 @@ __global__ void __launch_bounds__(kF32Threads) ffn_f32_kernel(FfnF32Args a) {
             reinterpret_cast<float4*>(sx)[i] = reinterpret_cast<const float4*>(src)[v];
         }
         __syncthreads();
+        // the warp's (row, chunk) items as one stream: the next item's weights
+        // are always in flight while the current one is applied
+        const int items = kRowsPerWarp * kchunks;
+        auto row_of = [&](int it) { return blockIdx.x * kRowsPerCta + (it / kchunks) * (kF32Threads / 32) + warp; };
+        auto load_item = [&](int it, float4 (&w)[8]) {
+            const int c = it % kchunks;
+            const float* wr = a.w + ((int64_t)e * M + row_of(it)) * K + c * 1024 + lane * 4;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                w[u] = c * 8 + u < nv ? ld_stream4(wr + u * 128) : make_float4(0.f, 0.f, 0.f, 0.f);
+        };
         float acc[kF32TokTile];
 #pragma unroll
         for (int t = 0; t < kF32TokTile; ++t) acc[t] = 0.f;
-        // ---- stream this thread's k-range of its weight row, 32 floats per
-        // round in flight, each 8-float group applied to every token in order
-        for (int k = 0; k < kn; k += 32) {
-            float4 w[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) w[u] = ld_stream4(wr + k + 4 * u);
+        float4 w[8];
+        load_item(0, w);
+        for (int it = 0; it < items; ++it) {
+            const int c = it % kchunks;
+            float4 wn[8];
+            if (it + 1 < items) load_item(it + 1, wn);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
+                const int k = c * 1024 + u * 128 + lane * 4;
 #pragma unroll
                 for (int t = 0; t < kF32TokTile; ++t) {
-                    if (t < nt) {
-                        const float4 x = *reinterpret_cast<const float4*>(sx + (int64_t)t * K + k0 + k + 4 * u);
+                    if (t < nt && c * 8 + u < nv) {
+                        const float4 x = *reinterpret_cast<const float4*>(sx + (int64_t)t * K + k);
                         acc[t] = fmaf(w[u].x, x.x, acc[t]);
                         acc[t] = fmaf(w[u].y, x.y, acc[t]);
                         acc[t] = fmaf(w[u].z, x.z, acc[t]);
@@ -141,29 +152,36 @@ __global__ void __launch_bounds__(kF32Threads) ffn_f32_kernel(FfnF32Args a) {
                     }
                 }
             }
-        }
-        // ---- the S partials of each row, summed in k order
-        if (S > 1) {
+            if (c == kchunks - 1) {  // the row is complete: reduce, write, restart
+                const int r = row_of(it);
+                // fixed xor butterfly over the 32 lanes (deterministic)
 #pragma unroll
-            for (int t = 0; t < kF32TokTile; ++t)
-                if (t < nt) red[((int64_t)row_l * S + ks) * tile + t] = acc[t];
-            __syncthreads();
-        }
-        if (ks == 0) {
-            for (int t = 0; t < nt; ++t) {
-                float v = acc[t];
-                if (S > 1) {
-                    v = red[((int64_t)row_l * S) * tile + t];
-                    for (int j = 1; j < S; ++j) v += red[((int64_t)row_l * S + j) * tile + t];
+                for (int t = 0; t < kF32TokTile; ++t) {
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
                 }
-                const int i = t0 + t;  // canonical index within the expert
-                if (MODE == 0) {
-                    a.H[(int64_t)(off_e + i) * a.dff + r] = gelu_exact(v + bias);
-                } else {
-                    const int64_t rr = recv_row(i);
-                    const float p = rmeta[rr].prob;
-                    a.res_x_out[(int64_t)(off_e + i) * a.d + r] = rx[rr * a.d + r] + p * (v + bias);
+                const float bias = a.bias[(int64_t)e * M + r];
+                // lane t writes token t (static register indexing via a select chain)
+                float mine = acc[0];
+#pragma unroll
+                for (int t = 1; t < kF32TokTile; ++t)
+                    if (lane == t) mine = acc[t];
+                if (lane < nt) {
+                    const int i = t0 + lane;  // canonical index within the expert
+                    if (MODE == 0) {
+                        a.H[(int64_t)(off_e + i) * a.dff + r] = gelu_exact(mine + bias);
+                    } else {
+                        const int64_t rrow = recv_row(i);
+                        const float p = rmeta[rrow].prob;
+                        a.res_x_out[(int64_t)(off_e + i) * a.d + r] = rx[rrow * a.d + r] + p * (mine + bias);
+                    }
                 }
+#pragma unroll
+                for (int t = 0; t < kF32TokTile; ++t) acc[t] = 0.f;
+            }
+            if (it + 1 < items) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) w[u] = wn[u];
             }
         }
         if (MODE == 1 && blockIdx.x == 0)
@@ -179,25 +197,22 @@ exf_status launch_ffn_f32(const FfnF32Args& a, int mode, cudaStream_t s) {
     const int M = mode == 0 ? a.dff : a.d;
     const int K = mode == 0 ? a.d : a.dff;
     if (a.G > 8) return invalid("fp32 FFN supports up to 8 ranks");
-    // GEMM1 (K = d): 2 threads per row; GEMM2 (K = d_ffn): 8 per row
-    const int S = mode == 0 ? 2 : 8;
-    const int RB = kF32Threads / S;
-    if (M % RB != 0 || K % (32 * S) != 0)
-        return invalid("fp32 FFN needs d_model, d_ffn multiples of 256 and of 32 x threads per row");
+    if (M % kRowsPerCta != 0 || K % 128 != 0)
+        return invalid("fp32 FFN needs d_model, d_ffn multiples of 128 (and of 64 output rows)");
     const int tile = std::min<int>(kF32TokTile, (int)(kF32SmemBudget / ((size_t)K * 4)));
     if (tile < 1) return invalid("fp32 FFN: a token row does not fit in shared memory");
-    const size_t smem = (size_t)tile * K * 4 + (size_t)RB * S * tile * 4;
-    auto k0 = ffn_f32_kernel<0, 2>;
-    auto k1 = ffn_f32_kernel<1, 8>;
+    const size_t smem = (size_t)tile * K * 4;
+    auto k0 = ffn_f32_kernel<0>;
+    auto k1 = ffn_f32_kernel<1>;
     static bool attr = false;
     if (!attr) {
-        EXF_CUDA_TRY(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024));
-        EXF_CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024));
+        EXF_CUDA_TRY(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32SmemBudget));
+        EXF_CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32SmemBudget));
         max_carveout(k0);
         max_carveout(k1);
         attr = true;
     }
-    const dim3 grid(M / RB, a.E_loc);
+    const dim3 grid(M / kRowsPerCta, a.E_loc);
     if (mode == 0) EXF_CUDA_TRY(launch_pdl(k0, grid, dim3(kF32Threads), smem, s, 0, a));
     else EXF_CUDA_TRY(launch_pdl(k1, grid, dim3(kF32Threads), smem, s, 0, a));
     return EXF_OK;

@@ -156,6 +156,7 @@ template <int NMAX, int STAGES, int BST, bool DENSE, bool DIAG, int NBUF = (NMAX
 __global__ void __launch_bounds__(kThreads, 1)
 layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
                    const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
+                   const __grid_constant__ CUtensorMap tmB2s, const __grid_constant__ CUtensorMap tmB2m,
                    const FusedArgs a) {
     using S = Smem<NMAX, STAGES, BST>;
     extern __shared__ uint8_t smem_raw[];
@@ -739,9 +740,18 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         asm volatile("fence.proxy.async.global;" ::: "memory");
                         waited_e = e;
                     }
-                    const CUtensorMap* tb = g == 0 ? &tmB1 : &tmB2;
                     const int row0 = g == 0 ? 0 : tab[e * S::kTabInts + 1];
+                    const int n_g = g == 0 ? 0 : cnt(1, e);
                     for (int c = 0; c < nch; ++c) {
+                        // GEMM2 B tiles: only as many H rows as the MMA reads
+                        // (ncol = tokens rounded up to 16), in boxes of 16 /
+                        // 32 / NMAX rows -- at ~8 tokens per expert a 64-row
+                        // box moved 4x the needed bytes, a third of the SM's
+                        // TMA ingest next to the weight stream
+                        const int nc_g = max(0, min(NMAX, n_g - c * NMAX));
+                        const int box = (g == 0 || !a.hbox) ? NMAX : (nc_g <= 16 ? 16 : (nc_g <= 32 ? 32 : NMAX));
+                        const CUtensorMap* tb = g == 0 ? &tmB1 : (box == 16 ? &tmB2s : (box == 32 ? &tmB2m : &tmB2));
+                        const uint32_t bbytes = (uint32_t)box * 128u * kKPS;
                         if (it == 0) ptx::pdl_wait();  // first read of the previous layer's output
                         for (int kb = 0; kb < kbp; kb += kKPS, ++it) {
                             const int sb = it % BST;
@@ -750,7 +760,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                             ptx::mbar_wait(&emptyB[sb], ((it / BST) & 1) ^ 1, a.err, 108);
                             if (ts && p == 1 && c == 0 && kb == 0) ts[13] = ptx::globaltimer();
                             if (ts5 && it < 16) ts5[it] = ptx::globaltimer();
-                            ptx::mbar_arrive_expect_tx(&fullB[sb], S::kB);
+                            ptx::mbar_arrive_expect_tx(&fullB[sb], bbytes);
 #pragma unroll
                             for (int h = 0; h < kKPS; ++h)
                                 ptx::tma_load_2d(smem + S::kOffB + sb * S::kB + h * S::kB1, tb, &fullB[sb],
@@ -1322,7 +1332,7 @@ struct FusedLauncher {
     exf_status launch(const CUtensorMap* maps, const FusedArgs& a, cudaStream_t s) {
         EXF_TRY(prepare());
         EXF_CUDA_TRY(launch_pdl(kern, dim3(ctas), dim3(kThreads), Sm::kBytes, s, 0, maps[0], maps[1],
-                                maps[2], maps[3], a));
+                                maps[2], maps[3], maps[4], maps[5], a));
         return EXF_OK;
     }
 };

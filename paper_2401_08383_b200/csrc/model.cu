@@ -152,6 +152,8 @@ struct exf_model {
     std::vector<CUtensorMap> tmap1, tmap2;  // per layer (weights, TMA tiles)
     CUtensorMap gmap_recv{}, gmap_h{};      // token rows for TMA gather4
     CUtensorMap tmap_x[2]{}, tmap_ht{};     // dense fused mode: resident rows / H as B tiles
+    CUtensorMap tmap_ht16{}, tmap_ht32{};   // dense: H as 16 / 32-row B tiles (few tokens per expert)
+    int hbox = 1;
     // symmetric region
     Symm sym{};
     uint8_t* sym_base = nullptr;
@@ -509,6 +511,7 @@ FusedArgs fused_args(exf_model* m, int j) {
     a.b2 = m->b2 + (int64_t)j * m->E_loc * c.d_model;
     a.dense = m->dense ? 1 : 0;
     a.xpre = m->xpre;
+    a.hbox = m->hbox;
     a.res_x_out = m->res_x[(j + 1) & 1];
     a.res_meta_out = m->res_meta[(j + 1) & 1];
     a.n_res_out = m->n_res + ((j + 1) & 1);
@@ -582,8 +585,9 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
             if (!m->fused)
                 return invalid("the fused layer kernel is not available for this configuration "
                                "(describe()[\"path\"] is the two-kernel path)");
-            const CUtensorMap maps[4] = {m->tmap1[j], m->tmap2[j], m->dense ? m->tmap_x[j & 1] : m->gmap_recv,
-                                         m->dense ? m->tmap_ht : m->gmap_h};
+            const CUtensorMap maps[6] = {m->tmap1[j], m->tmap2[j], m->dense ? m->tmap_x[j & 1] : m->gmap_recv,
+                                         m->dense ? m->tmap_ht : m->gmap_h, m->dense ? m->tmap_ht16 : m->gmap_h,
+                                         m->dense ? m->tmap_ht32 : m->gmap_h};
             return launch_layer_fused(maps, fused_args(m, j), m->f_nmax, s);
         }
         case 0:
@@ -741,6 +745,7 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         m->dense = m->fused && c.world_size == 1 && m->f_tpc == 1 && layer_weight_bytes <= 0.8e9;
         if (const char* env = std::getenv("EXF_DENSE")) m->dense = m->dense && std::atoi(env) != 0;
         if (const char* env = std::getenv("EXF_XPRE")) m->xpre = std::atoi(env);
+        if (const char* env = std::getenv("EXF_HBOX")) m->hbox = std::atoi(env);
         const int tok = m->dense ? C : m->nmax;
         const int nmax_f = tok <= 32 ? 32 : (tok <= 64 ? 64 : 128);
         m->f_nmax = nmax_f;
@@ -798,6 +803,8 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
     if (m->dense) {
         for (int i = 0; i < 2; ++i) EXF_M(make_tile_tmap(&m->tmap_x[i], m->res_x[i], C, d, m->f_nmax));
         EXF_M(make_tile_tmap(&m->tmap_ht, m->H, C, f, m->f_nmax));
+        EXF_M(make_tile_tmap(&m->tmap_ht16, m->H, C, f, std::min(16, m->f_nmax)));
+        EXF_M(make_tile_tmap(&m->tmap_ht32, m->H, C, f, std::min(32, m->f_nmax)));
     }
     if (cudaMemset(m->trace, 0xff, sizeof(int32_t) * C * L) != cudaSuccess) return fail(EXF_CUDA);
     EXF_M(init_weights(m));

@@ -189,6 +189,7 @@ struct FusedArgs {
     // epilogue keeps routed rows only, GEMM2 runs on the compact H
     int32_t dense;
     int32_t xpre;  // dense: pieces whose weights are L2-prefetched before the PDL wait
+    int32_t hbox;  // dense: GEMM2 H tiles in 16/32-row boxes when the expert has few tokens
     unsigned long long* tl;
     uint64_t* tstamp;    // optional per-CTA stamps [grid][16] (diagnostics)
 };
