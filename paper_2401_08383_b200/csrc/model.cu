@@ -744,6 +744,10 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         const double layer_weight_bytes = (double)m->E_loc * 4.0 * d * f;
         m->dense = m->fused && c.world_size == 1 && m->f_tpc == 1 && layer_weight_bytes <= 0.8e9;
         if (const char* env = std::getenv("EXF_DENSE")) m->dense = m->dense && std::atoi(env) != 0;
+        // dense: L2-prefetch the rest of each CTA's first piece before the PDL
+        // wait (measured 27.5-27.7 vs 28.2 us/layer at configs[1]; prefetching
+        // 2 or 4 pieces was slower: 28.6-28.8 / 31.8)
+        m->xpre = m->dense ? 1 : 0;
         if (const char* env = std::getenv("EXF_XPRE")) m->xpre = std::atoi(env);
         if (const char* env = std::getenv("EXF_HBOX")) m->hbox = std::atoi(env);
         const int tok = m->dense ? C : m->nmax;

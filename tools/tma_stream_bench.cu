@@ -53,6 +53,80 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
     __syncthreads();
 }
 
+// The same weight stream plus the dense-mode token operand: per weight box, a
+// 64-row x 64-col box of a small L2-resident token matrix (B) through its own
+// ring, like the fused kernel's GEMM1 (does B traffic slow the weight stream?)
+template <int S, int SB>
+__global__ void __launch_bounds__(96, 1) stream_ab_kernel(const __grid_constant__ CUtensorMap tm,
+                                                          const __grid_constant__ CUtensorMap tx, int rows_per_cta,
+                                                          int kblocks, int with_b, int* err) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int a_bytes = 128 * 128, b_bytes = 64 * 128;
+    uint8_t* sb = smem + S * a_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sb + SB * b_bytes);
+    uint64_t* empty = full + S;
+    uint64_t* fullb = empty + S;
+    uint64_t* emptyb = fullb + SB;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < SB; ++s) {
+            ptx::mbar_init(&fullb[s], 1);
+            ptx::mbar_init(&emptyb[s], 1);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    const int row0 = blockIdx.x * rows_per_cta;
+    const int tiles = (rows_per_cta / 128) * kblocks;
+    const uint64_t pol = ptx::policy_evict_first(), polx = ptx::policy_evict_last();
+    if (threadIdx.x == 0) {
+        for (int it = 0; it < tiles; ++it) {
+            const int st = it % S;
+            ptx::mbar_wait(&empty[st], ((it / S) & 1) ^ 1, err, 1);
+            const int rt = it / kblocks, kb = it % kblocks;
+            ptx::mbar_arrive_expect_tx(&full[st], a_bytes);
+            ptx::tma_load_2d(smem + st * a_bytes, &tm, &full[st], kb * 64, row0 + rt * 128, pol);
+        }
+    } else if (threadIdx.x == 64 && with_b) {
+        for (int it = 0; it < tiles; ++it) {
+            const int st = it % SB;
+            ptx::mbar_wait(&emptyb[st], ((it / SB) & 1) ^ 1, err, 1);
+            ptx::mbar_arrive_expect_tx(&fullb[st], b_bytes);
+            ptx::tma_load_2d(sb + st * b_bytes, &tx, &fullb[st], (it % kblocks) * 64, 0, polx);
+        }
+    } else if (threadIdx.x == 32) {
+        for (int it = 0; it < tiles; ++it) {
+            const int st = it % S, stb = it % SB;
+            ptx::mbar_wait(&full[st], (it / S) & 1, err, 1);
+            if (with_b) ptx::mbar_wait(&fullb[stb], (it / SB) & 1, err, 1);
+            ptx::mbar_arrive(&empty[st]);
+            if (with_b) ptx::mbar_arrive(&emptyb[stb]);
+        }
+    }
+    __syncthreads();
+}
+
+template <int S, int SB>
+float run_ab(CUtensorMap* tm, CUtensorMap* tx, int ctas, int rows_per_cta, int kblocks, int with_b, int* err) {
+    const int smem = S * 128 * 128 + SB * 64 * 128 + 2 * (S + SB) * 8 + 1024;
+    cudaFuncSetAttribute(stream_ab_kernel<S, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    stream_ab_kernel<S, SB><<<ctas, 96, smem>>>(*tm, *tx, rows_per_cta, kblocks, with_b, err);
+    cudaEventRecord(a);
+    for (int r = 0; r < 5; ++r) stream_ab_kernel<S, SB><<<ctas, 96, smem>>>(*tm, *tx, rows_per_cta, kblocks, with_b, err);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms / 5;
+}
+
 template <int S>
 float run(CUtensorMap* tm, int ctas, int rows_per_cta, int box_rows, int kblocks, int* err) {
     const int smem = S * box_rows * 128 + 2 * S * 8 + 1024;
@@ -118,6 +192,30 @@ int main() {
                 report(5, run<5>(&tm, ctas, rows_per_cta, box_rows, kblocks, err));
                 report(6, run<6>(&tm, ctas, rows_per_cta, box_rows, kblocks, err));
             }
+        }
+    }
+    {  // weight stream with / without the token operand (dense GEMM1 pattern)
+        CUtensorMap tm, tx;
+        cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+        cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+        cuuint32_t box[2] = {64, 128};
+        cuuint32_t es[2] = {1, 1};
+        encode(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        void* xb = nullptr;
+        cudaMalloc(&xb, 64 * K * 2);
+        cudaMemset(xb, 2, 64 * K * 2);
+        cuuint64_t xdims[2] = {(cuuint64_t)K, 64};
+        cuuint32_t xbox[2] = {64, 64};
+        encode(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xb, xdims, strides, xbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        const int rows_per_cta = (int)(rows / sms) / 128 * 128;
+        const double bytes = (double)sms * rows_per_cta * K * 2;
+        for (int wb = 0; wb < 2; ++wb) {
+            const float m8 = run_ab<8, 10>(&tm, &tx, sms, rows_per_cta, kblocks, wb, err);
+            const float m10 = run_ab<10, 10>(&tm, &tx, sms, rows_per_cta, kblocks, wb, err);
+            printf("A 8 x 16 KB + B 10 x 8 KB, token operand %s: %7.1f GB/s of weights; A 10 stages: %7.1f GB/s\n",
+                   wb ? "ON " : "off", bytes / (m8 * 1e-3) / 1e9, bytes / (m10 * 1e-3) / 1e9);
         }
     }
     cudaDeviceSynchronize();
