@@ -56,8 +56,9 @@ int32_t exf_device_ok(void);
  * proj/src/trace.cpp:191-215): counts[j][a][b] = #{t : paths[t][j] == a and
  * paths[t][j+gap] == b}, row_totals[j][a] = sum_b counts[j][a][b].
  * Bit-exact (integer). Validation errors match trace.cpp:53-70 / :193-196.
- * d_workspace: exf_count_transitions_workspace_bytes(...) bytes (currently 0:
- * per-CTA privatised counters flush with exact 64-bit atomics; may be NULL).
+ * d_workspace: exf_count_transitions_workspace_bytes(...) bytes: 0 (may be
+ * NULL) when the per-CTA counters flush with exact 64-bit atomics, else the
+ * per-CTA u16 partials summed by a second kernel (large E).
  * ---------------------------------------------------------------------- */
 int64_t exf_count_transitions_workspace_bytes(int64_t T, int32_t L, int32_t E, int32_t gap);
 exf_status exf_count_transitions(const int32_t* d_paths, int64_t T, int32_t L, int32_t E,

@@ -70,8 +70,17 @@ HistPlan plan_hist(int64_t T, int32_t L, int32_t E, int32_t gap) {
     p.tile_tokens = (int32_t)std::min<int64_t>(kTileTokens, (int64_t)kHistThreads * kPrefetchVec * 4 / L);
     p.tile_tokens = std::max(1, p.tile_tokens & ~3);
     const int64_t tile_bytes = (int64_t)p.tile_tokens * L * 4;
-    p.pair_group = (int32_t)std::max<int64_t>(
-        1, std::min<int64_t>(p.pairs, (kCounterSmemBudget + 32 * 1024 - tile_bytes) / ((int64_t)p.pair_words * 4)));
+    // pair groups sized for two CTAs per SM (the counting is latency-bound on
+    // shared-memory atomics; one 188 KB CTA per SM at E = 64 left 3/4 of the
+    // warp slots empty), balanced across groups; every group re-reads its
+    // token range (L2 hits: the groups of a range run side by side)
+    const int64_t per_cta = 110 * 1024 - tile_bytes - 64;
+    const int64_t all_bytes = (int64_t)p.pairs * p.pair_words * 4;
+    int64_t groups = std::max<int64_t>(1, (all_bytes + per_cta - 1) / per_cta);
+    groups = std::min<int64_t>(groups, p.pairs);
+    p.pair_group = (int32_t)((p.pairs + groups - 1) / groups);
+    if ((int64_t)p.pair_group * p.pair_words * 4 + tile_bytes > kCounterSmemBudget + 32 * 1024)
+        p.pair_group = (int32_t)std::max<int64_t>(1, (kCounterSmemBudget + 32 * 1024 - tile_bytes) / ((int64_t)p.pair_words * 4));
     p.groups = (p.pairs + p.pair_group - 1) / p.pair_group;
     // token ranges: about two CTAs per SM over all groups, <= 65535 tokens each
     const int64_t min_splits = (T + kMaxTokensPerCta - 1) / kMaxTokensPerCta;
@@ -80,7 +89,10 @@ HistPlan plan_hist(int64_t T, int32_t L, int32_t E, int32_t gap) {
     splits = std::min<int64_t>(splits, std::max<int64_t>(1, (T + 63) / 64));
     p.splits = std::max<int64_t>(std::max(splits, min_splits), 1);
     p.smem_bytes = (size_t)p.pair_group * p.pair_words * 4 + (size_t)tile_bytes + 16;
-    p.workspace_bytes = 0;  // the flush is atomic into the result: no split partials
+    // few bins x CTAs: exact 64-bit atomic flush, no workspace; many (E >= 32):
+    // u16 partials in a workspace summed by hist_sum_kernel
+    const int64_t total_bins = (int64_t)p.pairs * E * E;
+    p.workspace_bytes = total_bins * p.splits > (4LL << 20) ? total_bins * p.splits * 2 : 0;
     return p;
 }
 
@@ -88,7 +100,8 @@ HistPlan plan_hist(int64_t T, int32_t L, int32_t E, int32_t gap) {
 __global__ void __launch_bounds__(kHistThreads)
 hist_kernel(const int32_t* __restrict__ paths, int64_t T, int32_t L, int32_t E, int32_t gap,
             int32_t pairs, int32_t pair_group, int32_t pair_words, int32_t tile_tokens, int64_t splits,
-            unsigned long long* __restrict__ counts, unsigned long long* __restrict__ row_totals) {
+            unsigned long long* __restrict__ counts, unsigned long long* __restrict__ row_totals,
+            uint16_t* __restrict__ partials) {
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);
     const int32_t group = blockIdx.x;
@@ -156,8 +169,20 @@ hist_kernel(const int32_t* __restrict__ paths, int64_t T, int32_t L, int32_t E, 
         }
     }
     __syncthreads();
-    // flush: non-zero bins into the exact 64-bit result; row totals per (pair, a)
     const uint16_t* c16 = reinterpret_cast<const uint16_t*>(cnt);
+    if (partials) {
+        // many bins x many CTAs (E >= 32): the CTA's u16 partials go to a
+        // workspace [split][pair][E][E] with coalesced stores; hist_sum_kernel
+        // adds them up (one 64-bit atomic per bin and CTA would be ~10^7
+        // global atomics at E = 64)
+        uint16_t* dst = partials + split * (int64_t)pairs * EE + (int64_t)j0 * EE;
+        for (int32_t i = tid; i < pg * EE; i += kHistThreads) {
+            const int32_t q = i / EE, bin = i - q * EE;
+            dst[i] = c16[(int64_t)q * pair_words * 2 + bin];
+        }
+        return;
+    }
+    // flush: non-zero bins into the exact 64-bit result; row totals per (pair, a)
     for (int32_t i = tid; i < pg * EE; i += kHistThreads) {
         const int32_t q = i / EE, bin = i - q * EE;
         const uint32_t c = c16[(int64_t)q * pair_words * 2 + bin];
@@ -171,6 +196,39 @@ hist_kernel(const int32_t* __restrict__ paths, int64_t T, int32_t L, int32_t E, 
             for (int32_t b = 0; b < E; ++b) sum += row[b];
             if (sum) atomicAdd(&row_totals[(int64_t)(j0 + q) * E + a], (unsigned long long)sum);
         }
+}
+
+// Sum of the per-CTA u16 partials, bin by bin: a block covers 64 consecutive
+// bins x 8 split groups (coalesced loads), integer sums (order-free, exact).
+__global__ void __launch_bounds__(512) hist_sum_kernel(const uint16_t* __restrict__ partials, int64_t splits,
+                                                       int64_t total_bins, unsigned long long* __restrict__ counts) {
+    __shared__ unsigned long long s_acc[8][64];
+    const int lane_bin = threadIdx.x & 63, grp = threadIdx.x >> 6;
+    const int64_t bin = (int64_t)blockIdx.x * 64 + lane_bin;
+    unsigned long long acc = 0;
+    if (bin < total_bins) {
+#pragma unroll 8
+        for (int64_t sp = grp; sp < splits; sp += 8) acc += partials[sp * total_bins + bin];
+    }
+    s_acc[grp][lane_bin] = acc;
+    __syncthreads();
+    if (grp == 0 && bin < total_bins) {
+        unsigned long long t = 0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) t += s_acc[g][lane_bin];
+        counts[bin] = t;
+    }
+}
+
+// Row totals from the final counts (proj/src/trace.cpp:210-213): one warp per row.
+__global__ void hist_rows_kernel(const unsigned long long* __restrict__ counts, int64_t rows, int32_t E,
+                                 unsigned long long* __restrict__ row_totals) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    unsigned long long s = 0;
+    for (int32_t b = threadIdx.x & 31; b < E; b += 32) s += counts[row * E + b];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) row_totals[row] = s;
 }
 
 exf_status check_hist_args(int64_t T, int32_t L, int32_t E, int32_t gap) {
@@ -204,7 +262,7 @@ extern "C" exf_status exf_count_transitions(const int32_t* d_paths, int64_t T, i
                                             exf_stream_t stream) {
     EXF_TRY(check_hist_args(T, L, E, gap));
     if (!d_paths || !d_counts) return invalid("null device pointer");
-    (void)d_workspace;  // no split partials in v2 (workspace_bytes == 0; may be NULL)
+    // (d_workspace: NULL allowed when exf_count_transitions_workspace_bytes == 0)
     const HistPlan p = plan_hist(T, L, E, gap);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     static size_t attr_bytes = 0;
@@ -214,12 +272,30 @@ extern "C" exf_status exf_count_transitions(const int32_t* d_paths, int64_t T, i
         attr_bytes = std::max<size_t>(p.smem_bytes, 48 * 1024);
     }
     const int64_t pairs_bins = (int64_t)p.pairs * E * E;
+    auto* counts = reinterpret_cast<unsigned long long*>(d_counts);
+    auto* totals = reinterpret_cast<unsigned long long*>(d_row_totals);
+    dim3 grid(p.groups, (unsigned)p.splits);
+    if (p.workspace_bytes > 0) {
+        if (!d_workspace) return invalid("workspace required (exf_count_transitions_workspace_bytes)");
+        auto* ws = static_cast<uint16_t*>(d_workspace);
+        hist_kernel<<<grid, kHistThreads, p.smem_bytes, s>>>(d_paths, T, L, E, gap, p.pairs, p.pair_group,
+                                                             p.pair_words, p.tile_tokens, p.splits, counts,
+                                                             totals, ws);
+        EXF_LAUNCH_CHECK("hist_kernel");
+        hist_sum_kernel<<<(unsigned)((pairs_bins + 63) / 64), 512, 0, s>>>(ws, p.splits, pairs_bins, counts);
+        EXF_LAUNCH_CHECK("hist_sum_kernel");
+        if (d_row_totals) {
+            const int64_t rows = (int64_t)p.pairs * E;
+            hist_rows_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(counts, rows, E, totals);
+            EXF_LAUNCH_CHECK("hist_rows_kernel");
+        }
+        return EXF_OK;
+    }
     EXF_CUDA_TRY(cudaMemsetAsync(d_counts, 0, (size_t)pairs_bins * 8, s));
     if (d_row_totals) EXF_CUDA_TRY(cudaMemsetAsync(d_row_totals, 0, (size_t)p.pairs * E * 8, s));
-    dim3 grid(p.groups, (unsigned)p.splits);
-    hist_kernel<<<grid, kHistThreads, p.smem_bytes, s>>>(
-        d_paths, T, L, E, gap, p.pairs, p.pair_group, p.pair_words, p.tile_tokens, p.splits,
-        reinterpret_cast<unsigned long long*>(d_counts), reinterpret_cast<unsigned long long*>(d_row_totals));
+    hist_kernel<<<grid, kHistThreads, p.smem_bytes, s>>>(d_paths, T, L, E, gap, p.pairs, p.pair_group,
+                                                         p.pair_words, p.tile_tokens, p.splits, counts, totals,
+                                                         nullptr);
     EXF_LAUNCH_CHECK("hist_kernel");
     return EXF_OK;
 }

@@ -24,11 +24,20 @@ namespace {
 constexpr int kReplayThreads = 256;
 constexpr int kReplayPrefetch = 8;  // int4 per thread per tile (tile <= 256 tokens x 32 layers)
 
+// MODE 1 (coherent) / 0 (vanilla). Per token and layer only the comparisons
+// that cannot be derived are counted (entries packed as gpu | node << 16; the
+// current GPU is tracked in both modes, sim.cpp:112/:143):
+//   same  = #(expert GPU == current GPU)       -> gpu_local, and moves = L - same
+//   snode = #(expert node == current node)     -> node_local
+//   away  = #(expert GPU != home)              -> away_from_home
+//   anode = #(expert node != home node)        (vanilla)
+// coherent: hops_inter = #(node changes) = L - snode, hops_intra = snode - same;
+// vanilla: hops_inter = 2 anode, hops_intra = 2 (away - anode) (sim.cpp:60-71)
+template <int MODE>
 __global__ void __launch_bounds__(kReplayThreads)
 route_replay_kernel(const int32_t* __restrict__ paths, const int32_t* __restrict__ homes,
                     const int32_t* __restrict__ assign, int64_t T, int32_t L, int32_t E,
-                    int32_t gpus_per_node, int32_t gpus, int32_t mode,
-                    unsigned long long* __restrict__ out) {
+                    int32_t gpus_per_node, int32_t gpus, unsigned long long* __restrict__ out) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int32_t stride = L | 1;
     int32_t* s_tab = reinterpret_cast<int32_t*>(smem);  // [L][E] gpu | node << 16
@@ -55,7 +64,7 @@ route_replay_kernel(const int32_t* __restrict__ paths, const int32_t* __restrict
             if (i < nvec) pre[u] = ld_nc_v4(s4 + i);
         }
     };
-    int64_t gl = 0, nl = 0, away = 0, moves = 0, hi = 0, he = 0;
+    int64_t c_same = 0, c_snode = 0, c_away = 0, c_anode = 0, c_tok = 0;
     if (vec && blockIdx.x < tiles) fetch(blockIdx.x);
     for (int64_t tile_id = blockIdx.x; tile_id < tiles; tile_id += gridDim.x) {
         const int64_t t0 = tile_id * kReplayThreads;
@@ -87,31 +96,42 @@ route_replay_kernel(const int32_t* __restrict__ paths, const int32_t* __restrict
         if (tid < nt) {
             const int64_t t = t0 + tid;
             const int32_t home = homes ? __ldg(homes + t) : (int32_t)(t % gpus);
-            const int32_t home_node = home / gpus_per_node;
-            int32_t loc = home, loc_node = home_node;
+            const int32_t home_ent = home | ((home / gpus_per_node) << 16);
+            int32_t loc_ent = home_ent;
+            int32_t same = 0, snode = 0, away = 0, anode = 0;  // per tile: <= L each
             const int32_t* p = tile + tid * stride;
-            for (int32_t j = 0; j < L; ++j) {
+            const int32_t* tab = s_tab;
+            for (int32_t j = 0; j < L; ++j, tab += E) {
                 const int32_t e = p[j];
-                const int32_t ent = ((unsigned)e < (unsigned)E) ? s_tab[j * E + e] : (loc | (loc_node << 16));
-                const int32_t eg = ent & 0xFFFF, en = ent >> 16;
-                gl += (eg == loc);
-                nl += (en == loc_node);
-                away += (eg != home);
-                if (eg != loc) {
-                    ++moves;
-                    if (mode == 1) {
-                        if (en != loc_node) ++he; else ++hi;
-                    }
-                }
-                if (mode == 0 && eg != home) {
-                    if (en != home_node) he += 2; else hi += 2;
-                }
-                loc = eg;
-                loc_node = en;
+                const int32_t ent = ((unsigned)e < (unsigned)E) ? tab[e] : loc_ent;
+                // the current GPU is tracked in both modes (sim.cpp:112, :143)
+                same += (ent == loc_ent);
+                snode += ((ent ^ loc_ent) >> 16) == 0;
+                if (MODE == 0) anode += ((ent ^ home_ent) >> 16) != 0;
+                loc_ent = ent;
+                away += ((ent ^ home_ent) & 0xFFFF) != 0;
             }
+            c_same += same;
+            c_snode += snode;
+            c_away += away;
+            c_anode += anode;
+            ++c_tok;
         }
     }
-    int64_t v[6] = {gl, nl, away, moves, hi, he};
+    // gpu_local, node_local, away, coherent moves, hops intra, hops inter
+    const int64_t tl = c_tok * L;
+    int64_t v[6];
+    v[0] = c_same;
+    v[1] = c_snode;
+    v[2] = c_away;
+    v[3] = tl - c_same;
+    if (MODE == 1) {
+        v[4] = c_snode - c_same;
+        v[5] = tl - c_snode;
+    } else {
+        v[4] = 2 * (c_away - c_anode);
+        v[5] = 2 * c_anode;
+    }
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
         const int64_t sm = warp_sum(v[k]);
@@ -140,17 +160,17 @@ extern "C" exf_status exf_route_replay(const int32_t* d_paths, const int32_t* d_
     if (!d_paths || !d_assign || !d_out) return invalid("null device pointer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t smem = (size_t)((L * E + 3) & ~3) * 4 + (size_t)kReplayThreads * (L | 1) * 4;
-    EXF_CUDA_TRY(cudaFuncSetAttribute(route_replay_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kern = mode == 1 ? route_replay_kernel<1> : route_replay_kernel<0>;
+    EXF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     EXF_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(exf_sim_counters), s));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t tiles = (T + kReplayThreads - 1) / kReplayThreads;
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 3LL * sms));
-    route_replay_kernel<<<blocks, kReplayThreads, smem, s>>>(
-        d_paths, d_homes, d_assign, T, L, E, gpus_per_node, num_nodes * gpus_per_node, mode,
-        reinterpret_cast<unsigned long long*>(d_out));
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 4LL * sms));
+    kern<<<blocks, kReplayThreads, smem, s>>>(d_paths, d_homes, d_assign, T, L, E, gpus_per_node,
+                                              num_nodes * gpus_per_node,
+                                              reinterpret_cast<unsigned long long*>(d_out));
     EXF_LAUNCH_CHECK("route_replay_kernel");
     return EXF_OK;
 }
