@@ -79,6 +79,28 @@ def _wire(t):
     return t.view(torch.bfloat16) if t.dtype == torch.int16 else t
 
 
+def warm_up(group=None) -> None:
+    """Open the NCCL peer-to-peer connections between every pair of ranks
+    (one tiny send/recv per pair): NCCL sets them up lazily on first use,
+    which would otherwise land inside the first timed migration."""
+    import torch
+    import torch.distributed as dist
+    G, rank = dist.get_world_size(group), dist.get_rank(group)
+    dist.barrier(group=group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    send = [torch.zeros(1, device=dev) for _ in range(G)]
+    recv = [torch.empty(1, device=dev) for _ in range(G)]
+    ops = []
+    for p in range(G):
+        if p != rank:
+            ops.append(dist.P2POp(dist.isend, send[p], p, group=group))
+            ops.append(dist.P2POp(dist.irecv, recv[p], p, group=group))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    torch.cuda.synchronize()
+
+
 def migrate_nccl(model, new_assign: np.ndarray, group=None) -> int:
     """One process per GPU (every rank calls it with the same table): the old
     owner sends each moved expert's weights over NCCL, the new owner receives
