@@ -1054,6 +1054,13 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 const int64_t slot = slot_of_tile(g, e, mt, c);
                 const int Smax = a.max_contrib;
                 bool from_ws = false;  // finished values come from the k-ordered partial sum
+                // cooperative finish (host-marked: every contributor of the tile
+                // is its CTA's last piece, so nobody's later work waits): all S
+                // contributors wait for each other and each finishes a 1/S
+                // slice of the columns -- the lone last-arriver finisher was the
+                // layer's tail at N >= 2 (7.6 us, ~2 us per L2 round trip)
+                const bool coop = (pc.pad & 1) != 0 && Sg > 1;
+                int cs = 0, ce = nc;  // columns this CTA finishes
                 if (Sg > 1) {
                     // park the partial; the last-arriving piece of this tile
                     // reduces all partials in k order (deterministic)
@@ -1073,9 +1080,16 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         // release this piece's partials; only the last arriver
                         // acquires (one load on the counter)
                         const int prev = atom_add_release(a.item_ctr + slot, 1);
-                        if (prev == Sg - 1) (void)ld_acq_s32(a.item_ctr + slot);
-                        s_flag = (prev == Sg - 1);
-                        if (s_flag) a.item_ctr[slot] = 0;  // next use is a later launch
+                        if (coop) {
+                            ptx::SpinGuard sg;
+                            while (ptx::ld_relaxed_s32(a.item_ctr + slot) < Sg) sg.step(a.err, 114);
+                            (void)ld_acq_s32(a.item_ctr + slot);
+                            s_flag = 1;
+                        } else {
+                            if (prev == Sg - 1) (void)ld_acq_s32(a.item_ctr + slot);
+                            s_flag = (prev == Sg - 1);
+                            if (s_flag) a.item_ctr[slot] = 0;  // next use is a later launch
+                        }
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     if (!DENSE && ts4 && et == 0 && job < 4) ts4[9 + 2 * job] = ptx::globaltimer();
@@ -1084,7 +1098,23 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         continue;
                     }
                     from_ws = true;
+                    if (coop) {
+                        cs = (kp * nc) / Sg;
+                        ce = ((kp + 1) * nc) / Sg;
+                    }
                 }
+                // cooperative finish: the last contributor to complete its slice
+                // resets the counter (and, for GEMM1, signals the expert's tile)
+                auto coop_done = [&](bool gemm1) {
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (et == 0) {
+                        const int prev = atom_add_acq_rel(a.item_ctr + slot, 1);
+                        if (prev == 2 * Sg - 1) {
+                            a.item_ctr[slot] = 0;
+                            if (gemm1) red_add_release(a.hdone + parity * a.E_loc + e, 1);
+                        }
+                    }
+                };
                 // Final values 4 tokens at a time in a ROLLED loop. ncu showed the
                 // epilogue stalled on instruction fetch (stall_no_inst): a
                 // 16-token unrolled body (~15 KB of SASS) does not fit a
@@ -1141,7 +1171,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                         for (int k = 0; k < 4; ++k)
 #pragma unroll
                             for (int i = 0; i < 16; ++i)
-                                pk[k][i] = (k0 + k < Sg && c0 + i < nc)
+                                pk[k][i] = (k0 + k < Sg && c0 + i < ce)
                                                ? __ldcg(w0 + (int64_t)(k0 + k) * NMAX * kBM + (c0 + i) * kBM) : 0.f;
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
@@ -1188,7 +1218,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     // keeps the routed ones), values from TMEM or the partials
                     if (from_ws) {
 #pragma unroll 1
-                        for (int c0 = 0; c0 < nc; c0 += 16) {
+                        for (int c0 = cs; c0 < ce; c0 += 16) {
                             float sv[16];
                             fin16(c0, sv);
 #pragma unroll
@@ -1196,7 +1226,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                                 const int j = cb + c0 + i;
                                 const int slot_j = DENSE ? s_exp[j < a.C ? j : 0] : e;
                                 const int pos_j = DENSE ? s_pos[j < a.C ? j : 0] : off_e + j;
-                                if (c0 + i < nc && slot_j == e)
+                                if (c0 + i < ce && slot_j == e)
                                     a.H[(int64_t)pos_j * a.dff + m_glob] = __float2bfloat16(gelu_erf(sv[i] + bias));
                             }
                         }
@@ -1224,9 +1254,13 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     if (ts2 && et == 0 && job == 0) ts2[job] = (uint64_t)(clock64() - c_in);  // diagnostics
                     if (!from_ws) release_tmem();
                     if (DENSE && ts3 && et == 0 && job == 0) ts3[4] = ptx::globaltimer();
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (DENSE && ts3 && et == 0 && job == 0) ts3[5] = ptx::globaltimer();
-                    if (et == 0) red_add_release(a.hdone + parity * a.E_loc + e, 1);
+                    if (coop) {
+                        coop_done(true);
+                    } else {
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        if (DENSE && ts3 && et == 0 && job == 0) ts3[5] = ptx::globaltimer();
+                        if (et == 0) red_add_release(a.hdone + parity * a.E_loc + e, 1);
+                    }
                     if (DENSE && ts3 && et == 0 && job == 0) ts3[6] = ptx::globaltimer();
                 } else {
                     // per token: source row of the residual, gate prob, output row
@@ -1250,11 +1284,11 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     if (from_ws) {  // finisher: 16 columns per L2 round trip
                         if (!DENSE && ts4 && et == 0 && job == 0) ts4[12] = ptx::globaltimer();
 #pragma unroll 1
-                        for (int c0 = 0; c0 < nc; c0 += 16) {
+                        for (int c0 = cs; c0 < ce; c0 += 16) {
                             __nv_bfloat16 xin[16];  // residual loads in flight with the partials
 #pragma unroll
                             for (int i = 0; i < 16; ++i)
-                                if (c0 + i < nc) xin[i] = xres[s_rrow[c0 + i] * a.d + m_glob];
+                                if (c0 + i < ce) xin[i] = xres[s_rrow[c0 + i] * a.d + m_glob];
                             float sv[16];
                             fin16(c0, sv);
                             if (!DENSE && ts4 && et == 0 && job == 0 && c0 == 0) {
@@ -1265,7 +1299,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                             }
 #pragma unroll
                             for (int i = 0; i < 16; ++i)
-                                if (c0 + i < nc)
+                                if (c0 + i < ce)
                                     a.res_x_out[(int64_t)(off_e + cb + c0 + i) * a.d + m_glob] = __float2bfloat16(
                                         __bfloat162float(xin[i]) + s_rprob[c0 + i] * (sv[i] + bias));
                             if (!DENSE && ts4 && et == 0 && job == 0 && c0 == 0) ts4[13] = ptx::globaltimer();
@@ -1291,6 +1325,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                     if (!from_ws) release_tmem();
                     if (!DENSE && mt == 0 && et < nc)  // dense: the token's own CTA wrote it
                         a.res_meta_out[off_e + cb + et] = ResMeta{s_rtok[et], s_rexp[et]};
+                    if (coop) coop_done(false);
                 }
                 if (ts4 && et == 0 && job < (DENSE ? 8 : 4)) ts4[2 * job + 1] = ptx::globaltimer() | ((uint64_t)from_ws << 63);
             }
@@ -1369,7 +1404,7 @@ int fused_ctas() {
 // A CTA's GEMM2 pieces always follow its GEMM1 pieces (deadlock freedom of the
 // hdone waits). Returns false if a CTA would need more than kMaxPieces.
 bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece>& pieces,
-                          std::vector<int32_t>& off, int* max_contrib, int* max_pieces) {
+                          std::vector<int32_t>& off, int* max_contrib, int* max_pieces, bool coop_default) {
     const int k1 = d / kBK, k2 = dff / kBK, mt1 = dff / kBM, mt2 = d / kBM;
     // measured at configs[1]: (16, 16) 45.9 us/layer; (16, 8) 53.2, (16, 12) 49.8,
     // (16, 32) 50.9, (8, 8) 65.2: per-piece costs exceed the model's estimate
@@ -1487,6 +1522,28 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
         for (auto& v : per)
             for (auto& p : v)
                 if (p.g == 1) p.S = cnt[p.e * mt2 + p.mt];
+    }
+    // cooperative split-K finish where every contributor of a tile is the last
+    // piece of its CTA (nothing queued behind a contributor's wait). Dispatch
+    // path only: measured 38.1 -> 34.6 us/layer at N=4 (32.9-33.2 -> 32.1-32.9
+    // at N=2) but 27.9 -> 29.8 in dense mode, whose last-round tiles have
+    // contributors finish microseconds apart
+    bool coop_on = coop_default;
+    if (const char* s = std::getenv("EXF_COOP")) coop_on = std::atoi(s) != 0;
+    if (coop_on) {
+        std::vector<int> total_pieces, last_pieces;  // per (g, e, mt) tile
+        auto tile_id = [&](const Piece& p) { return ((int)p.g * E_loc + p.e) * std::max(mt1, mt2) + p.mt; };
+        const int ntiles = 2 * E_loc * std::max(mt1, mt2);
+        total_pieces.assign(ntiles, 0);
+        last_pieces.assign(ntiles, 0);
+        for (auto& v : per)
+            for (size_t i = 0; i < v.size(); ++i) {
+                total_pieces[tile_id(v[i])]++;
+                if (i + 1 == v.size()) last_pieces[tile_id(v[i])]++;
+            }
+        for (auto& v : per)
+            for (auto& p : v)
+                if (p.S > 1 && last_pieces[tile_id(p)] == total_pieces[tile_id(p)]) p.pad |= 1;
     }
     pieces.clear();
     off.assign(ctas + 1, 0);

@@ -60,7 +60,7 @@ exf_status make_tile_tmap(CUtensorMap* map, const void* base, int64_t rows, int6
 exf_status plan_ffn_gemm(int nmax, int mode, int items, int K, int* ksplit, int* clusters);
 exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int nmax, cudaStream_t s);
 bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece>& pieces,
-                          std::vector<int32_t>& off, int* max_contrib, int* max_pieces);
+                          std::vector<int32_t>& off, int* max_contrib, int* max_pieces, bool coop_default);
 int fused_ctas();
 
 namespace {
@@ -757,7 +757,7 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         std::vector<Piece> pieces;
         std::vector<int32_t> off;
         if (!build_fused_schedule(m->E_loc, d, f, m->f_ctas, pieces, off, &m->f_max_contrib,
-                                  &m->f_max_pieces))
+                                  &m->f_max_pieces, !m->dense))
             m->fused = m->dense = false;  // too many pieces per CTA: two-kernel path
         EXF_M(dalloc(&m->f_pieces, pieces.size()));
         EXF_M(dalloc(&m->f_piece_off, off.size()));
