@@ -598,6 +598,13 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         const int c = (cnt(g, e) + NMAX - 1) / NMAX;
         return (p == 0 && c == 0) ? 1 : c;
     };
+    // k-blocks a piece streams: an expert without tokens only drains the
+    // first piece's prefetched stages (at E_loc = 64 on one GPU with 8
+    // tokens, 56 experts are idle and every CTA's first piece streamed a
+    // whole idle tile: +38 MB per layer)
+    auto kbp_of = [&](int p, const Piece& pc) {
+        return (p == 0 && cnt(pc.g, pc.e) == 0) ? min((int)pc.nkb, npre * kKPS) : (int)pc.nkb;
+    };
     auto slot_of_tile = [&](int g, int e, int mt, int c) -> int64_t {
         const int64_t base = g == 0 ? 0 : (int64_t)a.E_loc * mt1 * a.max_chunks;
         const int mts = g == 0 ? mt1 : mt2;
@@ -611,7 +618,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             uint64_t hold_ns = 0, hold_n = 0;
             for (int p = 0; p < npc; ++p) {
                 const Piece pc = s_pc[p];
-                const int g = pc.g, e = pc.e, mt = pc.mt, kbp = pc.nkb;
+                const int g = pc.g, e = pc.e, mt = pc.mt, kbp = kbp_of(p, pc);
                 const int nch = nchunks(p, g, e);
                 const CUtensorMap* tm = g == 0 ? &tmA1 : &tmA2;
                 const int rows = g == 0 ? a.dff : a.d;
@@ -646,7 +653,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         if (ts2 && lane == 0) ts2[3] = ptx::globaltimer();  // diagnostics: MMA role entry
         for (int p = 0; p < npc; ++p) {
             const Piece pc = s_pc[p];
-            const int g = pc.g, e = pc.e, kbp = pc.nkb;
+            const int g = pc.g, e = pc.e, kbp = kbp_of(p, pc);
             const int n_e = cnt(g, e);
             const int nch = nchunks(p, g, e);
             for (int c = 0; c < nch; ++c, ++job) {
@@ -729,7 +736,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 ptx::tma_prefetch_desc(&tmB2);
                 for (int p = 0; p < npc; ++p) {
                     const Piece pc = s_pc[p];
-                    const int g = pc.g, e = pc.e, kbp = pc.nkb;
+                    const int g = pc.g, e = pc.e, kbp = kbp_of(p, pc);
                     const int nch = nchunks(p, g, e);
                     if (g == 1 && nch > 0 && waited_e != e) {
                         const int target = mt1 * ((cnt(0, e) + NMAX - 1) / NMAX);
@@ -772,7 +779,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         } else
         for (int p = 0; p < npc; ++p) {
             const Piece pc = s_pc[p];
-            const int g = pc.g, e = pc.e, kbp = pc.nkb;
+            const int g = pc.g, e = pc.e, kbp = kbp_of(p, pc);
             const int n_e = cnt(g, e);
             const int off_e = tab[e * S::kTabInts + 1];
             const int nch = nchunks(p, g, e);

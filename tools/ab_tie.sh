@@ -1,4 +1,6 @@
 cd /root/repo
-for f in 1 0 1 0; do EXF_COOP=$f timeout 120 python tools/step_time.py; done
-for n in 2 4; do for f in 1 0 1; do EXF_COOP=$f timeout 200 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2956$n tools/step_time.py 2>&1 | grep "step "; done; done
-timeout 900 python -m pytest -q -x tests/test_gpu_model.py tests/test_multi_gpu_shapes.py tests/test_multi_gpu.py 2>&1 | tail -2
+for v in new old new old; do
+  if [ $v = old ]; then cp gpurun_tmp/libexflow_b200.so paper_2401_08383_b200/libexflow_b200.so.old; cp paper_2401_08383_b200/libexflow_b200.so gpurun_tmp/new.so; cp gpurun_tmp/libexflow_b200.so paper_2401_08383_b200/libexflow_b200.so; fi
+  echo "== $v"; timeout 120 python tools/step_time.py --experts 64 --batch 8; timeout 120 python tools/step_time.py --experts 32 --d-model 2048 --d-ffn 8192 --batch 16
+  if [ $v = old ]; then cp gpurun_tmp/new.so paper_2401_08383_b200/libexflow_b200.so; fi
+done
