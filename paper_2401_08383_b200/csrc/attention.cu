@@ -21,6 +21,8 @@
 // the partial (m, l, acc) in split order (deterministic, no second launch).
 #include "common.cuh"
 
+#include <algorithm>
+
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
@@ -229,8 +231,11 @@ int attn_splits(int64_t N, int32_t H, int32_t Dh, int32_t C) {
 
 }  // namespace
 
-int64_t attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh, int32_t C) {
-    const int splits = attn_splits(N, H, Dh, C);
+// n_plan: the token count the split plan is made for (a decode rank holds
+// about tokens_per_gpu tokens, the grid covers the capacity N; planning for N
+// left 3/4 of the GPU idle at N = 4 GPUs)
+int64_t attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh, int32_t C, int64_t n_plan) {
+    const int splits = attn_splits(std::max<int64_t>(1, std::min(n_plan, N)), H, Dh, C);
     cudaGetLastError();
     if (splits <= 1) return 0;
     return (int64_t)ws_partials_off(N, H) * (int64_t)sizeof(float) +
@@ -240,10 +245,10 @@ int64_t attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh, int32_t C) {
 exf_status launch_attention_model(const void* q, const int32_t* seq, int32_t seq_stride,
                                   const int32_t* n_dev, int64_t n_max, const int32_t* ctx,
                                   const void* k, const void* v, int32_t H, int32_t Dh, int32_t C,
-                                  float scale, void* ws, void* out, cudaStream_t st) {
+                                  float scale, void* ws, void* out, int64_t n_plan, cudaStream_t st) {
     if (n_max <= 0) return EXF_OK;
     if (Dh != 64 && Dh != 128) return invalid("attention: head dim must be 64 or 128");
-    const int splits = attn_splits(n_max, H, Dh, C);
+    const int splits = attn_splits(std::max<int64_t>(1, std::min(n_plan, n_max)), H, Dh, C);
     if (splits > 1 && !ws) return invalid("attention: workspace required");
     const int chunk = ((C + splits - 1) / splits + 63) / 64 * 64;
     const float scale_log2 = scale * 1.4426950408889634f;

@@ -1380,11 +1380,17 @@ struct FusedLauncher {
 };
 
 template <int NMAX, int STAGES, int BST>
-exf_status launch_nmax(const CUtensorMap* maps, const FusedArgs& a, cudaStream_t s) {
+exf_status launch_nmax(const CUtensorMap* maps, const FusedArgs& a, cudaStream_t s, bool prepare_only = false) {
     static FusedLauncher<NMAX, STAGES, BST, true, false> dense;
     static FusedLauncher<NMAX, STAGES, BST, false, false> dispatch;
     static FusedLauncher<NMAX, STAGES, BST, true, true> dense_diag;
     static FusedLauncher<NMAX, STAGES, BST, false, true> dispatch_diag;
+    if (prepare_only) {
+        EXF_TRY(dense.prepare());
+        EXF_TRY(dispatch.prepare());
+        EXF_TRY(dense_diag.prepare());
+        return dispatch_diag.prepare();
+    }
     if (a.tstamp) return a.dense ? dense_diag.launch(maps, a, s) : dispatch_diag.launch(maps, a, s);
     return a.dense ? dense.launch(maps, a, s) : dispatch.launch(maps, a, s);
 }
@@ -1572,7 +1578,12 @@ namespace {
 int* g_dbg_host_words = nullptr;  // host view of this unit's g_dbg_host
 }
 
-exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int nmax, cudaStream_t s) {
+// Host-side setup outside any stream capture (model create): the
+// diagnostics channel's mapped page + symbol copy and the kernels'
+// attributes. A synchronous cudaMemcpyToSymbol inside exf_model_capture
+// invalidated the capture when the first fused launch of the process was the
+// captured one.
+exf_status prepare_layer_fused(int nmax) {
     if (!g_dbg_host_words) {  // diagnostics channel for timed-out spins (survives a trap)
         void* h = nullptr;
         void* dptr = nullptr;
@@ -1585,6 +1596,12 @@ exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int n
         }
         cudaGetLastError();
     }
+    if (nmax <= 32) return launch_nmax<32, 4, 10>(nullptr, FusedArgs{}, nullptr, true);
+    if (nmax <= 64) return launch_nmax<64, 4, 5>(nullptr, FusedArgs{}, nullptr, true);
+    return launch_nmax<128, 3, 3>(nullptr, FusedArgs{}, nullptr, true);
+}
+
+exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int nmax, cudaStream_t s) {
     if (a.E > kMaxKeys || a.E_loc > kMaxLocal) return invalid("at most 64 experts");
     if (a.d > 2048) return invalid("fused layer kernel supports d_model <= 2048");
     if (a.tpc > 32) return invalid("token slice too large for the fused layer kernel");

@@ -47,8 +47,8 @@ exf_status launch_kv_append_model(const void* k_new, const void* v_new, int64_t 
 exf_status launch_attention_model(const void* q, const int32_t* seq, int32_t seq_stride,
                                   const int32_t* n_dev, int64_t n_max, const int32_t* ctx,
                                   const void* k, const void* v, int32_t H, int32_t Dh, int32_t C,
-                                  float scale, void* ws, void* out, cudaStream_t st);
-int64_t attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh, int32_t C);
+                                  float scale, void* ws, void* out, int64_t n_plan, cudaStream_t st);
+int64_t attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh, int32_t C, int64_t n_plan);
 exf_status launch_gather_wait(uint8_t* own_sym, const Symm& sym, int G, uint64_t* step,
                               int32_t* err, cudaStream_t s);
 exf_status make_weight_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols);
@@ -59,6 +59,7 @@ exf_status make_gather_tmap(CUtensorMap* map, const void* base, int64_t rows, in
 exf_status make_tile_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
 exf_status plan_ffn_gemm(int nmax, int mode, int items, int K, int* ksplit, int* clusters);
 exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int nmax, cudaStream_t s);
+exf_status prepare_layer_fused(int nmax);
 bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece>& pieces,
                           std::vector<int32_t>& off, int* max_contrib, int* max_pieces, bool coop_default);
 int fused_ctas();
@@ -529,6 +530,17 @@ FusedArgs fused_args(exf_model* m, int j) {
     return a;
 }
 
+// diagnostics (EXF_CAPTURE_TRACE=1): report where a stream capture got invalidated
+void capture_trace(cudaStream_t s, const char* what, int j) {
+    static const bool on = std::getenv("EXF_CAPTURE_TRACE") != nullptr;
+    if (!on) return;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    const cudaError_t e = cudaStreamIsCapturing(s, &st);
+    const cudaError_t le = cudaPeekAtLastError();
+    std::fprintf(stderr, "[capture] %s j=%d status=%d (%s) last=%s\n", what, j, (int)st, cudaGetErrorString(e),
+                 cudaGetErrorString(le));
+}
+
 // q, k, v = x Wqkv^T + b -> K/V rows into every replica -> attention over the
 // local replica -> x += attn Wo^T + b (in place in the layer's input rows)
 exf_status run_attention(exf_model* m, int j, cudaStream_t s) {
@@ -547,6 +559,7 @@ exf_status run_attention(exf_model* m, int j, cudaStream_t s) {
     qa.out[2] = m->vb;
     qa.err = m->err;
     EXF_TRY(launch_dense_gemm(m->tm_qkv[j], m->tm_res[j & 1], qa, m->at_nt, 0, s));
+    capture_trace(s, "qkv", j);
     const int64_t layer_off = (int64_t)j * C * m->nh * m->Cctx * m->Dh * 2;
     void* kc[8];
     void* vc[8];
@@ -561,8 +574,10 @@ exf_status run_attention(exf_model* m, int j, cudaStream_t s) {
     const int32_t* seq = reinterpret_cast<const int32_t*>(m->res_meta[j & 1]);  // ResMeta.token
     EXF_TRY(launch_kv_append_model(m->kb, m->vb, (int64_t)d / 8, seq, 2, n_dev, C, m->nh, m->Dh, m->Cctx, G, kc,
                                    vc, lc, m->kv_overflow, s));
+    capture_trace(s, "kv_append", j);
     EXF_TRY(launch_attention_model(m->qb, seq, 2, n_dev, C, lc[0], kc[0], vc[0], m->nh, m->Dh, m->Cctx,
-                                   1.0f / std::sqrt((float)m->Dh), m->attn_ws, m->ab, s));
+                                   1.0f / std::sqrt((float)m->Dh), m->attn_ws, m->ab, c.tokens_per_gpu, s));
+    capture_trace(s, "attention", j);
     DenseArgs oa{};
     oa.M = d;
     oa.K = d;
@@ -637,8 +652,10 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
 
 exf_status run_step(exf_model* m, const void* x_in, cudaStream_t s) {
     EXF_TRY(run_phase(m, 0, 0, x_in, s));
+    capture_trace(s, "begin", 0);
     for (int j = 0; j < m->cfg.num_layers; ++j) {
         if (m->nh > 0) EXF_TRY(run_phase(m, 8, j, nullptr, s));
+        capture_trace(s, "attn block", j);
         if (m->fused) {
             EXF_TRY(run_phase(m, 5, j, nullptr, s));
         } else {
@@ -773,6 +790,7 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         EXF_M(dalloc(&m->hdone, (size_t)2 * m->E_loc));
         EXF_M(dalloc(&m->fbar, 2 * 260));  // 256 per-CTA barrier slots + epoch (u64)
         EXF_M(dalloc(&m->f_cta_cnt, (size_t)m->f_ctas * E));
+        if (m->fused) EXF_M(prepare_layer_fused(nmax_f));
     }
     if (std::getenv("EXF_FFN_TIMELINE")) {
         EXF_M(dalloc(&m->tstamp, (size_t)6 * kTimelineCtas * 16));
@@ -793,7 +811,7 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         m->at_nt = C <= 64 ? 64 : 128;
         m->ks_qkv = dense_gemm_ksplit(3 * d, d);
         m->ks_o = dense_gemm_ksplit(d, d);
-        const int64_t wsb = attention_workspace_bytes(C, m->nh, m->Dh, m->Cctx);
+        const int64_t wsb = attention_workspace_bytes(C, m->nh, m->Dh, m->Cctx, c.tokens_per_gpu);
         if (wsb > 0) EXF_M(cuda_status_ok(cudaMalloc(&m->attn_ws, (size_t)wsb), "attention workspace"));
         for (int i = 0; i < 2; ++i) EXF_M(make_tile_tmap(&m->tm_res[i], m->res_x[i], C, d, m->at_nt));
         EXF_M(make_tile_tmap(&m->tm_attn, m->ab, C, d, m->at_nt));
