@@ -246,15 +246,22 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = misc[0];
-    const int npre = npc > 0 ? min((int)s_pc[0].nkb / kKPS, STAGES) : 0;  // prefetched stages
-    // k-block offset of pipeline step kb within a piece of nkb k-blocks: each
-    // CTA starts at its own stage and wraps around, so the CTAs' concurrent
-    // token-row loads spread over the activation matrix (in dense mode every
-    // CTA's first GEMM1 piece reads the same rows: the first stage took ~4 us
-    // from 148-way same-line L2 traffic); the order is fixed per CTA
-    auto kbr = [&](int nkb, int kb) {
+    // prefetched stages (none with virtual expert slots: the first piece's
+    // expert is unknown until the counts are in)
+    const bool remap = !DENSE && a.remap;
+    const int npre = (npc > 0 && !remap) ? min((int)s_pc[0].nkb / kKPS, STAGES) : 0;
+    // k-block offset of pipeline step kb within a piece of nkb k-blocks: the
+    // pieces start at different stages and wrap around, so the CTAs'
+    // concurrent token-row loads spread over the activation matrix (in dense
+    // mode every CTA's first GEMM1 piece reads the same rows: the first stage
+    // took ~4 us from 148-way same-line L2 traffic). Dense mode rotates by
+    // CTA; the dispatch path by tile (expert + row tile), so a tile's
+    // accumulation order -- and its bits -- do not depend on which CTA the
+    // schedule (or the virtual expert binding) gives it to.
+    auto kbr = [&](const Piece& pc, int nkb, int kb) {
         const int nst = nkb / kKPS;
-        return ((kb / kKPS + (int)blockIdx.x) % nst) * kKPS;
+        const int rot = DENSE ? (int)blockIdx.x : (int)pc.e + (int)pc.mt;
+        return ((kb / kKPS + rot) % nst) * kKPS;
     };
     const uint64_t pol_a = ptx::policy_evict_first();
     // the layer's gate matrix is a weight too: bulk-copy it into the B-stage
@@ -267,7 +274,14 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // previous kernel: safe to read before the PDL wait
     if (tid < a.E) s_key[tid] = a.gpu_of[tid] * a.E_loc + a.slot_of[tid];
     // (never in dense mode: there the token-row ring is live from the start)
-    const bool wg_smem = !DENSE && wg_bytes <= (uint32_t)(BST * S::kB) && gate_cta;
+    // gate scratch [Wg | token rows | logits]: the idle token-row ring, or,
+    // with virtual expert slots (no weight prefetch), both rings (at E = 64,
+    // d = 1024 the 128 KB gate matrix did not fit the row ring: every dot
+    // product read it from L2/HBM, ~9 us for one token per CTA)
+    const uint32_t gate_off = remap ? (uint32_t)S::kOffA : (uint32_t)S::kOffB;
+    const uint32_t gate_cap = (uint32_t)(S::kOffB + BST * S::kB) - gate_off;
+    const bool wg_smem = !DENSE && gate_cta &&
+                         ((wg_bytes + 1023u) & ~1023u) + (uint32_t)((a.tpc * a.E * 4 + 1023) & ~1023) <= gate_cap;
     auto prefetch_a = [&]() {  // first weight stages of the CTA's first piece
         if (npc == 0) return;
         const Piece pc = s_pc[0];
@@ -277,7 +291,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             ptx::mbar_arrive_expect_tx(&full[s], S::kA);
             for (int j = 0; j < kKPS; ++j)
                 ptx::tma_load_2d(smem + S::kOffA + s * S::kA + j * S::kA1, tm, &full[s],
-                                 (pc.kb0 + kbr(pc.nkb, s * kKPS) + j) * kBK, pc.e * rows + pc.mt * kBM, pol_a);
+                                 (pc.kb0 + kbr(pc, pc.nkb, s * kKPS) + j) * kBK, pc.e * rows + pc.mt * kBM, pol_a);
         }
         // dense: the rest of the first pieces into L2 while the previous layer
         // drains (its tail leaves HBM bandwidth idle)
@@ -286,21 +300,21 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             const CUtensorMap* tq = q.g == 0 ? &tmA1 : &tmA2;
             const int rq = q.g == 0 ? a.dff : a.d;
             for (int kb = p == 0 ? npre * kKPS : 0; kb < q.nkb; ++kb)
-                ptx::tma_prefetch_l2_2d(tq, (q.kb0 + kbr(q.nkb, kb - kb % kKPS) + kb % kKPS) * kBK, q.e * rq + q.mt * kBM);
+                ptx::tma_prefetch_l2_2d(tq, (q.kb0 + kbr(q, q.nkb, kb - kb % kKPS) + kb % kKPS) * kBK, q.e * rq + q.mt * kBM);
         }
     };
     if (warp == 0 && lane == 0) {
         if (wg_smem) {
             ptx::mbar_arrive_expect_tx(wg_bar, wg_bytes);
             for (uint32_t o = 0; o < wg_bytes; o += 32768)
-                ptx::bulk_load(smem + S::kOffB + o, reinterpret_cast<const uint8_t*>(a.wg) + o,
+                ptx::bulk_load(smem + gate_off + o, reinterpret_cast<const uint8_t*>(a.wg) + o,
                                min(32768u, wg_bytes - o), wg_bar);
         }
         ptx::tma_prefetch_desc(&tmA1);
         ptx::tma_prefetch_desc(&tmA2);
         // before the PDL wait: issued mid-token-phase, the 160 KB bursts of the
         // token-owning CTAs delayed every flag poll behind them by ~4 us
-        if (DENSE || a.xpre >= 0) prefetch_a();
+        if (DENSE || (a.xpre >= 0 && !remap)) prefetch_a();
     }
 
     // ---------------- dependent part
@@ -312,7 +326,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     if (!DENSE) ptx::pdl_wait();
     // (diagnostics, EXF_XPRE=-1: weight prefetch only once the previous layer
     // is complete, so its tail does not compete with the prefetch traffic)
-    if (!DENSE && a.xpre < 0 && warp == 0 && lane == 0) prefetch_a();
+    if (!DENSE && a.xpre < 0 && !remap && warp == 0 && lane == 0) prefetch_a();
     ptx::pdl_trigger();
     mark3(1);
     if (tid == 0) tl_mark(a.tl, 1);
@@ -365,16 +379,16 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     }
     mark3(12);
     if (spec && lane == 0) s_meta_spec[warp] = mk;
-    // Gate scratch in the (still idle) B-ring region: [Wg | token rows | logits].
+    // Gate scratch in the (still idle) ring region: [Wg | token rows | logits].
     // A warp walking one token through every expert is a serial chain of
     // ~600 instructions (~1.5 us); instead each warp takes (token, expert)
     // items, every dot product still in the oracle's order (lane-sliced,
     // c-major/k-minor, xor butterfly), and one thread per token does softmax.
     const uint32_t wg_al = wg_smem ? (wg_bytes + 1023u) & ~1023u : 0u;
-    const uint32_t lg_off = (uint32_t)(BST * S::kB) - (uint32_t)((a.tpc * E * 4 + 1023) & ~1023);
-    float* s_logit = reinterpret_cast<float*>(smem + S::kOffB + lg_off);
+    const uint32_t lg_off = gate_cap - (uint32_t)((a.tpc * E * 4 + 1023) & ~1023);
+    float* s_logit = reinterpret_cast<float*>(smem + gate_off + lg_off);
     const bool x_smem = wg_al + (uint32_t)nt * a.d * 2 <= lg_off;
-    const uint32_t xs_base = ptx::smem_u32(smem + S::kOffB + wg_al);
+    const uint32_t xs_base = ptx::smem_u32(smem + gate_off + wg_al);
     if (x_smem) {  // stage the CTA's token rows (first rows still in registers)
         for (int i = warp; i < nt; i += kWarps) {
             const __nv_bfloat16* x = a.res_x_in + (int64_t)(t0 + i) * a.d;
@@ -382,72 +396,111 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             for (int c = 0; c < 8; ++c) {
                 if (c < chunks) {
                     const int4 v = i == warp ? xk[c] : *reinterpret_cast<const int4*>(x + c * 256 + lane * 8);
-                    *reinterpret_cast<int4*>(smem + S::kOffB + wg_al + ((uint32_t)i * a.d + c * 256 + lane * 8) * 2) = v;
+                    *reinterpret_cast<int4*>(smem + gate_off + wg_al + ((uint32_t)i * a.d + c * 256 + lane * 8) * 2) = v;
                 }
             }
         }
         __syncthreads();
     }
     mark3(14);
-    for (int w = warp; w < nt * E; w += kWarps) {
-        const int i = w / E, e = w - i * E;
-        float acc = 0.f;
-        if (x_smem && wg_smem) {
-            const uint32_t xa = xs_base + ((uint32_t)i * a.d) * 2 + lane * 16;
-            const uint32_t wa = ptx::smem_u32(smem + S::kOffB) + ((uint32_t)e * a.d) * 2 + lane * 16;
-            for (int c = 0; c < chunks; ++c) {
-                float xf[8], wf[8];
-                unpack8(lds128(xa + c * 512), xf);
-                unpack8(lds128(wa + c * 512), wf);
+    // kGI items per warp in flight: one item at a time was a latency chain
+    // (dependent smem loads, 32 FMAs, 5 shuffles) of ~0.45 us per item, ~4 us
+    // for one token over 64 experts; each item keeps its own FMA order
+    constexpr int kGI = 8;
+    for (int w0 = warp; w0 < nt * E; w0 += kWarps * kGI) {
+        float acc[kGI];
+        int xi[kGI], we[kGI];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) acc = fmaf(xf[k], wf[k], acc);
+        for (int u = 0; u < kGI; ++u) {
+            const int w = min(w0 + u * kWarps, nt * E - 1);  // past the end: recompute the last (discarded)
+            xi[u] = w / E;
+            we[u] = w - xi[u] * E;
+            acc[u] = 0.f;
+        }
+        if (x_smem && wg_smem) {
+            const uint32_t wbase = ptx::smem_u32(smem + gate_off) + lane * 16;
+            for (int c = 0; c < chunks; ++c) {
+#pragma unroll
+                for (int u = 0; u < kGI; ++u) {
+                    float xf[8], wf[8];
+                    unpack8(lds128(xs_base + ((uint32_t)xi[u] * a.d) * 2 + lane * 16 + c * 512), xf);
+                    unpack8(lds128(wbase + ((uint32_t)we[u] * a.d) * 2 + c * 512), wf);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) acc[u] = fmaf(xf[k], wf[k], acc[u]);
+                }
             }
         } else {
-            const __nv_bfloat16* x = a.res_x_in + (int64_t)(t0 + i) * a.d + lane * 8;
-            const __nv_bfloat16* wr = a.wg + (int64_t)e * a.d + lane * 8;
             for (int c = 0; c < chunks; ++c) {
-                float xf[8], wf[8];
-                unpack8(*reinterpret_cast<const int4*>(x + c * 256), xf);
-                unpack8(*reinterpret_cast<const int4*>(wr + c * 256), wf);
 #pragma unroll
-                for (int k = 0; k < 8; ++k) acc = fmaf(xf[k], wf[k], acc);
+                for (int u = 0; u < kGI; ++u) {
+                    float xf[8], wf[8];
+                    unpack8(*reinterpret_cast<const int4*>(a.res_x_in + (int64_t)(t0 + xi[u]) * a.d + lane * 8 + c * 256), xf);
+                    unpack8(*reinterpret_cast<const int4*>(a.wg + (int64_t)we[u] * a.d + lane * 8 + c * 256), wf);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) acc[u] = fmaf(xf[k], wf[k], acc[u]);
+                }
             }
         }
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if (lane == 0) s_logit[w] = acc;
+        for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+            for (int u = 0; u < kGI; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], off);
+        if (lane == 0)
+#pragma unroll
+            for (int u = 0; u < kGI; ++u)
+                if (w0 + u * kWarps < nt * E) s_logit[w0 + u * kWarps] = acc[u];
     }
     __syncthreads();
     mark3(13);
-    if (tid < nt) {  // softmax / top-1 per token, experts in index order
-        const int i = tid, t = t0 + i;
-        const float* lg = s_logit + i * E;
-        int best = 0;
-        float mx = lg[0];
-        for (int e = 1; e < E; ++e)
-            if (lg[e] > mx) {
-                mx = lg[e];
-                best = e;
+    // softmax / top-1, one warp per token: top-1 = the lowest index among the
+    // maxima (lane-strided scan + butterfly), the exp terms in parallel, their
+    // sum in expert-index order by lane 0 (the oracle's order; one thread
+    // doing all of it cost ~1.8 us at E = 64)
+    for (int i = warp; i < nt; i += kWarps) {
+        const int t = t0 + i;
+        float* lg = s_logit + i * E;
+        float mv = __int_as_float(0xff800000);  // -inf
+        int mi = 0x7fffffff;
+        for (int e = lane; e < E; e += 32)
+            if (lg[e] > mv || mi == 0x7fffffff) {
+                mv = lg[e];
+                mi = e;
             }
-        float s = 0.f;
-        for (int e = 0; e < E; ++e) s += expf(lg[e] - mx);
-        const ResMeta m = (i < kWarps && i < a.tpc) ? s_meta_spec[i] : a.res_meta_in[t];
-        int sel = best;
-        float p = 1.f / s;
-        if (a.forced) {
-            sel = a.forced_routes[(int64_t)m.token * a.L + a.layer];
-            if ((unsigned)sel >= (unsigned)E) {
-                atomicExch(a.err, ERR_BAD_EXPERT);
-                sel = best;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, mv, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, mi, off);
+            if (ov > mv || (ov == mv && oi < mi)) {
+                mv = ov;
+                mi = oi;
             }
-            p = expf(lg[sel] - mx) / s;
         }
-        s_exp[i] = sel;
-        s_prob[i] = p;
-        s_tok[i] = m.token;
-        if (a.hist && a.layer > 0 && m.prev_expert >= 0)
-            atomicAdd(&a.hist[((int64_t)(a.layer - 1) * E + m.prev_expert) * E + sel], 1ull);
-        if (a.trace) a.trace[(int64_t)m.token * a.L + a.layer] = sel;
+        const int best = mi;
+        const float mx = mv;
+        __syncwarp();
+        for (int e = lane; e < E; e += 32) lg[e] = expf(lg[e] - mx);  // in place: the exp terms
+        __syncwarp();
+        if (lane == 0) {
+            float s = 0.f;
+            for (int e = 0; e < E; ++e) s += lg[e];
+            const ResMeta m = (i < kWarps && i < a.tpc) ? s_meta_spec[i] : a.res_meta_in[t];
+            int sel = best;
+            float p = 1.f / s;
+            if (a.forced) {
+                sel = a.forced_routes[(int64_t)m.token * a.L + a.layer];
+                if ((unsigned)sel >= (unsigned)E) {
+                    atomicExch(a.err, ERR_BAD_EXPERT);
+                    sel = best;
+                }
+                p = lg[sel] / s;
+            }
+            s_exp[i] = sel;
+            s_prob[i] = p;
+            s_tok[i] = m.token;
+            if (a.hist && a.layer > 0 && m.prev_expert >= 0)
+                atomicAdd(&a.hist[((int64_t)(a.layer - 1) * E + m.prev_expert) * E + sel], 1ull);
+            if (a.trace) a.trace[(int64_t)m.token * a.L + a.layer] = sel;
+        }
     }
     __syncthreads();
     mark3(2);
@@ -534,18 +587,53 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         }
     }
     __syncthreads();
+    mark3(4);  // (diagnostics: every route flag seen)
     for (int k = tid; k < K; k += kThreads)
         if (s_kslot[k] != 0xFF) atomicAdd(&s_cnt[s_kslot[k]], 1);
     __syncthreads();
-    if (tid == 0) {
-        int acc = 0;
-        for (int e = 0; e < a.E_loc; ++e) {
-            tab[e * S::kTabInts] = s_cnt[e];
-            tab[e * S::kTabInts + 1] = acc;
-            s_start[e] = acc;
-            acc += s_cnt[e];
+    // per-expert counts -> first canonical rows: a warp scan (E_loc <= 64, two
+    // experts per lane; thread 0 walking 64 experts was ~1 us of dependent
+    // smem loads). With virtual expert slots, also the binding: the active
+    // experts in id order, then the idle ones (a stable partition; every CTA
+    // derives the same one from the same counts)
+    __shared__ int16_t s_vmap[kMaxKeys];
+    if (warp == 0) {
+        const bool v0 = lane < a.E_loc, v1 = lane + 32 < a.E_loc;
+        const int c0 = v0 ? s_cnt[lane] : 0, c1 = v1 ? s_cnt[lane + 32] : 0;
+        int x0 = c0, x1 = c1;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y0 = __shfl_up_sync(0xffffffffu, x0, off);
+            const int y1 = __shfl_up_sync(0xffffffffu, x1, off);
+            if (lane >= off) {
+                x0 += y0;
+                x1 += y1;
+            }
         }
-        if (blockIdx.x == 0) *a.n_res_out = acc;
+        const int tot0 = __shfl_sync(0xffffffffu, x0, 31);
+        const int tot1 = __shfl_sync(0xffffffffu, x1, 31);
+        if (v0) {
+            tab[lane * S::kTabInts] = c0;
+            tab[lane * S::kTabInts + 1] = x0 - c0;
+            s_start[lane] = x0 - c0;
+        }
+        if (v1) {
+            tab[(lane + 32) * S::kTabInts] = c1;
+            tab[(lane + 32) * S::kTabInts + 1] = tot0 + x1 - c1;
+            s_start[lane + 32] = tot0 + x1 - c1;
+        }
+        if (lane == 0 && blockIdx.x == 0) *a.n_res_out = tot0 + tot1;
+        if (remap) {
+            const uint32_t lt = lanemask_lt();
+            const uint32_t b0 = __ballot_sync(0xffffffffu, v0 && c0 > 0);
+            const uint32_t b1 = __ballot_sync(0xffffffffu, v1 && c1 > 0);
+            const uint32_t i0 = __ballot_sync(0xffffffffu, v0 && c0 == 0);
+            const uint32_t i1 = __ballot_sync(0xffffffffu, v1 && c1 == 0);
+            const int na = __popc(b0) + __popc(b1), ni0 = __popc(i0);
+            if (v0) s_vmap[c0 > 0 ? __popc(b0 & lt) : na + __popc(i0 & lt)] = (int16_t)lane;
+            if (v1)
+                s_vmap[c1 > 0 ? __popc(b0) + __popc(b1 & lt) : na + ni0 + __popc(i1 & lt)] = (int16_t)(lane + 32);
+        }
     }
     __syncthreads();
     // stable placement in (source, t) order, 256 entries per round: warp ranks
@@ -572,6 +660,13 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         }
         __syncthreads();
     }
+    if (remap) {
+        // virtual slot v -> local expert s_vmap[v]. Results do not depend on
+        // the binding: a tile's k order is fixed by the tile (kbr) and its
+        // split-K parts reduce in k order.
+        for (int p = tid; p < npc; p += kThreads) s_pc[p].e = s_vmap[s_pc[p].e];
+        __syncthreads();
+    }
     if (tid == 0) tl_mark(a.tl, 7);
     if (ts && tid == 0) ts[1] = ptx::globaltimer();
     mark3(7);
@@ -596,7 +691,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // chunks of piece p (the CTA's first piece always runs >= 1: prefetched)
     auto nchunks = [&](int p, int g, int e) {
         const int c = (cnt(g, e) + NMAX - 1) / NMAX;
-        return (p == 0 && c == 0) ? 1 : c;
+        return (p == 0 && c == 0 && npre > 0) ? 1 : c;
     };
     // k-blocks a piece streams: an expert without tokens only drains the
     // first piece's prefetched stages (at E_loc = 64 on one GPU with 8
@@ -638,7 +733,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
 #pragma unroll
                         for (int j = 0; j < kKPS; ++j)
                             ptx::tma_load_2d(smem + S::kOffA + st * S::kA + j * S::kA1, tm, &full[st],
-                                             (pc.kb0 + kbr(kbp, kb) + j) * kBK, e * rows + mt * kBM, pol_a);
+                                             (pc.kb0 + kbr(pc, kbp, kb) + j) * kBK, e * rows + mt * kBM, pol_a);
                     }
             }
             if (ts2) {
@@ -771,7 +866,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
 #pragma unroll
                             for (int h = 0; h < kKPS; ++h)
                                 ptx::tma_load_2d(smem + S::kOffB + sb * S::kB + h * S::kB1, tb, &fullB[sb],
-                                                 (pc.kb0 + kbr(kbp, kb) + h) * kBK, row0 + c * NMAX, pol_b);
+                                                 (pc.kb0 + kbr(pc, kbp, kb) + h) * kBK, row0 + c * NMAX, pol_b);
                         }
                     }
                 }
@@ -835,7 +930,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
 #pragma unroll
                     for (int h = 0; h < kKPS; ++h) {
                         uint8_t* sbase = smem + S::kOffB + sb * S::kB + h * S::kB1;
-                        const __nv_bfloat16* kcol = src + (int64_t)(pc.kb0 + kbr(kbp, kb) + h) * kBK + cc * 8;
+                        const __nv_bfloat16* kcol = src + (int64_t)(pc.kb0 + kbr(pc, kbp, kb) + h) * kBK + cc * 8;
 #pragma unroll
                         for (int j = 0; j < NMAX / 4; ++j) {
                             const int r = (lane >> 3) + 4 * j;
@@ -1417,7 +1512,8 @@ int fused_ctas() {
 // A CTA's GEMM2 pieces always follow its GEMM1 pieces (deadlock freedom of the
 // hdone waits). Returns false if a CTA would need more than kMaxPieces.
 bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece>& pieces,
-                          std::vector<int32_t>& off, int* max_contrib, int* max_pieces, bool coop_default) {
+                          std::vector<int32_t>& off, int* max_contrib, int* max_pieces, bool coop_default,
+                          int active_hint) {
     const int k1 = d / kBK, k2 = dff / kBK, mt1 = dff / kBM, mt2 = d / kBM;
     // measured at configs[1]: (16, 16) 45.9 us/layer; (16, 8) 53.2, (16, 12) 49.8,
     // (16, 32) 50.9, (8, 8) 65.2: per-piece costs exceed the model's estimate
@@ -1448,8 +1544,15 @@ bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece
     // last round of pieces spreads over more CTAs
     int tail = 0;
     if (const char* s = std::getenv("EXF_TAIL")) tail = std::atoi(s);
+    // active_hint = A > 0 (virtual expert slots, sparse decode): the first A
+    // slots -- the ones the active experts bind to -- are scheduled as a
+    // complete layer of their own (GEMM1, then GEMM2 overlapping it), the
+    // other slots' pieces queue behind them for the case that more experts
+    // are active
+    const int A = (active_hint > 0 && active_hint < E_loc) ? active_hint : E_loc;
+    for (int blk = 0; blk < (A < E_loc ? 2 : 1); ++blk)
     for (int g = 0; g < (fill2 ? 1 : 2); ++g) {
-        for (int e = 0; e < E_loc; ++e) {
+        for (int e = blk == 0 ? 0 : A; e < (blk == 0 ? A : E_loc); ++e) {
             const int pz = (g == 1 && e >= E_loc - tail) ? std::max(kKPS, psz[g] / 2 / kKPS * kKPS) : psz[g];
             const int S = (kk[g] + pz - 1) / pz;
             for (int mt = 0; mt < mts[g]; ++mt)

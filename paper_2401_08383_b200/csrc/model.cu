@@ -61,7 +61,8 @@ exf_status plan_ffn_gemm(int nmax, int mode, int items, int K, int* ksplit, int*
 exf_status launch_layer_fused(const CUtensorMap* maps, const FusedArgs& a, int nmax, cudaStream_t s);
 exf_status prepare_layer_fused(int nmax);
 bool build_fused_schedule(int E_loc, int d, int dff, int ctas, std::vector<Piece>& pieces,
-                          std::vector<int32_t>& off, int* max_contrib, int* max_pieces, bool coop_default);
+                          std::vector<int32_t>& off, int* max_contrib, int* max_pieces, bool coop_default,
+                          int active_hint);
 int fused_ctas();
 
 namespace {
@@ -183,6 +184,8 @@ struct exf_model {
     // fused layer kernel (one launch per layer)
     bool fused = true;
     bool dense = false;                     // fused, single GPU: dense over resident tokens
+    int remap = 0;                          // dispatch path: virtual expert slots (FusedArgs.remap)
+    int f_active_hint = 0;                  // virtual slots scheduled as their own layer
     int xpre = 0;                           // dense: pieces L2-prefetched before the PDL wait
     int f_ctas = 148, f_tpc = 8, f_max_chunks = 1, f_nmax = 32, f_max_contrib = 1, f_max_pieces = 0;
     Piece* f_pieces = nullptr;              // stream-K schedule of the fused kernel
@@ -513,6 +516,7 @@ FusedArgs fused_args(exf_model* m, int j) {
     a.dense = m->dense ? 1 : 0;
     a.xpre = m->xpre;
     a.hbox = m->hbox;
+    a.remap = m->remap;
     a.res_x_out = m->res_x[(j + 1) & 1];
     a.res_meta_out = m->res_meta[(j + 1) & 1];
     a.n_res_out = m->n_res + ((j + 1) & 1);
@@ -767,14 +771,27 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         m->xpre = m->dense ? 1 : 0;
         if (const char* env = std::getenv("EXF_XPRE")) m->xpre = std::atoi(env);
         if (const char* env = std::getenv("EXF_HBOX")) m->hbox = std::atoi(env);
+        // sparse decode (on average < 2 tokens per local expert, e.g. configs[4]
+        // 64 experts with 8 sequences per GPU): the static schedule spreads
+        // each expert over a fixed set of CTAs, so the few active experts
+        // landed on a few CTAs; remapping puts them on the schedule's first
+        // virtual slots, which cover every CTA
+        m->remap = !m->dense && c.tokens_per_gpu < 2 * m->E_loc ? 1 : 0;
+        if (const char* env = std::getenv("EXF_REMAP")) m->remap = !m->dense && std::atoi(env) != 0;
         const int tok = m->dense ? C : m->nmax;
         const int nmax_f = tok <= 32 ? 32 : (tok <= 64 ? 64 : 128);
         m->f_nmax = nmax_f;
         EXF_M(dalloc(&m->H, (size_t)C * f * ew));
         std::vector<Piece> pieces;
         std::vector<int32_t> off;
+        // virtual slots: schedule the first min(E_loc, tokens per GPU) slots
+        // as a layer of their own (at most that many experts get tokens when a
+        // rank holds its share of the batch)
+        int hint = m->remap ? std::min(m->E_loc, c.tokens_per_gpu) : 0;
+        if (const char* env = std::getenv("EXF_ACTIVE_HINT")) hint = m->remap ? std::atoi(env) : 0;
+        m->f_active_hint = hint;
         if (!build_fused_schedule(m->E_loc, d, f, m->f_ctas, pieces, off, &m->f_max_contrib,
-                                  &m->f_max_pieces, !m->dense))
+                                  &m->f_max_pieces, !m->dense, hint))
             m->fused = m->dense = false;  // too many pieces per CTA: two-kernel path
         EXF_M(dalloc(&m->f_pieces, pieces.size()));
         EXF_M(dalloc(&m->f_piece_off, off.size()));
@@ -1228,6 +1245,8 @@ exf_status exf_model_describe(exf_model* m, char* buf, int32_t len) {
         s += ", \"path\": \"fused\", \"layer_kernel\": {\"ctas\": " + std::to_string(m->f_ctas) +
              ", \"tokens_per_cta\": " + std::to_string(m->f_tpc) +
              ", \"dense\": " + std::string(m->dense ? "true" : "false") +
+             ", \"virtual_expert_slots\": " + std::string(m->remap ? "true" : "false") +
+             ", \"active_hint\": " + std::to_string(m->f_active_hint) +
              ", \"schedule\": \"stream-k\", \"max_pieces_per_cta\": " + std::to_string(m->f_max_pieces) +
              ", \"max_tile_contributors\": " + std::to_string(m->f_max_contrib) + "}}";
     else

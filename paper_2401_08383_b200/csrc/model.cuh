@@ -190,6 +190,10 @@ struct FusedArgs {
     int32_t dense;
     int32_t xpre;  // dense: pieces whose weights are L2-prefetched before the PDL wait
     int32_t hbox;  // dense: GEMM2 H tiles in 16/32-row boxes when the expert has few tokens
+    // dispatch path, few tokens per local expert: the schedule's expert ids are
+    // virtual slots, bound to the local experts in descending token count once
+    // the counts are in (no weight prefetch before the PDL wait)
+    int32_t remap;
     unsigned long long* tl;
     uint64_t* tstamp;    // optional per-CTA stamps [grid][16] (diagnostics)
 };

@@ -409,3 +409,28 @@ def test_expert_migration_local(torch_cuda, orc):
             m.check()
         outs.append((_bf16_bits(ms[0].output()), _union_routes(ms)))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("E,L,d,dff,B,remap", [(64, 2, 1024, 4096, 8, "1"), (16, 3, 256, 512, 8, "1"),
+                                               (16, 3, 256, 512, 8, "0"), (64, 2, 512, 1024, 40, "1")])
+def test_fused_dispatch_virtual_expert_slots(torch_cuda, orc, monkeypatch, E, L, d, dff, B, remap):
+    # sparse decode (fewer tokens than 2 per local expert): the schedule's
+    # expert ids are virtual slots bound to the experts in descending token
+    # count per layer (FusedArgs.remap). Oracle per layer, and the step output
+    # bit-identical with the binding off (a tile's split-K parts still reduce
+    # in k order, whichever CTAs run them).
+    monkeypatch.setenv("EXF_DENSE", "0")
+    monkeypatch.setenv("EXF_REMAP", remap)
+    assign = orc.contiguous_placement(E, L, 1)
+    kw = dict(num_experts=E, num_layers=L, d_model=d, d_ffn=dff, tokens_per_gpu=B, seed=5 + E, gate_affinity=0.6)
+    models = _models(1, assign, **kw)
+    assert models[0].describe()["layer_kernel"]["virtual_expert_slots"] is (remap == "1")
+    xs = _inputs(torch_cuda, models, 3)
+    run_checked(torch_cuda, models, xs, assign, ffn_samples=16, fused=True)
+    out = _bf16_bits(models[0].output())
+    monkeypatch.setenv("EXF_REMAP", "0" if remap == "1" else "1")
+    other = _models(1, assign, **kw)
+    run_checked(torch_cuda, other, xs, assign, ffn_samples=4, fused=True)
+    assert np.array_equal(_bf16_bits(other[0].output()), out)
+    for m in models + other:
+        m.close()
