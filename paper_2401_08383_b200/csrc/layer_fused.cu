@@ -37,6 +37,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstring>
 #include <vector>
 
@@ -403,53 +404,60 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
         __syncthreads();
     }
     mark3(14);
-    // kGI items per warp in flight: one item at a time was a latency chain
+    // GI items per warp in flight: one item at a time was a latency chain
     // (dependent smem loads, 32 FMAs, 5 shuffles) of ~0.45 us per item, ~4 us
-    // for one token over 64 experts; each item keeps its own FMA order
-    constexpr int kGI = 8;
-    for (int w0 = warp; w0 < nt * E; w0 += kWarps * kGI) {
-        float acc[kGI];
-        int xi[kGI], we[kGI];
+    // for one token over 64 experts; each item keeps its own FMA order. GI is
+    // sized to the items per warp (2 / 4 / 8): the loop is issue-bound, and
+    // padding 2 items to 8 cost ~1 us at E = 8 with 2 tokens per CTA
+    auto gate_dots = [&](auto gi_c) {
+        constexpr int GI = decltype(gi_c)::value;
+        for (int w0 = warp; w0 < nt * E; w0 += kWarps * GI) {
+            float acc[GI];
+            int xi[GI], we[GI];
 #pragma unroll
-        for (int u = 0; u < kGI; ++u) {
-            const int w = min(w0 + u * kWarps, nt * E - 1);  // past the end: recompute the last (discarded)
-            xi[u] = w / E;
-            we[u] = w - xi[u] * E;
-            acc[u] = 0.f;
-        }
-        if (x_smem && wg_smem) {
-            const uint32_t wbase = ptx::smem_u32(smem + gate_off) + lane * 16;
-            for (int c = 0; c < chunks; ++c) {
+            for (int u = 0; u < GI; ++u) {
+                const int w = min(w0 + u * kWarps, nt * E - 1);  // past the end: recompute the last (discarded)
+                xi[u] = w / E;
+                we[u] = w - xi[u] * E;
+                acc[u] = 0.f;
+            }
+            if (x_smem && wg_smem) {
+                const uint32_t wbase = ptx::smem_u32(smem + gate_off) + lane * 16;
+                for (int c = 0; c < chunks; ++c) {
 #pragma unroll
-                for (int u = 0; u < kGI; ++u) {
-                    float xf[8], wf[8];
-                    unpack8(lds128(xs_base + ((uint32_t)xi[u] * a.d) * 2 + lane * 16 + c * 512), xf);
-                    unpack8(lds128(wbase + ((uint32_t)we[u] * a.d) * 2 + c * 512), wf);
+                    for (int u = 0; u < GI; ++u) {
+                        float xf[8], wf[8];
+                        unpack8(lds128(xs_base + ((uint32_t)xi[u] * a.d) * 2 + lane * 16 + c * 512), xf);
+                        unpack8(lds128(wbase + ((uint32_t)we[u] * a.d) * 2 + c * 512), wf);
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) acc[u] = fmaf(xf[k], wf[k], acc[u]);
+                        for (int k = 0; k < 8; ++k) acc[u] = fmaf(xf[k], wf[k], acc[u]);
+                    }
+                }
+            } else {
+                for (int c = 0; c < chunks; ++c) {
+#pragma unroll
+                    for (int u = 0; u < GI; ++u) {
+                        float xf[8], wf[8];
+                        unpack8(*reinterpret_cast<const int4*>(a.res_x_in + (int64_t)(t0 + xi[u]) * a.d + lane * 8 + c * 256), xf);
+                        unpack8(*reinterpret_cast<const int4*>(a.wg + (int64_t)we[u] * a.d + lane * 8 + c * 256), wf);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) acc[u] = fmaf(xf[k], wf[k], acc[u]);
+                    }
                 }
             }
-        } else {
-            for (int c = 0; c < chunks; ++c) {
 #pragma unroll
-                for (int u = 0; u < kGI; ++u) {
-                    float xf[8], wf[8];
-                    unpack8(*reinterpret_cast<const int4*>(a.res_x_in + (int64_t)(t0 + xi[u]) * a.d + lane * 8 + c * 256), xf);
-                    unpack8(*reinterpret_cast<const int4*>(a.wg + (int64_t)we[u] * a.d + lane * 8 + c * 256), wf);
+            for (int off = 16; off >= 1; off >>= 1)
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) acc[u] = fmaf(xf[k], wf[k], acc[u]);
-                }
-            }
+                for (int u = 0; u < GI; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], off);
+            if (lane == 0)
+#pragma unroll
+                for (int u = 0; u < GI; ++u)
+                    if (w0 + u * kWarps < nt * E) s_logit[w0 + u * kWarps] = acc[u];
         }
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1)
-#pragma unroll
-            for (int u = 0; u < kGI; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], off);
-        if (lane == 0)
-#pragma unroll
-            for (int u = 0; u < kGI; ++u)
-                if (w0 + u * kWarps < nt * E) s_logit[w0 + u * kWarps] = acc[u];
-    }
+    };
+    if (nt * E <= 2 * kWarps) gate_dots(std::integral_constant<int, 2>{});
+    else if (nt * E <= 4 * kWarps) gate_dots(std::integral_constant<int, 4>{});
+    else gate_dots(std::integral_constant<int, 8>{});
     __syncthreads();
     mark3(13);
     // softmax / top-1, one warp per token: top-1 = the lowest index among the
@@ -547,6 +555,11 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             }
         }
     }
+    // per-warp key counters of the route-flag scan below (token-row ring, free
+    // since the gate); the barrier that orders the rows before the flags
+    // orders these stores before the scan
+    int32_t* s_wcnt = reinterpret_cast<int32_t*>(smem + S::kOffB + kMaxList);  // [kWarps][kMaxKeys]
+    for (int x = tid; x < kWarps * kMaxKeys; x += kThreads) s_wcnt[x] = 0;
     __syncthreads();  // rows and metas stored before any flag (release below)
     mark3(5);
     // flags published by the last threads: thread 0 issued the weight-prefetch
@@ -563,43 +576,83 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     if (tid == 0) tl_mark(a.tl, 6);
     mark3(6);
     // ---------------- (3) every CTA reads the G*C route flags destined here
-    // (scratch in the idle token-row ring: slot per entry, per-warp counts)
+    // Warp w owns the contiguous entries [w*Kw, (w+1)*Kw) in 32-entry rounds:
+    // its lanes issue every flag load at once (up to 16 each), spin on the
+    // late ones, acquire with one fence, and rank the entries per local slot
+    // with match_any against per-warp running counts. One barrier, a warp
+    // scan over the per-warp counts, and one placement pass give the
+    // canonical (slot, source, order) lists -- the previous 256-entry rounds
+    // paid 4 CTA barriers each (~3 us at G*C = 1024) and one serial acquire
+    // per flag.
     const int K = a.G * a.C;
+    const int Kw = ((K + kWarps - 1) / kWarps + 31) & ~31;
+    const int nr = Kw >> 5;  // rounds per warp (<= kMaxList / kWarps / 32 = 16)
+    constexpr int kMaxRounds = kMaxList / kWarps / 32;
     uint8_t* s_kslot = smem + S::kOffB;
-    int32_t* s_wcnt = reinterpret_cast<int32_t*>(smem + S::kOffB + kMaxList);  // [kWarps][kMaxKeys]
+    int16_t* s_rank = reinterpret_cast<int16_t*>(smem + S::kOffB + kMaxList + kWarps * kMaxKeys * 4);
     int16_t* s_list = reinterpret_cast<int16_t*>(smem + S::kOffList);
-    if (tid < kMaxKeys) {
-        s_cnt[tid] = 0;
-        s_before[tid] = 0;
-    }
     {
         const uint64_t* f = reinterpret_cast<const uint64_t*>(a.own_sym + a.sym.cflags) + (int64_t)parity * K;
-        for (int k = tid; k < K; k += kThreads) {
-            ptx::SpinGuard g;
-            uint64_t v;
-            // (a poll back-off, which helped the dense route flags, measured
-            // no gain here at N=4: the flags arrive late, they are not polled late)
-            while (((v = ptx::ld_relaxed_u64(f + k, sys)) >> 40) != e24) g.step(a.err, 112);
-            // acquire once, on the flag itself (orders this slot's row + meta;
-            // bar.sync below extends it to the CTA)
-            (void)ptx::flag_read(f + k, sys);
-            s_kslot[k] = (uint8_t)((v >> 32) & 0xFF);
+        const int kb = warp * Kw + lane;
+        uint64_t v[kMaxRounds];
+#pragma unroll
+        for (int r = 0; r < kMaxRounds; ++r)
+            if (r < nr && kb + r * 32 < K) v[r] = ptx::ld_relaxed_u64(f + kb + r * 32, sys);
+        int32_t* wc = s_wcnt + warp * kMaxKeys;
+#pragma unroll
+        for (int r = 0; r < kMaxRounds; ++r) {
+            if (r >= nr) break;  // warp-uniform
+            const int k = kb + r * 32;
+            int key = -1;
+            if (k < K) {
+                ptx::SpinGuard g;
+                while ((v[r] >> 40) != e24) {
+                    g.step(a.err, 112);
+                    v[r] = ptx::ld_relaxed_u64(f + k, sys);
+                }
+                // acquire once, on the flag itself (orders this slot's row +
+                // meta; the barrier below extends it to the CTA). One fence per
+                // thread instead cost ~2.4 us before the next memory access.
+                (void)ptx::flag_read(f + k, sys);
+                const int sl = (int)((v[r] >> 32) & 0xFF);
+                s_kslot[k] = (uint8_t)sl;
+                key = sl != 0xFF ? sl : -1;
+            }
+            const uint32_t peers = __match_any_sync(0xffffffffu, key);
+            const int rk = __popc(peers & lanemask_lt());
+            const int base = key >= 0 ? wc[key] : 0;
+            __syncwarp();
+            if (key >= 0 && rk == 0) wc[key] = base + __popc(peers);
+            __syncwarp();
+            if (k < K) s_rank[k] = (int16_t)(base + rk);
         }
     }
     __syncthreads();
     mark3(4);  // (diagnostics: every route flag seen)
-    for (int k = tid; k < K; k += kThreads)
-        if (s_kslot[k] != 0xFF) atomicAdd(&s_cnt[s_kslot[k]], 1);
-    __syncthreads();
     // per-expert counts -> first canonical rows: a warp scan (E_loc <= 64, two
     // experts per lane; thread 0 walking 64 experts was ~1 us of dependent
-    // smem loads). With virtual expert slots, also the binding: the active
-    // experts in id order, then the idle ones (a stable partition; every CTA
-    // derives the same one from the same counts)
+    // smem loads), the per-warp counters turned into per-warp offsets in
+    // place. With virtual expert slots, also the binding: the active experts
+    // in id order, then the idle ones (a stable partition; every CTA derives
+    // the same one from the same counts)
     __shared__ int16_t s_vmap[kMaxKeys];
     if (warp == 0) {
         const bool v0 = lane < a.E_loc, v1 = lane + 32 < a.E_loc;
-        const int c0 = v0 ? s_cnt[lane] : 0, c1 = v1 ? s_cnt[lane + 32] : 0;
+        int c0 = 0, c1 = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            if (v0) {
+                const int n0 = s_wcnt[w * kMaxKeys + lane];
+                s_wcnt[w * kMaxKeys + lane] = c0;
+                c0 += n0;
+            }
+            if (v1) {
+                const int n1 = s_wcnt[w * kMaxKeys + lane + 32];
+                s_wcnt[w * kMaxKeys + lane + 32] = c1;
+                c1 += n1;
+            }
+        }
+        if (v0) s_cnt[lane] = c0;
+        if (v1) s_cnt[lane + 32] = c1;
         int x0 = c0, x1 = c1;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -635,31 +688,14 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
                 s_vmap[c1 > 0 ? __popc(b0) + __popc(b1 & lt) : na + ni0 + __popc(i1 & lt)] = (int16_t)(lane + 32);
         }
     }
+    mark3(3);  // (diagnostics: count scan done)
     __syncthreads();
-    // stable placement in (source, t) order, 256 entries per round: warp ranks
-    // by match_any, cross-warp prefix through s_wcnt
-    for (int k0 = 0; k0 < K; k0 += kThreads) {
-        const int k = k0 + tid;
-        const int key = (k < K && s_kslot[k] != 0xFF) ? s_kslot[k] : -1;
-        const uint32_t peers = __match_any_sync(0xffffffffu, key);
-        const int rk = __popc(peers & lanemask_lt());
-        for (int x = tid; x < kWarps * kMaxKeys; x += kThreads) s_wcnt[x] = 0;
-        __syncthreads();
-        if (key >= 0 && rk == 0) s_wcnt[warp * kMaxKeys + key] = __popc(peers);
-        __syncthreads();
-        if (key >= 0) {
-            int before = s_start[key] + s_before[key] + rk;
-            for (int w = 0; w < warp; ++w) before += s_wcnt[w * kMaxKeys + key];
-            s_list[before] = (int16_t)k;
-        }
-        __syncthreads();
-        if (tid < a.E_loc) {
-            int tot = 0;
-            for (int w = 0; w < kWarps; ++w) tot += s_wcnt[w * kMaxKeys + tid];
-            s_before[tid] += tot;
-        }
-        __syncthreads();
+    // placement: slot start + entries of earlier warps + rank within the warp
+    for (int k = tid; k < K; k += kThreads) {
+        const int key = s_kslot[k];
+        if (key != 0xFF) s_list[s_start[key] + s_wcnt[(k / Kw) * kMaxKeys + key] + s_rank[k]] = (int16_t)k;
     }
+    __syncthreads();
     if (remap) {
         // virtual slot v -> local expert s_vmap[v]. Results do not depend on
         // the binding: a tile's k order is fixed by the tile (kbr) and its

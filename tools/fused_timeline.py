@@ -136,7 +136,7 @@ def main():
     cur = buf[3].astype(np.int64)
     prv = buf[2].astype(np.int64)
     z = prv[:, 15].max()
-    names = ["entry", "pdl wait", "gate", "dots(t0)", "flags", "dispatch", "completion", "tables"]
+    names = ["entry", "pdl wait", "gate", "scan", "flags", "dispatch", "completion", "tables"]
     print(f"token phase rel. previous layer's last exit (prev exit min {(prv[:, 15].min() - z) / 1e3:.2f}):")
     for k, nm in enumerate(names):
         v = (cur[:, k] - z) / 1e3
