@@ -1504,7 +1504,8 @@ struct FusedLauncher {
     }
     exf_status launch(const CUtensorMap* maps, const FusedArgs& a, cudaStream_t s) {
         EXF_TRY(prepare());
-        EXF_CUDA_TRY(launch_pdl(kern, dim3(ctas), dim3(kThreads), Sm::kBytes, s, 0, maps[0], maps[1],
+        const int grid = a.ctas > 0 ? std::min(a.ctas, ctas) : ctas;
+        EXF_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(kThreads), Sm::kBytes, s, 0, maps[0], maps[1],
                                 maps[2], maps[3], maps[4], maps[5], a));
         return EXF_OK;
     }

@@ -517,6 +517,7 @@ FusedArgs fused_args(exf_model* m, int j) {
     a.xpre = m->xpre;
     a.hbox = m->hbox;
     a.remap = m->remap;
+    a.ctas = m->f_ctas;
     a.res_x_out = m->res_x[(j + 1) & 1];
     a.res_meta_out = m->res_meta[(j + 1) & 1];
     a.n_res_out = m->n_res + ((j + 1) & 1);
@@ -748,6 +749,11 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         if (const char* env = std::getenv("EXF_FUSED")) m->fused = std::atoi(env) != 0;
         if (m->esz == 4) m->fused = false;  // fp32 mode: two-kernel path with the SIMT fp32 FFN
         m->f_ctas = fused_ctas();
+        // EXF_FUSED_CTAS: a smaller persistent grid, so that several ranks'
+        // layer kernels can be co-resident on one GPU (tests run the G=8
+        // dispatch path as 8 ranks x 18 CTAs on one device)
+        if (const char* env = std::getenv("EXF_FUSED_CTAS"))
+            m->f_ctas = std::max(1, std::min(m->f_ctas, std::atoi(env)));
         // one token per CTA while C <= #SMs: the gate's (token, expert) dot
         // products then spread over 8 warps of many CTAs
         m->f_tpc = std::max(1, (C + m->f_ctas - 1) / m->f_ctas);

@@ -61,7 +61,7 @@ def _union_routes(models):
     return r
 
 
-def run_checked(torch, models, xs, assign, ffn_samples=48, seed=0, forced=None, fused=False):
+def run_checked(torch, models, xs, assign, ffn_samples=48, seed=0, forced=None, fused=False, streams=None):
     """Lock-step phased run with per-layer oracle checks; returns final routes.
     fused=True drives the one-launch-per-layer kernel (layer_fused.cu). With
     ep_mode EP_VANILLA every layer is followed by the combine (outputs back to
@@ -85,8 +85,12 @@ def run_checked(torch, models, xs, assign, ffn_samples=48, seed=0, forced=None, 
             for r in range(G):
                 assert (before[r][1][:, 0] == cfg.home_tokens(r)).all()
         if fused:
-            assert G == 1, "the fused layer kernel needs one process (or GPU) per rank"
-            models[0].phase(PHASE_FUSED, j)
+            # one rank per GPU, or co-resident ranks (EXF_FUSED_CTAS) on their
+            # own streams: every rank's layer kernel must run concurrently
+            assert G == 1 or streams is not None, "the fused layer kernel needs concurrent ranks"
+            for r, m in enumerate(models):
+                m.phase(PHASE_FUSED, j, stream=None if streams is None else streams[r])
+            torch.cuda.synchronize()
         else:
             for m in models:
                 m.phase(PHASE_DISPATCH, j)
@@ -433,4 +437,26 @@ def test_fused_dispatch_virtual_expert_slots(torch_cuda, orc, monkeypatch, E, L,
     run_checked(torch_cuda, other, xs, assign, ffn_samples=4, fused=True)
     assert np.array_equal(_bf16_bits(other[0].output()), out)
     for m in models + other:
+        m.close()
+
+
+@pytest.mark.parametrize("E,B,ep", [(8, 16, "coherent"), (8, 64, "coherent"), (64, 8, "coherent"), (16, 16, "vanilla")])
+def test_fused_dispatch_path_eight_ranks_one_gpu(torch_cuda, orc, monkeypatch, E, B, ep):
+    # the fused dispatch path at G = 8 (BASELINE configs[1] one expert per GPU,
+    # configs[4] eight experts per GPU) without eight GPUs: 8 ranks share this
+    # device with 18-CTA layer kernels (EXF_FUSED_CTAS), all co-resident, each
+    # on its own stream; route flags, receive regions and peers as across GPUs
+    from paper_2401_08383_b200.model import EP_VANILLA
+    monkeypatch.setenv("EXF_FUSED_CTAS", "18")
+    G, L = 8, 3
+    assign = orc.random_placement(E, L, G, 11)
+    kw = dict(ep_mode=EP_VANILLA) if ep == "vanilla" else {}
+    models = _models(G, assign, num_experts=E, num_layers=L, d_model=1024, d_ffn=4096, tokens_per_gpu=B,
+                     seed=21 + E, gate_affinity=0.6, **kw)
+    d = models[0].describe()
+    assert d["path"] == "fused" and d["layer_kernel"]["ctas"] == 18
+    streams = [torch_cuda.cuda.Stream() for _ in models]
+    xs = _inputs(torch_cuda, models, 4)
+    run_checked(torch_cuda, models, xs, assign, ffn_samples=6, fused=True, streams=streams)
+    for m in models:
         m.close()
