@@ -260,6 +260,7 @@ extern "C" exf_status exf_count_transitions(const int32_t* d_paths, int64_t T, i
                                             int32_t E, int32_t gap, int64_t* d_counts,
                                             int64_t* d_row_totals, void* d_workspace,
                                             exf_stream_t stream) {
+    exf::NvtxRange nvtx_range("exf.count_transitions");
     EXF_TRY(check_hist_args(T, L, E, gap));
     if (!d_paths || !d_counts) return invalid("null device pointer");
     // (d_workspace: NULL allowed when exf_count_transitions_workspace_bytes == 0)
@@ -303,6 +304,7 @@ extern "C" exf_status exf_count_transitions(const int32_t* d_paths, int64_t T, i
 extern "C" exf_status exf_count_transitions_host(const int32_t* h_paths, int64_t T, int32_t L,
                                                  int32_t E, int32_t gap, int64_t* h_counts,
                                                  int64_t* h_row_totals) {
+    exf::NvtxRange nvtx_range("exf.count_transitions_host");
     EXF_TRY(check_hist_args(T, L, E, gap));
     for (int64_t i = 0; i < T * (int64_t)L; ++i)
         if (h_paths[i] < 0 || h_paths[i] >= E)

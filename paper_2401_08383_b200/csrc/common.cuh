@@ -11,7 +11,30 @@
 
 #include "exflow_c.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace exf {
+
+// NVTX range over a host entry point (header-only NVTX v3: a no-op unless a
+// tool such as nsys/ncu attaches). Names are "exf.<what>"; the step phases
+// carry the layer in the payload.
+struct NvtxRange {
+    explicit NvtxRange(const char* name, int64_t payload = -1) {
+        nvtxEventAttributes_t ev{};
+        ev.version = NVTX_VERSION;
+        ev.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+        ev.messageType = NVTX_MESSAGE_TYPE_ASCII;
+        ev.message.ascii = name;
+        if (payload >= 0) {
+            ev.payloadType = NVTX_PAYLOAD_TYPE_INT64;
+            ev.payload.llValue = payload;
+        }
+        nvtxRangePushEx(&ev);
+    }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Thread-local last-error message behind exf_last_error().
 void set_error(const std::string& msg);

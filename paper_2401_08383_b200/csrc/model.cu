@@ -597,6 +597,10 @@ exf_status run_attention(exf_model* m, int j, cudaStream_t s) {
 }
 
 exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStream_t s) {
+    static const char* const kNames[] = {"exf.step_begin", "exf.gate_dispatch", "exf.expert_ffn",
+                                         "exf.gather_send", "exf.gather_wait", "exf.layer_fused",
+                                         "exf.combine_send", "exf.combine_wait", "exf.attention_block"};
+    NvtxRange range(phase >= 0 && phase <= 8 ? kNames[phase] : "exf.phase", j);
     const auto& c = m->cfg;
     if (!m->connected) return invalid("model is not connected to its peers (exf_model_connect)");
     switch (phase) {
@@ -939,6 +943,7 @@ exf_status exf_model_connect_local(exf_model* const* models, int32_t count) {
 
 exf_status exf_model_step(exf_model* m, const void* d_x_in, exf_stream_t stream) {
     if (!m) return invalid("null model");
+    NvtxRange range("exf.model_step");
     return run_step(m, d_x_in, static_cast<cudaStream_t>(stream));
 }
 
@@ -1064,6 +1069,7 @@ exf_status exf_model_expert_storage(exf_model* m, int32_t layer, int32_t slot, v
 }
 
 exf_status exf_model_set_placement(exf_model* m, const int32_t* h_assign) {
+    NvtxRange nvtx_range("exf.set_placement");
     if (!m || !h_assign) return invalid("null argument");
     EXF_CUDA_TRY(cudaDeviceSynchronize());  // no step may be in flight
     return set_placement(m, h_assign);
@@ -1074,6 +1080,7 @@ exf_status exf_model_context_setup(exf_model* m, exf_stream_t stream) {
 }
 
 exf_status exf_model_context_setup_phase(exf_model* m, int32_t phase, exf_stream_t stream) {
+    NvtxRange nvtx_range("exf.context_setup");
     if (!m) return invalid("null model");
     if (phase < 0 || phase > 3)
         return invalid("context setup phase must be 0 (both), 1 (publish), 2 (wait) or 3 (local synthesis)");
@@ -1172,6 +1179,7 @@ exf_status exf_model_read_resident(exf_model* m, int32_t which, uint16_t* h_x, i
 }
 
 exf_status exf_model_capture(exf_model* m, const void* d_x_in, exf_stream_t stream) {
+    NvtxRange nvtx_range("exf.capture");
     if (!m) return invalid("null model");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (!s) return invalid("graph capture needs a non-default stream");
@@ -1198,6 +1206,7 @@ exf_status exf_model_capture(exf_model* m, const void* d_x_in, exf_stream_t stre
 }
 
 exf_status exf_model_replay(exf_model* m, exf_stream_t stream) {
+    NvtxRange nvtx_range("exf.replay");
     if (!m || !m->graph_exec) return invalid("no captured graph (exf_model_capture)");
     EXF_CUDA_TRY(cudaGraphLaunch(m->graph_exec, static_cast<cudaStream_t>(stream)));
     return EXF_OK;

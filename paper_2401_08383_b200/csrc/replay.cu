@@ -210,6 +210,7 @@ extern "C" exf_status exf_simulate_host(const int32_t* h_paths, int64_t T, int32
                                         int32_t gpus_per_node, double intra_cost,
                                         double inter_cost, int32_t tokens_per_gpu, int32_t mode,
                                         const int32_t* h_homes, exf_sim_report* out) {
+    exf::NvtxRange nvtx_range("exf.simulate_host");
     // validation order follows simulate (proj/src/sim.cpp:78-105): the trace
     // (trace.cpp:53-70), then the placement (placement.cpp:434-470), then the
     // config (topology, then tokens_per_gpu; sim.cpp:24-32), then the homes
