@@ -185,6 +185,9 @@ struct exf_model {
     bool fused = true;
     bool dense = false;                     // fused, single GPU: dense over resident tokens
     int remap = 0;                          // dispatch path: virtual expert slots (FusedArgs.remap)
+    uint64_t* fin_gen = nullptr;            // fused kernel: per-CTA exit generation (FusedArgs.fin_gen)
+    bool in_step = false;                   // eager run_step in progress: chained layer kernels
+    bool chain_ok = true;                   // EXF_CHAIN=0 disables chaining
     int f_active_hint = 0;                  // virtual slots scheduled as their own layer
     int xpre = 0;                           // dense: pieces L2-prefetched before the PDL wait
     int f_ctas = 148, f_tpc = 8, f_max_chunks = 1, f_nmax = 32, f_max_contrib = 1, f_max_pieces = 0;
@@ -517,6 +520,10 @@ FusedArgs fused_args(exf_model* m, int j) {
     a.xpre = m->xpre;
     a.hbox = m->hbox;
     a.remap = m->remap;
+    a.fin_gen = m->fin_gen;
+    // chained layers: only inside a whole step (run_step), from the second
+    // layer on, when nothing else runs between two layer kernels
+    a.chain = (m->in_step && j > 0 && !m->dense && m->nh == 0 && c.ep_mode != EXF_EP_VANILLA && m->chain_ok) ? 1 : 0;
     a.ctas = m->f_ctas;
     a.res_x_out = m->res_x[(j + 1) & 1];
     a.res_meta_out = m->res_meta[(j + 1) & 1];
@@ -659,7 +666,21 @@ exf_status run_phase(exf_model* m, int phase, int j, const void* x_in, cudaStrea
     }
 }
 
-exf_status run_step(exf_model* m, const void* x_in, cudaStream_t s) {
+exf_status run_step_layers(exf_model* m, const void* x_in, cudaStream_t s);
+
+// chain: layer kernels after the first wait for the previous layer's CTA exit
+// generations instead of griddepcontrol.wait (FusedArgs.chain). Measured at
+// N=4: eager steps 952 -> 894 us, graph replays 882 -> 895 us (a replayed
+// graph already hides most of the grid-completion flush), so only the eager
+// exf_model_step chains.
+exf_status run_step(exf_model* m, const void* x_in, cudaStream_t s, bool chain = false) {
+    m->in_step = chain;
+    const exf_status st = run_step_layers(m, x_in, s);
+    m->in_step = false;
+    return st;
+}
+
+exf_status run_step_layers(exf_model* m, const void* x_in, cudaStream_t s) {
     EXF_TRY(run_phase(m, 0, 0, x_in, s));
     capture_trace(s, "begin", 0);
     for (int j = 0; j < m->cfg.num_layers; ++j) {
@@ -817,6 +838,8 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         EXF_M(dalloc(&m->hdone, (size_t)2 * m->E_loc));
         EXF_M(dalloc(&m->fbar, 2 * 260));  // 256 per-CTA barrier slots + epoch (u64)
         EXF_M(dalloc(&m->f_cta_cnt, (size_t)m->f_ctas * E));
+        EXF_M(dalloc(&m->fin_gen, (size_t)m->f_ctas));
+        if (const char* env = std::getenv("EXF_CHAIN")) m->chain_ok = std::atoi(env) != 0;
         if (m->fused) EXF_M(prepare_layer_fused(nmax_f));
     }
     if (std::getenv("EXF_FFN_TIMELINE")) {
@@ -880,7 +903,7 @@ exf_status exf_model_destroy(exf_model* m) {
                     m->res_x[1], m->res_meta[0], m->res_meta[1], m->n_res, m->expert, m->prob, m->H,
                     m->hist, m->crossed, m->trace, m->forced, m->step, m->err, m->done_ctr,
                     m->cta_cnt, m->gbar, m->tl, m->ws, m->item_ctr, m->hdone, m->fbar,
-                    m->f_cta_cnt, m->f_pieces, m->f_piece_off,
+                    m->f_cta_cnt, m->f_pieces, m->f_piece_off, m->fin_gen,
                     m->d_peers, m->sym_base, m->tstamp, m->wg32, m->w1_32, m->b1_32, m->w2_32,
                     m->b2_32, m->wqkv, m->bqkv, m->wo, m->bo, m->qb, m->kb, m->vb, m->ab,
                     m->attn_ws, m->kv_overflow};
@@ -944,7 +967,7 @@ exf_status exf_model_connect_local(exf_model* const* models, int32_t count) {
 exf_status exf_model_step(exf_model* m, const void* d_x_in, exf_stream_t stream) {
     if (!m) return invalid("null model");
     NvtxRange range("exf.model_step");
-    return run_step(m, d_x_in, static_cast<cudaStream_t>(stream));
+    return run_step(m, d_x_in, static_cast<cudaStream_t>(stream), true);
 }
 
 exf_status exf_model_step_phase(exf_model* m, int32_t phase, int32_t layer, const void* d_x_in,

@@ -194,6 +194,8 @@ struct FusedArgs {
     // virtual slots, bound to the local experts in descending token count once
     // the counts are in (no weight prefetch before the PDL wait)
     int32_t remap;
+    int32_t chain;      // previous kernel in the stream = this model's previous layer (see fin_gen)
+    uint64_t* fin_gen;  // [ctas] exit generation (global layer index + 1) per CTA
     int32_t ctas;  // grid size (the schedule's CTA count; <= #SMs, all co-resident)
     unsigned long long* tl;
     uint64_t* tstamp;    // optional per-CTA stamps [grid][16] (diagnostics)

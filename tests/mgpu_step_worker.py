@@ -54,6 +54,20 @@ def main():
     m.check()
     dist.barrier()
     res = check_step(m, x, assign, rows_per_layer=a.rows)
+    # the eager step (layer kernels chained on exit generations, FusedArgs.chain)
+    # and a graph replay (griddepcontrol.wait between layers) give the same bits
+    m.step(x, s)
+    s.synchronize()
+    eager = m.output().clone()
+    dist.barrier()
+    m.capture(x, s)
+    m.replay(s)
+    s.synchronize()
+    m.check()
+    if not torch.equal(eager, m.output()):
+        res["parity"] = "FAIL"
+        res["failures"] = res.get("failures", []) + ["eager (chained) step != graph replay"]
+    dist.barrier()
     path = m.describe().get("path")
     if rank == 0:
         tag = (f"G={G} E={E} L={L} d={a.d_model} dff={a.d_ffn} B={a.batch} {a.dtype} path={path} "

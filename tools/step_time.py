@@ -17,6 +17,7 @@ def main():
     p.add_argument("--layers", type=int, default=24)
     p.add_argument("--d-model", type=int, default=1024)
     p.add_argument("--d-ffn", type=int, default=4096)
+    p.add_argument("--eager", action="store_true", help="time exf_model_step calls instead of graph replays")
     a = p.parse_args()
     import torch
     from paper_2401_08383_b200 import placement as pl
@@ -38,14 +39,16 @@ def main():
     s = torch.cuda.Stream()
     for _ in range(3):
         m.step(x, s)
-    m.capture(x, s)
+    run = (lambda: m.step(x, s)) if a.eager else (lambda: m.replay(s))
+    if not a.eager:
+        m.capture(x, s)
     for _ in range(5):
-        m.replay(s)
+        run()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.synchronize()
     e0.record(s)
     for _ in range(a.reps):
-        m.replay(s)
+        run()
     e1.record(s)
     e1.synchronize()
     m.check()
