@@ -211,12 +211,16 @@ __host__ __device__ inline int64_t bytes_bf16(int64_t n) { return n * 2; }
 // which made the expert epilogues the critical path.
 __device__ __forceinline__ float gelu_erf(float v) {
     const float z = fabsf(v) * 0.70710678118654752440f;
-    const float t = __fdividef(1.0f, fmaf(0.3275911f, z, 1.0f));
+    // single MUFU ops (flush-to-zero approximations; the 7.1.26 polynomial's
+    // own error, 1.5e-7, dominates): __fdividef / exp2f carried denormal
+    // fix-up code into the epilogue loops
+    float t, e;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.0f)));
     float p = fmaf(1.061405429f, t, -1.453152027f);
     p = fmaf(p, t, 1.421413741f);
     p = fmaf(p, t, -0.284496736f);
     p = fmaf(p, t, 0.254829592f);
-    const float e = exp2f(-z * z * 1.44269504088896341f);
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-z * z * 1.44269504088896341f));
     const float erf_abs = fmaf(-p * t, e, 1.0f);
     return 0.5f * v * (1.0f + copysignf(erf_abs, v));
 }
