@@ -447,10 +447,12 @@ def main():
     # DRAM bytes per launch of the dominant kernel from the committed
     # `ncu --set full` capture (profiles/), when it matches this kernel
     traffic, traffic_src = None, None
-    ncu_path = os.path.join(ROOT, "profiles", "r01_fused_ncu_summary.json")
-    if fused and n == 1 and os.path.exists(ncu_path):
-        summ = json.load(open(ncu_path))
-        traffic, traffic_src = summ.get("traffic_bytes_per_launch"), "profiles/r01_fused_ncu_summary.json"
+    for name in ("r02_fused_ncu_summary.json", "r01_fused_ncu_summary.json"):
+        ncu_path = os.path.join(ROOT, "profiles", name)
+        if fused and n == 1 and os.path.exists(ncu_path):
+            summ = json.load(open(ncu_path))
+            traffic, traffic_src = summ.get("traffic_bytes_per_launch"), "profiles/" + name
+            break
     launches = model.launches_per_step()
 
     # ---- fp32 mode (north_star: 1e-5 in fp32 mode): the same workload with
