@@ -416,7 +416,9 @@ def test_expert_migration_local(torch_cuda, orc):
 
 
 @pytest.mark.parametrize("E,L,d,dff,B,remap", [(64, 2, 1024, 4096, 8, "1"), (16, 3, 256, 512, 8, "1"),
-                                               (16, 3, 256, 512, 8, "0"), (64, 2, 512, 1024, 40, "1")])
+                                               (16, 3, 256, 512, 8, "0"), (64, 2, 512, 1024, 40, "1"),
+                                               # BASELINE configs[3] (1.3B: E=32, d=2048) at B=16
+                                               (32, 2, 2048, 8192, 16, "1")])
 def test_fused_dispatch_virtual_expert_slots(torch_cuda, orc, monkeypatch, E, L, d, dff, B, remap):
     # sparse decode (fewer tokens than 2 per local expert): the schedule's
     # expert ids are virtual slots bound to the experts in descending token
