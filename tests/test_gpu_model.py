@@ -288,10 +288,16 @@ def test_forced_markov_routes_replay_parity(torch_cuda, orc):
         assert crossed.sum() / (G * B * L) == rep.p_star
 
 
-def test_full_step_and_graph_replay_match_phased(torch_cuda, orc):
+@pytest.mark.parametrize("E,B,dense", [(8, 128, "1"), (8, 128, "0"), (64, 8, "0")])
+def test_full_step_and_graph_replay_match_phased(torch_cuda, orc, monkeypatch, E, B, dense):
+    # eager exf_model_step (dispatch path: layer kernels chained on exit
+    # generations), graph replays (PDL waits) and the phased run give the same
+    # bits; dense single-GPU mode, the dispatch path, and sparse decode with
+    # virtual expert slots (E=64, 8 tokens)
     torch = torch_cuda
-    assign = orc.contiguous_placement(8, 4, 1)
-    kw = dict(num_experts=8, num_layers=4, d_model=512, d_ffn=1024, tokens_per_gpu=128, seed=8,
+    monkeypatch.setenv("EXF_DENSE", dense)
+    assign = orc.contiguous_placement(E, 4, 1)
+    kw = dict(num_experts=E, num_layers=4, d_model=512, d_ffn=1024, tokens_per_gpu=B, seed=8,
               gate_affinity=0.5)
     m = _models(1, assign, **kw)[0]
     x = _inputs(torch, [m], 2)[0]
