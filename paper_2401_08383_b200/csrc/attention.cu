@@ -381,7 +381,12 @@ __global__ void __launch_bounds__(128) kv_append_kernel(const uint4* __restrict_
             reinterpret_cast<uint4*>(rep.v[r])[off] = vv;
         }
     }
-    __threadfence_system();  // rows visible before the new length
+    // rows visible before the new length: system scope when replicas live on
+    // peer GPUs, device scope when the only replica is local
+    if (replicas > 1)
+        __threadfence_system();
+    else
+        __threadfence();
     __syncthreads();
     if (threadIdx.x == 0)
         for (int r = 0; r < replicas; ++r) rep.ctx[r][s] = pos + 1;
