@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kF32Threads) ffn_f32_kernel(FfnF32Args a) {
         const uint64_t epoch = q + 1;
         const uint64_t* f = reinterpret_cast<const uint64_t*>(a.own_sym + a.sym.flags) + parity * a.G + tid;
         ptx::SpinGuard g;
-        while (ptx::ld_acquire_sys(f) < epoch) g.step(a.err, ERR_TIMEOUT_DISPATCH);
+        while (ptx::flag_read(f, a.G > 1) < epoch) g.step(a.err, ERR_TIMEOUT_DISPATCH);
     }
     __syncthreads();
     const int32_t* cnt = reinterpret_cast<const int32_t*>(a.own_sym + a.sym.recv_cnt) +

@@ -135,7 +135,7 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant
     if (MODE == 0 && tid < a.G) {
         const uint64_t* f = reinterpret_cast<const uint64_t*>(a.own_sym + a.sym.flags) + parity * a.G + tid;
         ptx::SpinGuard g;
-        while (ptx::ld_acquire_sys(f) < epoch) g.step(a.err, ERR_TIMEOUT_DISPATCH);
+        while (ptx::flag_read(f, a.G > 1) < epoch) g.step(a.err, ERR_TIMEOUT_DISPATCH);
     }
     __syncthreads();
     // ---- per-expert segment tables: tokens of expert e from source s occupy

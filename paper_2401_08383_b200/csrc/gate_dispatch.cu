@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kGdThreads) gate_dispatch_kernel(LayerArgs a, 
     __syncthreads();  // counts and rows precede the release stores below
     if (tid < a.G) {
         uint64_t* f = reinterpret_cast<uint64_t*>(a.peers[tid] + a.sym.flags);
-        ptx::st_release_sys(f + parity * a.G + a.rank, epoch);
+        ptx::flag_publish(f + parity * a.G + a.rank, epoch, a.G > 1);  // .gpu scope on one GPU
     }
     if (tid == 0 && nactive > 1) *a.done_ctr = 0;
     if (tid == 0) tl_mark(a.tl, 3);
@@ -368,8 +368,8 @@ __global__ void __launch_bounds__(512) gather_send_kernel(
         if (prev == (int)gridDim.x - 1) {
             if (G > 1) __threadfence_system(); else __threadfence();
             const uint64_t epoch = *step + 1;
-            for (int p = 0; p < G; ++p)
-                ptx::st_release_sys(reinterpret_cast<uint64_t*>(peers[p] + sym.gflags) + rank, epoch);
+            for (int p = 0; p < G; ++p)  // .gpu scope on one GPU (a .sys release costs ~4 us)
+                ptx::flag_publish(reinterpret_cast<uint64_t*>(peers[p] + sym.gflags) + rank, epoch, G > 1);
             *done_ctr = 0;
         }
     }
@@ -383,7 +383,7 @@ __global__ void gather_wait_kernel(uint8_t* own_sym, Symm sym, int G, uint64_t* 
     if ((int)threadIdx.x < G) {
         const uint64_t* f = reinterpret_cast<const uint64_t*>(own_sym + sym.gflags) + threadIdx.x;
         ptx::SpinGuard g;
-        while (ptx::ld_acquire_sys(f) < epoch) g.step(err, ERR_TIMEOUT_GATHER);
+        while (ptx::flag_read(f, G > 1) < epoch) g.step(err, ERR_TIMEOUT_GATHER);
     }
     __syncthreads();
     if (threadIdx.x == 0) *step = epoch;
