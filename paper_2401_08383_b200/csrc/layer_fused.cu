@@ -335,7 +335,10 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
             const uint64_t qc = ptx::ld_relaxed_u64(a.step, false) * (uint64_t)a.L + (uint64_t)a.layer;
             if (tid < (int)gridDim.x) {
                 ptx::SpinGuard g;
-                while (ptx::ld_relaxed_u64(a.fin_gen + tid, false) < qc) g.step(a.err, 115);
+                // equality, not >=: a stale generation from an earlier run of
+                // the same layers (a phased step left incomplete) must not
+                // release this layer before the previous kernel has finished
+                while (ptx::ld_relaxed_u64(a.fin_gen + tid, false) != qc) g.step(a.err, 115);
                 (void)ptx::ld_acquire_gpu_u64(a.fin_gen + tid);
             }
             __syncthreads();
