@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-parity", action="store_true", help="skip the per-placement checked step")
     p.add_argument("--no-fp32", action="store_true", help="skip the fp32-mode sub-measurement")
+    p.add_argument("--no-config-sweep", action="store_true",
+                   help="skip the BASELINE configs[0]/[2]/[3] throughput sweep")
     p.add_argument("--no-configs4", action="store_true",
                    help="skip the BASELINE configs[4] long-context sub-measurement")
     p.add_argument("--no-routing-kernels", action="store_true",
@@ -488,6 +490,18 @@ def main():
         log(f"[bench] configs4: {json.dumps(configs4)[:300]}")
         barrier()
 
+    # ---- BASELINE configs[0], configs[2] and the configs[3] decode-batch
+    # sweep at this N (throughput lines; their parity is the test suite's:
+    # tests/test_gpu_model.py, tests/test_multi_gpu_shapes.py)
+    sweep = None
+    if not a.no_config_sweep:
+        try:
+            sweep = measure_config_sweep(a, n, rank, stream, barrier, allmax, hbm_peak)
+        except Exception as e:  # informational; never blocks the headline line
+            sweep = {"error": f"{type(e).__name__}: {e}"}
+        log(f"[bench] config sweep: {json.dumps(sweep)[:300]}")
+        barrier()
+
     # ---- CPU baseline (rank 0, at every N; the other ranks wait): whole
     # decode steps of the same G*B tokens on the host cores, nothing
     # extrapolated; the reference's own CPU routing bookkeeping included
@@ -546,6 +560,7 @@ def main():
         "expert_migration": migration,
         "fp32_mode": fp32,
         "configs4_long_context": configs4,
+        "config_sweep": sweep,
         "e2e": {"value": a.batch * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "roofline": {"kernel": ("layer_fused_kernel (gate+dispatch+GEMM1+GEMM2 per layer, tcgen05)"
@@ -575,6 +590,77 @@ def main():
     model.close()
     if n > 1:
         dist.destroy_process_group()
+
+
+def measure_config_sweep(a, n, rank, stream, barrier, allmax, hbm_peak):
+    """Graph-replayed decode steps (CUDA events, max over ranks) of the other
+    BASELINE configs at this N, contiguous placement, synthetic tokens:
+    configs[0] tiny (E=8, 4 layers, d=512, 256 tokens over the N GPUs),
+    configs[2] (E=16, 24 layers, d=1024, 64 tokens/GPU), configs[3] (1.3B:
+    E=32, 24 layers, d=2048, d_ffn=8192) at decode batches 16/64/256/512 per
+    GPU. bytes = weights of the active local experts per layer (from the
+    recorded routes of the timed step) + token rows; frac against the
+    measured HBM peak."""
+    import torch
+    from paper_2401_08383_b200 import dist as xd, placement as pl
+    from paper_2401_08383_b200.affinity import Topology
+    from paper_2401_08383_b200.model import MoeModel, MoeModelConfig
+    dev = torch.device("cuda", torch.cuda.current_device())
+    steps = max(3, min(a.steps, 10))
+
+    def one(name, E, L, d, dff, B):
+        if E % n or B < 1:
+            return {"config": name, "skipped": f"{E} experts / {B} tokens over {n} GPUs"}
+        assign = pl.contiguous_placement(E, L, Topology(1, n))
+        cfg = MoeModelConfig(num_experts=E, num_layers=L, d_model=d, d_ffn=dff, tokens_per_gpu=B, world_size=n,
+                             rank=rank, seed=99 + E + B, gate_affinity=a.gate_affinity)
+        m = MoeModel(cfg, assign)
+        if n > 1:
+            m.connect(xd.exchange_handles(m.ipc_handle()))
+        g = torch.Generator(device="cpu").manual_seed(4000 + rank + B)
+        x = torch.randn(B, d, generator=g).to(torch.bfloat16).to(dev)
+        m.capture(x, stream)
+        for _ in range(3):
+            m.replay(stream)
+        stream.synchronize()
+        m.check()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            m.replay(stream)
+        e1.record(stream)
+        stream.synchronize()
+        m.check()
+        ms = allmax(e0.elapsed_time(e1)) / steps
+        routes = m.routes()
+        e_loc = E // n
+        active = 0
+        for j in range(L):
+            r = routes[:, j]
+            r = r[r >= 0]
+            active += len({int(e) for e in r.tolist() if int(assign[j][e]) == rank})
+        wbytes = active * (4 * d * dff + 2 * (d + dff)) + L * B * (2 * d + 4 * dff + 4 * d)
+        bw = allmax(wbytes / (ms * 1e-3) / 1e9)
+        desc = m.describe()
+        lk = desc.get("layer_kernel", {})
+        m.close()
+        torch.cuda.empty_cache()
+        return {"config": name, "E": E, "L": L, "d_model": d, "d_ffn": dff, "tokens_per_gpu": B,
+                "experts_per_gpu": e_loc, "value": B * n / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms,
+                "steps": steps, "path": desc.get("path") + (" dense" if lk.get("dense") else "") +
+                (" virtual-slots" if lk.get("virtual_expert_slots") else ""),
+                "hbm_gbs_max_rank": bw, "hbm_frac": bw / hbm_peak}
+
+    out = [one("configs[0]", 8, 4, 512, 2048, 256 // n)]
+    out.append(one("configs[2]", 16, a.layers, 1024, 4096, 64))
+    for B in (16, 64, 256, 512):
+        out.append(one("configs[3]", 32, a.layers, 2048, 8192, B))
+    return {"lines": out, "placement": "contiguous", "data": "synthetic tokens, random-init weights",
+            "timing": f"graph replay, {steps} steps after 3 warm-up, CUDA events, max over ranks",
+            "parity": "tests/test_gpu_model.py (configs[0], configs[3] shapes), tests/test_multi_gpu_shapes.py "
+                      "(configs[2], configs[3] at G=2/4); every run here checks the device error word"}
 
 
 def measure_configs4(a, n, rank, stream, barrier, allmax, allsum_i64, check_step, hbm_peak):
