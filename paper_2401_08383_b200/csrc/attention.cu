@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kThreads) coherent_attn_kernel(
     const int32_t* __restrict__ ctx, const __nv_bfloat16* __restrict__ k,
     const __nv_bfloat16* __restrict__ v, int32_t H, int32_t C, int32_t chunk, float scale_log2,
     float* __restrict__ ws, __nv_bfloat16* __restrict__ out, int32_t seq_stride,
-    const int32_t* __restrict__ n_dev) {
+    const int32_t* __restrict__ n_dev, int32_t len_add) {
     constexpr int LPK = Dh / 8;                  // lanes per key
     constexpr int GROUPS = kThreads / LPK;       // keys in flight per CTA step
     const int h = blockIdx.x, n = blockIdx.y, split = blockIdx.z, splits = gridDim.z;
@@ -74,7 +74,9 @@ __global__ void __launch_bounds__(kThreads) coherent_attn_kernel(
     // on the device (uniform per CTA: every split of token n leaves together)
     if (n_dev && n >= *n_dev) return;
     const int s = seq[(size_t)n * seq_stride];
-    const int len = ctx[s];
+    // len_add = 1: the step's own K/V row was stored at position ctx[s] by the
+    // projection (folded append) and the length advances after this kernel
+    const int len = min(ctx[s] + len_add, C);
     const int lane_in = threadIdx.x % LPK, grp = threadIdx.x / LPK;
     const int k_begin = split * chunk;
     const int k_end = min(len, k_begin + chunk);
@@ -245,7 +247,8 @@ int64_t attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh, int32_t C, i
 exf_status launch_attention_model(const void* q, const int32_t* seq, int32_t seq_stride,
                                   const int32_t* n_dev, int64_t n_max, const int32_t* ctx,
                                   const void* k, const void* v, int32_t H, int32_t Dh, int32_t C,
-                                  float scale, void* ws, void* out, int64_t n_plan, cudaStream_t st) {
+                                  float scale, void* ws, void* out, int64_t n_plan, int32_t len_add,
+                                  cudaStream_t st) {
     if (n_max <= 0) return EXF_OK;
     if (Dh != 64 && Dh != 128) return invalid("attention: head dim must be 64 or 128");
     const int splits = attn_splits(std::max<int64_t>(1, std::min(n_plan, n_max)), H, Dh, C);
@@ -261,10 +264,10 @@ exf_status launch_attention_model(const void* q, const int32_t* seq, int32_t seq
     auto w = static_cast<float*>(ws);
     if (Dh == 64)
         coherent_attn_kernel<64><<<grid, kThreads, 0, st>>>(qq, seq, ctx, kk, vv, H, C, chunk, scale_log2, w, oo,
-                                                            seq_stride, n_dev);
+                                                            seq_stride, n_dev, len_add);
     else
         coherent_attn_kernel<128><<<grid, kThreads, 0, st>>>(qq, seq, ctx, kk, vv, H, C, chunk, scale_log2, w,
-                                                             oo, seq_stride, n_dev);
+                                                             oo, seq_stride, n_dev, len_add);
     EXF_LAUNCH_CHECK("attention_model");
     return EXF_OK;
 }
@@ -325,10 +328,10 @@ extern "C" exf_status exf_coherent_attention(const void* d_q, const int32_t* d_s
     }
     if (Dh == 64) {
         coherent_attn_kernel<64><<<grid, kThreads, 0, st>>>(q, d_seq, d_ctx_len, k, v, H, C, chunk,
-                                                            scale_log2, ws, o, 1, nullptr);
+                                                            scale_log2, ws, o, 1, nullptr, 0);
     } else {
         coherent_attn_kernel<128><<<grid, kThreads, 0, st>>>(q, d_seq, d_ctx_len, k, v, H, C,
-                                                             chunk, scale_log2, ws, o, 1, nullptr);
+                                                             chunk, scale_log2, ws, o, 1, nullptr, 0);
     }
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_status(err, "coherent_attention launch");

@@ -117,6 +117,19 @@ dense_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant
     ptx::pdl_wait();
     ptx::pdl_trigger();
     const int n = *a.n_dev;
+    if (MODE == 1 && a.replicas > 0 && blockIdx.x == 0) {
+        // folded K/V append, second half: the attention (previous kernel) has
+        // read every length; advance each resident token's sequence in every
+        // replica (rows were stored two kernels earlier, in stream order)
+        for (int t = tid; t < n; t += kDThreads) {
+            const int sq = a.seq[(int64_t)t * 2];
+            if (a.lens[0][sq] >= a.kv_C) {
+                if (a.overflow) atomicAdd(a.overflow, 1);
+                continue;
+            }
+            for (int r = 0; r < a.replicas; ++r) a.lens[r][sq] += 1;
+        }
+    }
     const int chunks = max(1, (n + NT - 1) / NT);  // >= 1: the prefetched stages are consumed
 
     if (warp == 0) {
@@ -207,8 +220,21 @@ dense_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant
                 if (MODE == 0) {
                     // q | k | v column ranges of the fused projection
                     const int which = m_glob / a.d, col = m_glob - which * a.d;
-                    __nv_bfloat16* dst = which == 0 ? a.out[0] : (which == 1 ? a.out[1] : a.out[2]);
-                    dst[row * a.d + col] = __float2bfloat16(acc);
+                    if (which > 0 && a.replicas > 0) {
+                        // k / v row straight into every replica of the context
+                        // cache at the sequence's current length
+                        const int sq = a.seq[row * 2];
+                        const int pos = a.lens[0][sq];
+                        if (pos < a.kv_C) {
+                            const int h = col / a.kv_Dh, dc = col - h * a.kv_Dh;
+                            const int64_t off = (((int64_t)sq * a.kv_H + h) * a.kv_C + pos) * a.kv_Dh + dc;
+                            const __nv_bfloat16 v = __float2bfloat16(acc);
+                            for (int r = 0; r < a.replicas; ++r) (which == 1 ? a.kc[r] : a.vc[r])[off] = v;
+                        }
+                    } else {
+                        __nv_bfloat16* dst = which == 0 ? a.out[0] : (which == 1 ? a.out[1] : a.out[2]);
+                        dst[row * a.d + col] = __float2bfloat16(acc);
+                    }
                 } else {
                     __nv_bfloat16* x = a.out[0] + row * a.d + m_glob;
                     *x = __float2bfloat16(__bfloat162float(*x) + acc);

@@ -47,7 +47,8 @@ exf_status launch_kv_append_model(const void* k_new, const void* v_new, int64_t 
 exf_status launch_attention_model(const void* q, const int32_t* seq, int32_t seq_stride,
                                   const int32_t* n_dev, int64_t n_max, const int32_t* ctx,
                                   const void* k, const void* v, int32_t H, int32_t Dh, int32_t C,
-                                  float scale, void* ws, void* out, int64_t n_plan, cudaStream_t st);
+                                  float scale, void* ws, void* out, int64_t n_plan, int32_t len_add,
+                                  cudaStream_t st);
 int64_t attention_workspace_bytes(int64_t N, int32_t H, int32_t Dh, int32_t C, int64_t n_plan);
 exf_status launch_gather_wait(uint8_t* own_sym, const Symm& sym, int G, uint64_t* step,
                               int32_t* err, cudaStream_t s);
@@ -188,6 +189,7 @@ struct exf_model {
     uint64_t* fin_gen = nullptr;            // fused kernel: per-CTA exit generation (FusedArgs.fin_gen)
     bool in_step = false;                   // eager run_step in progress: chained layer kernels
     bool chain_ok = true;                   // EXF_CHAIN=0 disables chaining
+    bool kv_fused = true;                   // K/V append folded into the projections (EXF_KV_FUSED=0: own kernel)
     int f_active_hint = 0;                  // virtual slots scheduled as their own layer
     int xpre = 0;                           // dense: pieces L2-prefetched before the PDL wait
     int f_ctas = 148, f_tpc = 8, f_max_chunks = 1, f_nmax = 32, f_max_contrib = 1, f_max_pieces = 0;
@@ -557,21 +559,8 @@ void capture_trace(cudaStream_t s, const char* what, int j) {
 // local replica -> x += attn Wo^T + b (in place in the layer's input rows)
 exf_status run_attention(exf_model* m, int j, cudaStream_t s) {
     const auto& c = m->cfg;
-    const int d = c.d_model, G = c.world_size, L = c.num_layers, C = m->C;
+    const int d = c.d_model, G = c.world_size, C = m->C;
     const int32_t* n_dev = m->n_res + (j & 1);
-    DenseArgs qa{};
-    qa.M = 3 * d;
-    qa.K = d;
-    qa.d = d;
-    qa.ksplit = m->ks_qkv;
-    qa.n_dev = n_dev;
-    qa.bias = m->bqkv + (int64_t)j * 3 * d;
-    qa.out[0] = m->qb;
-    qa.out[1] = m->kb;
-    qa.out[2] = m->vb;
-    qa.err = m->err;
-    EXF_TRY(launch_dense_gemm(m->tm_qkv[j], m->tm_res[j & 1], qa, m->at_nt, 0, s));
-    capture_trace(s, "qkv", j);
     const int64_t layer_off = (int64_t)j * C * m->nh * m->Cctx * m->Dh * 2;
     void* kc[8];
     void* vc[8];
@@ -584,11 +573,45 @@ exf_status run_attention(exf_model* m, int j, cudaStream_t s) {
         lc[r] = reinterpret_cast<int32_t*>(base + m->sym.kv_len) + (int64_t)j * C;
     }
     const int32_t* seq = reinterpret_cast<const int32_t*>(m->res_meta[j & 1]);  // ResMeta.token
-    EXF_TRY(launch_kv_append_model(m->kb, m->vb, (int64_t)d / 8, seq, 2, n_dev, C, m->nh, m->Dh, m->Cctx, G, kc,
-                                   vc, lc, m->kv_overflow, s));
-    capture_trace(s, "kv_append", j);
+    // K/V append folded into the projections (default): the QKV epilogue stores
+    // k / v rows into every replica at the current length, the attention reads
+    // one row past it, the O projection advances the lengths -- one launch
+    // fewer per layer than the separate kv_append kernel (EXF_KV_FUSED=0)
+    auto kv_into = [&](DenseArgs& a) {
+        a.replicas = G;
+        a.kv_H = m->nh;
+        a.kv_Dh = m->Dh;
+        a.kv_C = m->Cctx;
+        a.seq = seq;
+        for (int r = 0; r < G; ++r) {
+            a.kc[r] = static_cast<__nv_bfloat16*>(kc[r]);
+            a.vc[r] = static_cast<__nv_bfloat16*>(vc[r]);
+            a.lens[r] = lc[r];
+        }
+        a.overflow = m->kv_overflow;
+    };
+    DenseArgs qa{};
+    qa.M = 3 * d;
+    qa.K = d;
+    qa.d = d;
+    qa.ksplit = m->ks_qkv;
+    qa.n_dev = n_dev;
+    qa.bias = m->bqkv + (int64_t)j * 3 * d;
+    qa.out[0] = m->qb;
+    qa.out[1] = m->kb;
+    qa.out[2] = m->vb;
+    qa.err = m->err;
+    if (m->kv_fused) kv_into(qa);
+    EXF_TRY(launch_dense_gemm(m->tm_qkv[j], m->tm_res[j & 1], qa, m->at_nt, 0, s));
+    capture_trace(s, "qkv", j);
+    if (!m->kv_fused) {
+        EXF_TRY(launch_kv_append_model(m->kb, m->vb, (int64_t)d / 8, seq, 2, n_dev, C, m->nh, m->Dh, m->Cctx, G,
+                                       kc, vc, lc, m->kv_overflow, s));
+        capture_trace(s, "kv_append", j);
+    }
     EXF_TRY(launch_attention_model(m->qb, seq, 2, n_dev, C, lc[0], kc[0], vc[0], m->nh, m->Dh, m->Cctx,
-                                   1.0f / std::sqrt((float)m->Dh), m->attn_ws, m->ab, c.tokens_per_gpu, s));
+                                   1.0f / std::sqrt((float)m->Dh), m->attn_ws, m->ab, c.tokens_per_gpu,
+                                   m->kv_fused ? 1 : 0, s));
     capture_trace(s, "attention", j);
     DenseArgs oa{};
     oa.M = d;
@@ -599,7 +622,7 @@ exf_status run_attention(exf_model* m, int j, cudaStream_t s) {
     oa.bias = m->bo + (int64_t)j * d;
     oa.out[0] = m->res_x[j & 1];
     oa.err = m->err;
-    (void)L;
+    if (m->kv_fused) kv_into(oa);
     return launch_dense_gemm(m->tm_o[j], m->tm_attn, oa, m->at_nt, 1, s);
 }
 
@@ -856,6 +879,7 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         EXF_M(dalloc(&m->vb, (size_t)C * d));
         EXF_M(dalloc(&m->ab, (size_t)C * d));
         EXF_M(dalloc(&m->kv_overflow, 1));
+        if (const char* env = std::getenv("EXF_KV_FUSED")) m->kv_fused = std::atoi(env) != 0;
         m->tm_qkv.resize(L);
         m->tm_o.resize(L);
         m->at_nt = C <= 64 ? 64 : 128;
@@ -1237,9 +1261,10 @@ exf_status exf_model_replay(exf_model* m, exf_stream_t stream) {
 
 int32_t exf_model_launches_per_step(exf_model* m) {
     if (!m) return 0;
-    // begin, L x ([qkv + kv append + attention + o-proj] + fused layer | gate_dispatch + GEMM1 +
+    // begin, L x ([qkv (+ kv append unless folded) + attention + o-proj] + fused layer | gate_dispatch + GEMM1 +
     // GEMM2) [+ combine send + wait], gather send + wait
-    const int per_layer = (m->nh > 0 ? 4 : 0) + (m->fused ? 1 : 3) + (m->cfg.ep_mode == EXF_EP_VANILLA ? 2 : 0);
+    const int per_layer = (m->nh > 0 ? (m->kv_fused ? 3 : 4) : 0) + (m->fused ? 1 : 3) +
+                          (m->cfg.ep_mode == EXF_EP_VANILLA ? 2 : 0);
     return 1 + per_layer * m->cfg.num_layers + 2;
 }
 

@@ -111,6 +111,16 @@ struct DenseArgs {
     const __nv_bfloat16* bias;     // [M]
     __nv_bfloat16* out[3];         // MODE 0: q, k, v [C][d]; MODE 1: out[0] = x [C][d] (in place)
     int32_t* err;
+    // K/V append folded into the projection (replicas > 0): MODE 0 stores each
+    // resident token's k and v rows at position lens[0][seq] of every replica
+    // (instead of out[1] / out[2]); MODE 1 then advances every replica's length
+    // of each resident token's sequence (after the attention has read it)
+    int32_t replicas, kv_H, kv_Dh, kv_C;
+    const int32_t* seq;            // resident row -> sequence (ResMeta.token, stride 2)
+    __nv_bfloat16* kc[8];
+    __nv_bfloat16* vc[8];
+    int32_t* lens[8];              // per replica [S] lengths of this layer; [0] = local
+    int32_t* overflow;
 };
 
 // Arguments of the setup AllGather of the replicated context (attn_block.cu).

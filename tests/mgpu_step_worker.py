@@ -25,6 +25,8 @@ def main():
     p.add_argument("--batch", type=int, default=64)
     p.add_argument("--dtype", choices=["bf16", "f32"], default="bf16")
     p.add_argument("--rows", type=int, default=3, help="sampled output rows per layer per rank")
+    p.add_argument("--attn-heads", type=int, default=0, help="attention block per layer (0: MoE stack only)")
+    p.add_argument("--context", type=int, default=512, help="context capacity per sequence (attention)")
     a = p.parse_args()
     import torch
     import torch.distributed as dist
@@ -41,9 +43,16 @@ def main():
     f32 = a.dtype == "f32"
     cfg = MoeModelConfig(num_experts=E, num_layers=L, d_model=a.d_model, d_ffn=a.d_ffn,
                          tokens_per_gpu=a.batch, world_size=G, rank=rank, seed=2024,
-                         gate_affinity=0.6, dtype=DTYPE_F32 if f32 else DTYPE_BF16)
+                         gate_affinity=0.6, dtype=DTYPE_F32 if f32 else DTYPE_BF16,
+                         attn_heads=a.attn_heads, context_len=a.context if a.attn_heads else 0,
+                         context_prefix=a.context // 2 if a.attn_heads else 0)
     m = MoeModel(cfg, assign)
     m.connect(xd.exchange_handles(m.ipc_handle()))
+    if a.attn_heads:
+        # setup AllGather across the GPUs: every replica holds every prompt
+        m.context_setup(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        dist.barrier()
     g = torch.Generator().manual_seed(500 + rank)
     x = torch.randn(a.batch, a.d_model, generator=g)
     x = (x if f32 else x.to(torch.bfloat16)).cuda()
@@ -56,6 +65,18 @@ def main():
     res = check_step(m, x, assign, rows_per_layer=a.rows)
     # the eager step (layer kernels chained on exit generations, FusedArgs.chain)
     # and a graph replay (griddepcontrol.wait between layers) give the same bits
+    # (without attention: with it every step appends a context row)
+    if a.attn_heads:
+        path = m.describe().get("path")
+        if rank == 0:
+            tag = (f"G={G} E={E} L={L} d={a.d_model} B={a.batch} attention heads={a.attn_heads} path={path} "
+                   f"max rel err {res['max_rel_err_sampled']:.2e} attention {res['attention_max_rel_err_sampled']:.2e}")
+            print(f"[mgpu-shape] {tag} {'OK' if res['parity'] == 'ok' else 'FAIL ' + str(res['failures'])}",
+                  flush=True)
+        dist.barrier()
+        m.close()
+        dist.destroy_process_group()
+        sys.exit(0 if res["parity"] == "ok" else 1)
     m.step(x, s)
     s.synchronize()
     eager = m.output().clone()
