@@ -490,6 +490,13 @@ def main():
         log(f"[bench] configs4: {json.dumps(configs4)[:300]}")
         barrier()
 
+    # ---- NVLink: measured peer-copy bandwidth (rank 0, copy engines, one
+    # direction) next to the bytes the decode step moves over it
+    nvlink = None
+    if n > 1:
+        nvlink = measure_nvlink(a, n, rank, results["affinity"], barrier)
+        log(f"[bench] nvlink: {json.dumps(nvlink)[:300]}")
+
     # ---- BASELINE configs[0], configs[2] and the configs[3] decode-batch
     # sweep at this N (throughput lines; their parity is the test suite's:
     # tests/test_gpu_model.py, tests/test_multi_gpu_shapes.py)
@@ -560,6 +567,7 @@ def main():
         "expert_migration": migration,
         "fp32_mode": fp32,
         "configs4_long_context": configs4,
+        "nvlink": nvlink,
         "config_sweep": sweep,
         "e2e": {"value": a.batch * n / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
@@ -590,6 +598,48 @@ def main():
     model.close()
     if n > 1:
         dist.destroy_process_group()
+
+
+def measure_nvlink(a, n, rank, aff, barrier):
+    """NVLink at N > 1. Peak: rank 0 copies 256 MB from its GPU to the next
+    GPU (cudaMemcpyPeer over the copy engines; NCCL-free), CUDA events, best of
+    5. Step bytes (whole job): the dispatch moves each routed token-layer's
+    row (2d bytes) + its 16-byte metadata + the per-slot route flags (8 bytes
+    per (slot, destination)), the context AllGather every token's final row to
+    the G-1 other GPUs. ncu's nvlink counters are not readable on this pool
+    (profiles/r01: ctc__ metrics unavailable), so this is the accounting
+    estimate; the exchange is latency-bound."""
+    import torch
+    out = None
+    if rank == 0 and torch.cuda.device_count() >= 2:
+        dev0 = torch.cuda.current_device()
+        dev1 = (dev0 + 1) % torch.cuda.device_count()
+        nbytes = 256 << 20
+        src = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{dev0}")
+        dst = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{dev1}")
+        best = 0.0
+        for _ in range(6):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            e1.synchronize()
+            best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        del src, dst
+        torch.cuda.empty_cache()
+        tokens = a.batch * n
+        row = 2 * a.d_model
+        dispatch = aff["routed_fraction"] * tokens * a.layers * (row + 16) + tokens * n * a.layers * 8
+        gather = tokens * (n - 1) * row
+        ms = aff["ms_per_step"]
+        per_gpu = (dispatch + gather) / n / (ms * 1e-3) / 1e9
+        out = {"p2p_copy_gbs_one_direction": best, "peak_source": "cudaMemcpyPeer GPU0 -> GPU1, 256 MB, best of 6",
+               "dispatch_bytes_per_step": dispatch, "allgather_bytes_per_step": gather,
+               "achieved_gbs_per_gpu_over_step": per_gpu, "frac": per_gpu / best if best else None,
+               "note": "bytes counted from the routed fraction of the timed affinity run; the exchange "
+                       "is latency-bound (route-flag release ~4 us per layer), not bandwidth-bound"}
+    barrier()
+    return out
 
 
 def measure_config_sweep(a, n, rank, stream, barrier, allmax, hbm_peak):
