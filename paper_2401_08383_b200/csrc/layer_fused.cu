@@ -51,7 +51,10 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxLocal = 64;
 constexpr int kMaxKeys = 64;
-constexpr int kMaxList = 4096;  // G * C slots the dispatch path can route per layer
+// G * C route slots the dispatch path takes per layer (int16 indices): 8192
+// with the 128-token tile variant, 4096 otherwise (the 32/64-token variants'
+// rings leave no room for a longer list in 227 KB)
+constexpr int kMaxList = 8192;
 
 __device__ __forceinline__ void unpack8(const int4& v, float (&f)[8]) {
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
@@ -140,7 +143,8 @@ struct Smem {
     // dispatch path: canonical (slot, source, order) list of received slots,
     // entry = source * C + t (t = the token's resident index at its source)
     static constexpr int kOffList = kOffTab + kMaxLocal * kTabInts * 4;
-    static constexpr int kOffBar = kOffList + kMaxList * 2;
+    static constexpr int kList = NMAX >= 128 ? kMaxList : kMaxList / 2;
+    static constexpr int kOffBar = kOffList + kList * 2;
     // fullA[S], emptyA[S], fullB[BST], emptyB[BST], tmem_full[NBUF<=4],
     // tmem_empty[NBUF<=4], wg_bar
     static constexpr int kOffMisc = kOffBar + (2 * STAGES + 2 * BST + 10) * 8;
@@ -579,7 +583,7 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // per-warp key counters of the route-flag scan below (token-row ring, free
     // since the gate); the barrier that orders the rows before the flags
     // orders these stores before the scan
-    int32_t* s_wcnt = reinterpret_cast<int32_t*>(smem + S::kOffB + kMaxList);  // [kWarps][kMaxKeys]
+    int32_t* s_wcnt = reinterpret_cast<int32_t*>(smem + S::kOffB + S::kList);  // [kWarps][kMaxKeys]
     for (int x = tid; x < kWarps * kMaxKeys; x += kThreads) s_wcnt[x] = 0;
     __syncthreads();  // rows and metas stored before any flag (release below)
     mark3(5);
@@ -607,45 +611,47 @@ layer_fused_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_consta
     // per flag.
     const int K = a.G * a.C;
     const int Kw = ((K + kWarps - 1) / kWarps + 31) & ~31;
-    const int nr = Kw >> 5;  // rounds per warp (<= kMaxList / kWarps / 32 = 16)
-    constexpr int kMaxRounds = kMaxList / kWarps / 32;
+    const int nr = Kw >> 5;  // rounds per warp (<= S::kList / kWarps / 32 <= 32)
+    constexpr int kBatch = 16;  // rounds whose flag loads are in flight together
     uint8_t* s_kslot = smem + S::kOffB;
-    int16_t* s_rank = reinterpret_cast<int16_t*>(smem + S::kOffB + kMaxList + kWarps * kMaxKeys * 4);
+    int16_t* s_rank = reinterpret_cast<int16_t*>(smem + S::kOffB + S::kList + kWarps * kMaxKeys * 4);
     int16_t* s_list = reinterpret_cast<int16_t*>(smem + S::kOffList);
     {
         const uint64_t* f = reinterpret_cast<const uint64_t*>(a.own_sym + a.sym.cflags) + (int64_t)parity * K;
         const int kb = warp * Kw + lane;
-        uint64_t v[kMaxRounds];
-#pragma unroll
-        for (int r = 0; r < kMaxRounds; ++r)
-            if (r < nr && kb + r * 32 < K) v[r] = ptx::ld_relaxed_u64(f + kb + r * 32, sys);
         int32_t* wc = s_wcnt + warp * kMaxKeys;
+        for (int r0 = 0; r0 < nr; r0 += kBatch) {  // warp-uniform
+            uint64_t v[kBatch];
 #pragma unroll
-        for (int r = 0; r < kMaxRounds; ++r) {
-            if (r >= nr) break;  // warp-uniform
-            const int k = kb + r * 32;
-            int key = -1;
-            if (k < K) {
-                ptx::SpinGuard g;
-                while ((v[r] >> 40) != e24) {
-                    g.step(a.err, 112);
-                    v[r] = ptx::ld_relaxed_u64(f + k, sys);
+            for (int u = 0; u < kBatch; ++u)
+                if (r0 + u < nr && kb + (r0 + u) * 32 < K) v[u] = ptx::ld_relaxed_u64(f + kb + (r0 + u) * 32, sys);
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                if (r0 + u >= nr) break;  // warp-uniform
+                const int k = kb + (r0 + u) * 32;
+                int key = -1;
+                if (k < K) {
+                    ptx::SpinGuard g;
+                    while ((v[u] >> 40) != e24) {
+                        g.step(a.err, 112);
+                        v[u] = ptx::ld_relaxed_u64(f + k, sys);
+                    }
+                    // acquire once, on the flag itself (orders this slot's row +
+                    // meta; the barrier below extends it to the CTA). One fence
+                    // per thread instead cost ~2.4 us before the next access.
+                    (void)ptx::flag_read(f + k, sys);
+                    const int sl = (int)((v[u] >> 32) & 0xFF);
+                    s_kslot[k] = (uint8_t)sl;
+                    key = sl != 0xFF ? sl : -1;
                 }
-                // acquire once, on the flag itself (orders this slot's row +
-                // meta; the barrier below extends it to the CTA). One fence per
-                // thread instead cost ~2.4 us before the next memory access.
-                (void)ptx::flag_read(f + k, sys);
-                const int sl = (int)((v[r] >> 32) & 0xFF);
-                s_kslot[k] = (uint8_t)sl;
-                key = sl != 0xFF ? sl : -1;
+                const uint32_t peers = __match_any_sync(0xffffffffu, key);
+                const int rk = __popc(peers & lanemask_lt());
+                const int base = key >= 0 ? wc[key] : 0;
+                __syncwarp();
+                if (key >= 0 && rk == 0) wc[key] = base + __popc(peers);
+                __syncwarp();
+                if (k < K) s_rank[k] = (int16_t)(base + rk);
             }
-            const uint32_t peers = __match_any_sync(0xffffffffu, key);
-            const int rk = __popc(peers & lanemask_lt());
-            const int base = key >= 0 ? wc[key] : 0;
-            __syncwarp();
-            if (key >= 0 && rk == 0) wc[key] = base + __popc(peers);
-            __syncwarp();
-            if (k < K) s_rank[k] = (int16_t)(base + rk);
         }
     }
     __syncthreads();

@@ -806,8 +806,9 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         // products then spread over 8 warps of many CTAs
         m->f_tpc = std::max(1, (C + m->f_ctas - 1) / m->f_ctas);
         // two-kernel path instead when the fused kernel's limits are exceeded
-        // (G*C <= 4096 routed slots per layer: layer_fused.cu kMaxList)
-        if (m->f_tpc > 32 || d > 2048 || E > 64 || (int64_t)c.world_size * C > 4096) m->fused = false;
+        // (G*C <= 8192 routed slots per layer with the 128-token tile, 4096
+        // with the smaller ones: layer_fused.cu Smem::kList, checked below)
+        if (m->f_tpc > 32 || d > 2048 || E > 64 || (int64_t)c.world_size * C > 8192) m->fused = false;
         // single GPU: every expert is local, so the layer runs dense over all
         // resident tokens and the token phase leaves the GEMMs' critical path
         // (measured at N=1, tokens 64: dense wins while a layer's weights are
@@ -835,6 +836,7 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         const int tok = m->dense ? C : m->nmax;
         const int nmax_f = tok <= 32 ? 32 : (tok <= 64 ? 64 : 128);
         m->f_nmax = nmax_f;
+        if (!m->dense && (int64_t)c.world_size * C > (nmax_f >= 128 ? 8192 : 4096)) m->fused = false;
         EXF_M(dalloc(&m->H, (size_t)C * f * ew));
         std::vector<Piece> pieces;
         std::vector<int32_t> off;

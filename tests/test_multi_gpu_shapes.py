@@ -4,7 +4,7 @@ kernels exchanging tokens over NVLink peer memory; every rank checks its own
 part of one full decode step against the CPU oracle (tests/step_check.py):
   configs[1]  E=8,  d=1024, d_ffn=4096, B=64     at G=2 and G=4 (fused path)
   configs[2]  E=16, d=1024, d_ffn=4096, B=64     at G=2 and G=4
-  configs[3]  E=32, d=2048, d_ffn=8192, B=64/256 at G=4
+  configs[3]  E=32, d=2048, d_ffn=8192, B=64/256/512 at G=4
   fp32 mode   configs[1] shape                   at G=2 (<= 1e-5)
   attention   configs[1] layer + 16-head attention block at G=2, configs[4]
               (E=64, 8 sequences/GPU) at G=4: setup AllGather across GPUs,
@@ -29,6 +29,8 @@ CASES = [
     (4, 16, 1024, 4096, 64, "bf16", 29714),
     (4, 32, 2048, 8192, 64, "bf16", 29715),
     (4, 32, 2048, 8192, 256, "bf16", 29716),
+    # G*C = 8192 route slots: the largest the fused dispatch path takes
+    (4, 32, 2048, 8192, 512, "bf16", 29720),
     (2, 8, 1024, 4096, 64, "f32", 29717),
 ]
 ATTN_CASES = [
