@@ -834,7 +834,10 @@ exf_status exf_model_create(const exf_model_config* config, const int32_t* h_ass
         m->remap = !m->dense && c.tokens_per_gpu < 2 * m->E_loc ? 1 : 0;
         if (const char* env = std::getenv("EXF_REMAP")) m->remap = !m->dense && std::atoi(env) != 0;
         const int tok = m->dense ? C : m->nmax;
-        const int nmax_f = tok <= 32 ? 32 : (tok <= 64 ? 64 : 128);
+        int nmax_f = tok <= 32 ? 32 : (tok <= 64 ? 64 : 128);
+        // more than 4096 route slots: only the 128-token tile variant has room
+        // for the longer canonical list
+        if (!m->dense && (int64_t)c.world_size * C > 4096) nmax_f = 128;
         m->f_nmax = nmax_f;
         if (!m->dense && (int64_t)c.world_size * C > (nmax_f >= 128 ? 8192 : 4096)) m->fused = false;
         EXF_M(dalloc(&m->H, (size_t)C * f * ew));

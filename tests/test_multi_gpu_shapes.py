@@ -31,6 +31,8 @@ CASES = [
     (4, 32, 2048, 8192, 256, "bf16", 29716),
     # G*C = 8192 route slots: the largest the fused dispatch path takes
     (4, 32, 2048, 8192, 512, "bf16", 29720),
+    # 5120 route slots with a 64-token natural tile: the 128-token variant is forced
+    (4, 64, 1024, 4096, 320, "bf16", 29721),
     (2, 8, 1024, 4096, 64, "f32", 29717),
 ]
 ATTN_CASES = [
