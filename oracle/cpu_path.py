@@ -98,6 +98,22 @@ def time_cpu_path(E, L, d, dff, tokens, G, assign, steps=None, seed=0, min_secon
     max_steps). Returns (tokens_per_s, seconds measured, sample str, threads,
     steps timed)."""
     threads = os.cpu_count() or 1
+    # BLAS on every host core even under torchrun, which exports
+    # OMP_NUM_THREADS=1 to each rank (the CPU baseline would otherwise run
+    # single-threaded at N > 1)
+    try:
+        from threadpoolctl import threadpool_limits
+        limiter = threadpool_limits(limits=threads)
+    except Exception:  # threadpoolctl absent: the environment's setting stands
+        limiter = None
+    try:
+        return _time_steps(E, L, d, dff, tokens, G, assign, steps, seed, min_seconds, max_steps, threads)
+    finally:
+        if limiter is not None:
+            limiter.restore_original_limits()
+
+
+def _time_steps(E, L, d, dff, tokens, G, assign, steps, seed, min_seconds, max_steps, threads):
     path = CpuDecodePath(E, L, d, dff, tokens, G, assign, seed)
     rng = np.random.default_rng(seed + 1)
     x = rng.standard_normal((tokens, d), dtype=np.float32)
