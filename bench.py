@@ -567,6 +567,15 @@ def main():
             a.experts, a.layers, a.d_model, a.d_ffn, a.batch * n, n, vanilla, steps=None,
             min_seconds=10.0, max_steps=5)
         cpu = {"value": tps, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+    if n > 1 and not a.no_cpu_baseline:
+        # the other ranks sleep on the rendezvous store meanwhile: waiting in
+        # the next NCCL barrier they spun a host core each, and the baseline's
+        # BLAS threads (all cores) collapsed from ~400 to ~9 tokens/s
+        store = dist.distributed_c10d._get_default_store()
+        if rank == 0:
+            store.set("exf_cpu_baseline_done", "1")
+        else:
+            store.wait(["exf_cpu_baseline_done"])
     # ---- the reference's own hot loops as GPU kernels: affinity histogram
     # (proj/src/trace.cpp:205-209) and routing replay (proj/src/sim.cpp:110-145)
     routing = None
