@@ -138,9 +138,15 @@ def main():
     z = prv[:, 15].max()
     names = ["entry", "pdl wait", "gate", "scan", "flags", "dispatch", "completion", "tables"]
     print(f"token phase rel. previous layer's last exit (prev exit min {(prv[:, 15].min() - z) / 1e3:.2f}):")
+    def rel_us(col):  # stamps never written (this mode's path skips them) -> nan
+        return np.where(col > 0, (col - z) / 1e3, np.nan)
+
     for k, nm in enumerate(names):
-        v = (cur[:, k] - z) / 1e3
-        print(f"  {nm:10s} min {v.min():7.2f} mean {v.mean():7.2f} max {v.max():7.2f}")
+        v = rel_us(cur[:, k])
+        if np.isnan(v).all():
+            print(f"  {nm:10s} (not stamped on this path)")
+            continue
+        print(f"  {nm:10s} min {np.nanmin(v):7.2f} mean {np.nanmean(v):7.2f} max {np.nanmax(v):7.2f}")
     print(f"  first MMA  min {(t[:, 2] - z).min() / 1e3:7.2f} mean {(t[:, 2] - z).mean() / 1e3:7.2f}")
     print("  dense token warp (rel. prev exit; median/max): gate %s ranks %s barrier %s published %s flag %s" % tuple(
         "%.2f/%.2f" % (np.median((cur[:, k] - z) / 1e3), ((cur[:, k] - z) / 1e3).max()) for k in (12, 13, 14, 7, 2)))
